@@ -1,0 +1,161 @@
+/*
+ * fw_capi.h — C-ABI of the B200-native variable-order fractional-Laplacian
+ * apply (the hot path of fracwave, arXiv 2311.13049 reference).
+ *
+ * Plain pointers and sizes only; no exceptions or C++/torch types cross this
+ * boundary.  Every call returns an FW_* status; fw_last_error() gives the
+ * thread-local message.  Status codes map 1:1 onto the reference's exception
+ * types in proj/include/fracwave/errors.hpp (see INTEGRATION.md for the C++
+ * shim that re-throws them).
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/proj):
+ *   fw_op_create            build_expansion(OrderField(grid, s, s0), M)   flap.hpp:24, flap.cpp:96-135
+ *                           (with OrderField validation orderfield.cpp:10-36, Grid validation grid.cpp:35-58)
+ *   fw_op_create_from_tables  uploading a host ExpansionOperator          flap.hpp:14-22
+ *   fw_apply                apply_matrix_free / _serial / apply_perturbation  flap.hpp:34-41, flap.cpp:151-168
+ *   fw_apply_device         same, device-resident buffers (no reference equivalent: the GPU-resident form)
+ *   fw_apply_batch_device   a batch of independent applies (config 5 sweep; reference runs them serially)
+ *   fw_seis_create          derive_medium + SeismicStepper ctor           seismic.cpp:11-44, 85-109
+ *   fw_seis_step            SeismicStepper::step / advance               seismic.cpp:111-137
+ *   fw_seis_get             SeismicStepper::current / n                  seismic.hpp:44-46
+ *   fw_tsfp2_*              Stepper (Method::TSFP2) ctor / step            stepping.cpp:119-138, 266-304
+ *   fw_grid_dft             Grid::dft on a real/Hermitian field           grid.cpp:134-137 (canonical FFT, test hook)
+ */
+#ifndef FW_CAPI_H
+#define FW_CAPI_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FW_CAPI_VERSION 1
+
+enum fw_status {
+  FW_OK = 0,
+  FW_E_ARG = 1,             /* invalid argument (null pointer, bad handle, bad m_first) */
+  FW_E_GRID_MISMATCH = 2,   /* fwave::GridMismatch */
+  FW_E_NEGATIVE_M = 3,      /* fwave::NegativeM */
+  FW_E_ORDER_RANGE = 4,     /* fwave::OrderOutOfRange */
+  FW_E_DEVIATION = 5,       /* fwave::DeviationTooLarge */
+  FW_E_GAMMA_RANGE = 6,     /* fwave::GammaOutOfRange */
+  FW_E_BLOWUP = 7,          /* fwave::BlowupDetected */
+  FW_E_ODD_SIZE = 8,        /* fwave::OddSize */
+  FW_E_EMPTY_INTERVAL = 9,  /* fwave::EmptyInterval */
+  FW_E_DIM_RANGE = 10,      /* fwave::DimOutOfRange */
+  FW_E_OOM = 11,            /* device allocation failed */
+  FW_E_CUDA = 12,           /* CUDA runtime error / no device */
+  FW_E_UNSUPPORTED = 13,    /* valid for the reference but not for this backend (non-power-of-two axis) */
+  FW_E_NCCL = 14            /* collective failure (slab-decomposed grids) */
+};
+
+typedef struct fw_ctx_s* fw_ctx;
+typedef struct fw_op_s* fw_op;
+typedef struct fw_seis_s* fw_seis;
+typedef struct fw_tsfp2_s* fw_tsfp2;
+
+const char* fw_last_error(void);
+int fw_version(void);
+
+/* ---- context: one CUDA device + one stream ---- */
+int fw_ctx_create(int device, fw_ctx* out);
+void fw_ctx_destroy(fw_ctx ctx);
+int fw_ctx_sync(fw_ctx ctx);
+/* the CUDA stream (cudaStream_t) all work of this context is issued on */
+void* fw_ctx_stream(fw_ctx ctx);
+/* number of kernels this context has launched so far (diagnostics / bench) */
+long long fw_ctx_launches(fw_ctx ctx);
+
+/* ---- operator: ExpansionOperator resident on the device ----
+ * grid: dim in {1,2,3}, J[dim] points per axis (even, >= 4; this backend needs
+ * powers of two), periodic [lo, hi) per axis, row-major with axis 0 slowest.
+ * order_values: s(x_j), N = prod(J) doubles.  s0_override: NULL -> serial mean
+ * (or s exactly when constant), else the given value.  M >= 0 terms. */
+int fw_op_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                 const double* order_values, const double* s0_override, int M, fw_op* out);
+
+/* Upload the tables of an existing host ExpansionOperator (flap.hpp:14-22):
+ * base_symbol[N], log_weights[M][N], deviation_powers[M][N] (row pointers).
+ * Only the Hermitian half of the spectral tables and deviation_powers[0]
+ * are uploaded; higher deviation powers are regenerated on the device with the
+ * reference recurrence (flap.cpp:131), which is bit-identical. */
+int fw_op_create_from_tables(fw_ctx ctx, int dim, const int* J, const double* lo,
+                             const double* hi, int M, double s0, int constant_order,
+                             const double* base_symbol, const double* const* log_weights,
+                             const double* const* deviation_powers, fw_op* out);
+void fw_op_destroy(fw_op op);
+
+typedef struct {
+  int dim, J[3], M, constant_order;
+  double lo[3], hi[3];
+  double s0, smin, smax;
+  size_t N, N_half;        /* grid points, Hermitian half-spectrum bins */
+  size_t device_bytes;     /* resident table bytes */
+} fw_op_info_t;
+int fw_op_info(fw_op op, fw_op_info_t* info);
+
+/* Host buffers in/out (the reference call: Field in, new Field out).
+ * m_first: 0 = apply_matrix_free, 1 = apply_perturbation.
+ * imag_residue (nullable): max |Im| of the discarded imaginary parts. */
+int fw_apply(fw_op op, const double* u_host, double* out_host, int m_first,
+             double* imag_residue);
+/* Device buffers (u_dev, out_dev: N doubles each), enqueued on the ctx stream;
+ * no synchronization.  imag_residue_dev (nullable) is a device double that
+ * receives max(|Im|) (it is max-accumulated: caller zeroes it). */
+int fw_apply_device(fw_op op, const double* u_dev, double* out_dev, int m_first,
+                    double* imag_residue_dev);
+/* nfields independent applies ops[i](u[i]) -> out[i] (device pointers); all ops
+ * must share one grid and one M. */
+int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_dev,
+                          double* const* out_dev);
+
+/* ---- fused viscoacoustic stepper (SeismicStepper) ----
+ * gamma, c0: N doubles (gamma in [0, 0.5)); derive_medium is evaluated on the
+ * host with the reference formulas (seismic.cpp:30-39), both operators built
+ * with their own s0.  phi, psi: initial field and velocity. */
+int fw_seis_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                   const double* gamma, const double* c0, double omega0, int M,
+                   const double* phi, const double* psi, double tau, double blowup_factor,
+                   fw_seis* out);
+void fw_seis_destroy(fw_seis s);
+/* nsteps calls of step().  Blow-up is detected on the device; on FW_E_BLOWUP
+ * the state is the one before the offending step and n() is the offending step
+ * (as after the reference's throw, seismic.cpp:124-129). */
+int fw_seis_step(fw_seis s, int nsteps);
+/* enqueue nsteps without checking for blow-up (the check happens at the next
+ * fw_seis_step / fw_seis_get); for timing loops. */
+int fw_seis_enqueue(fw_seis s, int nsteps);
+/* current() -> cur_host (N), optional prev / atten_prev, n */
+int fw_seis_get(fw_seis s, double* cur_host, double* prev_host, double* atten_prev_host,
+                long* n);
+/* overwrite the current wavefield from host memory (host-owned state between
+ * steps: source injection / receivers), then the caller steps on. */
+int fw_seis_set_current(fw_seis s, const double* cur_host);
+/* device pointer of the current wavefield (valid until the next step) */
+const double* fw_seis_current_device(fw_seis s);
+/* the two operators, for diagnostics */
+int fw_seis_ops(fw_seis s, fw_op* disp, fw_op* atten);
+int fw_seis_medium(fw_seis s, double* c, double* eta, double* tau_coef);
+
+/* ---- TSFP2 time-splitting stepper (Stepper, Method::TSFP2) ----
+ * f: 0 = none, 1 = cubic u^3. */
+int fw_tsfp2_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                    const double* order_values, int M, double kappa, int f_kind,
+                    const double* phi, const double* psi, double tau, fw_tsfp2* out);
+void fw_tsfp2_destroy(fw_tsfp2 t);
+int fw_tsfp2_step(fw_tsfp2 t, int nsteps);
+int fw_tsfp2_get(fw_tsfp2 t, double* u_host, double* v_host, long* n);
+
+/* ---- canonical transforms (test hooks) ----
+ * forward: real x[N] -> half spectrum H[N_half] (interleaved re,im), unscaled;
+ * backward: H -> real x (unnormalized C2R). */
+int fw_rfftn(fw_ctx ctx, int dim, const int* J, const double* x_host, double* H_host);
+int fw_irfftn(fw_ctx ctx, int dim, const int* J, const double* H_host, double* x_host);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

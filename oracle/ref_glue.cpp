@@ -9,6 +9,8 @@
 // expr.cpp:20-29); seismic.cpp is therefore not linked separately.
 #include "src/seismic.cpp"
 
+#include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -18,6 +20,7 @@
 #include "fracwave/errors.hpp"
 #include "fracwave/flap.hpp"
 #include "fracwave/grid.hpp"
+#include "fracwave/harness.hpp"
 #include "fracwave/orderfield.hpp"
 #include "fracwave/seismic.hpp"
 #include "fracwave/stepping.hpp"
@@ -213,6 +216,54 @@ int ref_lffp(int d, const int* J, const double* lo, const double* hi, const doub
     Stepper st(p, cfg);
     for (int i = 0; i < nsteps; ++i) st.step();
     std::memcpy(u_out, st.current().values().data(), N * sizeof(double));
+  });
+}
+
+// CPU-baseline timers, following the reference's own drivers: best-of-`repeats`
+// steady_clock around apply_matrix_free (bench_kernels.cpp:22-31,
+// harness.cpp:407-415) and the mean per step over SeismicStepper::step() after
+// construction (construction = 3 applies, untimed).
+int ref_time_apply(int d, const int* J, const double* lo, const double* hi, const double* s, int M,
+                   const double* u, int repeats, double* best_seconds) {
+  return guard([&] {
+    Grid g = make_grid(d, J, lo, hi);
+    const std::size_t N = g.total();
+    ExpansionOperator op = build_expansion(OrderField(g, vec(s, N)), M);
+    Field uf(g, vec(u, N));
+    double best = 1e300;
+    for (int r = 0; r < repeats; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      Field out = apply_matrix_free(op, uf);
+      const auto t1 = std::chrono::steady_clock::now();
+      best = std::min(best, std::chrono::duration<double>(t1 - t0).count());
+    }
+    *best_seconds = best;
+  });
+}
+
+int ref_time_seismic(int d, const int* J, const double* lo, const double* hi, const double* gamma,
+                     const double* c0, double omega0, int M, const double* phi, const double* psi,
+                     double tau, int warmup, int steps, double* per_step_seconds, double* cur_out) {
+  return guard([&] {
+    Grid g = make_grid(d, J, lo, hi);
+    const std::size_t N = g.total();
+    SeismicMedium m = derive_medium(g, vec(gamma, N), vec(c0, N), omega0, M);
+    SeismicStepper st(m, Field(g, vec(phi, N)), Field(g, vec(psi, N)), tau);
+    for (int i = 0; i < warmup; ++i) st.step();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < steps; ++i) st.step();
+    const auto t1 = std::chrono::steady_clock::now();
+    *per_step_seconds = std::chrono::duration<double>(t1 - t0).count() / std::max(steps, 1);
+    if (cur_out) std::memcpy(cur_out, st.current().values().data(), N * sizeof(double));
+  });
+}
+
+// write_snapshot (harness.cpp:541-557): FWS1 files written by the reference itself
+int ref_write_snapshot(int d, const int* J, const double* lo, const double* hi, const double* values,
+                       double time, const char* path) {
+  return guard([&] {
+    Grid g = make_grid(d, J, lo, hi);
+    write_snapshot(Field(g, vec(values, g.total())), time, path);
   });
 }
 

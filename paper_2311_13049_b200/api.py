@@ -1,0 +1,404 @@
+"""Reference-shaped host API over the C-ABI (see package docstring).
+
+Names, argument meaning and error behaviour follow fracwave's C++ API:
+Grid (grid.hpp:20-59), OrderField (orderfield.hpp:13-29), build_expansion /
+apply_matrix_free / apply_perturbation (flap.hpp:14-41), SeismicMedium /
+build_medium / SeismicStepper (seismic.hpp:13-55), Stepper TSFP2
+(stepping.hpp:72-104).  Fields are numpy float64 arrays of the grid's shape
+(row-major, axis 0 slowest, as the reference's Field).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import DimOutOfRange, EmptyInterval, GridMismatch, OddSize, check, load_library
+
+_dp = C.POINTER(C.c_double)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _f64(a, n: Optional[int] = None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if n is not None and a.size != n:
+        raise GridMismatch(f"field length {a.size} does not match grid point count {n}")
+    return a
+
+
+class Context:
+    """One CUDA device + stream (fw_ctx)."""
+
+    def __init__(self, device: int = 0):
+        lib = load_library()
+        h = C.c_void_p()
+        check(lib.fw_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def sync(self):
+        check(load_library().fw_ctx_sync(self._h))
+
+    @property
+    def stream(self) -> int:
+        return int(load_library().fw_ctx_stream(self._h) or 0)
+
+    def launches(self) -> int:
+        return int(load_library().fw_ctx_launches(self._h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().fw_ctx_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+_default: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+class Grid:
+    """Periodic tensor-product grid (grid.cpp:35-58 validation)."""
+
+    def __init__(self, bounds: Sequence[Sequence[float]], sizes: Sequence[int]):
+        if len(bounds) != len(sizes):
+            raise DimOutOfRange("bounds and sizes length mismatch")
+        d = len(bounds)
+        if d < 1 or d > 3:
+            raise DimOutOfRange(f"dimension must be 1, 2 or 3, got {d}")
+        for m, (J, (a, b)) in enumerate(zip(sizes, bounds)):
+            if J < 4 or J % 2 != 0:
+                raise OddSize(f"axis {m}: point count {J} must be even and >= 4")
+            if not (b > a):
+                raise EmptyInterval(f"axis {m}: empty interval")
+        self.dim = d
+        self.sizes = tuple(int(J) for J in sizes)
+        self.lo = tuple(float(a) for a, _ in bounds)
+        self.hi = tuple(float(b) for _, b in bounds)
+
+    @property
+    def shape(self):
+        return self.sizes
+
+    def total(self) -> int:
+        return int(np.prod(self.sizes))
+
+    def size(self, axis: int) -> int:
+        return self.sizes[axis]
+
+    def step(self, axis: int) -> float:
+        return (self.hi[axis] - self.lo[axis]) / self.sizes[axis]
+
+    def same_as(self, other: "Grid") -> bool:
+        return self.sizes == other.sizes and self.lo == other.lo and self.hi == other.hi
+
+    def coords(self):
+        """Per-axis coordinate vectors a + j h (Grid::point, grid.cpp:107-116)."""
+        return [self.lo[m] + np.arange(self.sizes[m]) * self.step(m) for m in range(self.dim)]
+
+    def mesh(self):
+        return np.meshgrid(*self.coords(), indexing="ij")
+
+    def _carrays(self):
+        J = (C.c_int * 3)(*(list(self.sizes) + [1] * (3 - self.dim)))
+        lo = (C.c_double * 3)(*(list(self.lo) + [0.0] * (3 - self.dim)))
+        hi = (C.c_double * 3)(*(list(self.hi) + [1.0] * (3 - self.dim)))
+        return J, lo, hi
+
+
+def build_grid(bounds, sizes) -> Grid:
+    return Grid(bounds, sizes)
+
+
+class OrderField:
+    """Sampled s(x) with optional s0 override.  Validation (range, deviation) is
+    performed when the operator is built, exactly as orderfield.cpp:10-36."""
+
+    def __init__(self, grid: Grid, values, s0_override: Optional[float] = None):
+        self.grid = grid
+        self.values = _f64(values, grid.total()).reshape(grid.shape)
+        self.s0_override = s0_override
+
+
+class ExpansionOperator:
+    """Device-resident M-term operator (fw_op)."""
+
+    def __init__(self, handle, grid: Grid, ctx: Context, order: Optional[OrderField] = None):
+        self._h = handle
+        self.grid = grid
+        self.ctx = ctx
+        self.order = order
+        info = _capi.OpInfo()
+        check(load_library().fw_op_info(handle, C.byref(info)))
+        self.M = info.M
+        self.constant_order = bool(info.constant_order)
+        self.s0 = info.s0
+        self.smin, self.smax = info.smin, info.smax
+        self.N, self.N_half = info.N, info.N_half
+        self.device_bytes = info.device_bytes
+
+    @property
+    def handle(self):
+        return self._h
+
+    @classmethod
+    def from_tables(cls, grid: Grid, M: int, s0: float, constant_order: bool, base_symbol,
+                    log_weights, deviation_powers, ctx: Optional[Context] = None):
+        """Upload a host ExpansionOperator's tables (flap.hpp:14-22)."""
+        ctx = ctx or default_context()
+        N = grid.total()
+        base = _f64(base_symbol, N)
+        lw = [_f64(r, N) for r in log_weights]
+        dv = [_f64(r, N) for r in deviation_powers]
+        lwp = (_dp * max(M, 1))(*[_ptr(r) for r in lw])
+        dvp = (_dp * max(M, 1))(*[_ptr(r) for r in dv])
+        J, lo, hi = grid._carrays()
+        h = C.c_void_p()
+        check(load_library().fw_op_create_from_tables(ctx.handle, grid.dim, J, lo, hi, int(M), float(s0),
+                                                      int(bool(constant_order)), _ptr(base), lwp, dvp,
+                                                      C.byref(h)))
+        return cls(h, grid, ctx)
+
+    def apply(self, u, m_first: int = 0, residue: bool = False):
+        u = _f64(u, self.N)
+        out = np.empty(self.grid.shape, dtype=np.float64)
+        res = C.c_double(0.0)
+        check(load_library().fw_apply(self._h, _ptr(u), _ptr(out), int(m_first),
+                                      C.byref(res) if residue else None))
+        return (out, res.value) if residue else out
+
+    def apply_device(self, u_ptr: int, out_ptr: int, m_first: int = 0, residue_ptr: int = 0):
+        """Device pointers (e.g. torch.Tensor.data_ptr()), enqueued on the context stream."""
+        check(load_library().fw_apply_device(self._h, C.c_void_p(u_ptr), C.c_void_p(out_ptr), int(m_first),
+                                             C.c_void_p(residue_ptr) if residue_ptr else None))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().fw_op_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def build_expansion(order: OrderField, M: int, ctx: Optional[Context] = None) -> ExpansionOperator:
+    """build_expansion (flap.cpp:96-135): NegativeM / OrderOutOfRange / DeviationTooLarge."""
+    ctx = ctx or default_context()
+    g = order.grid
+    J, lo, hi = g._carrays()
+    s0 = C.c_double(order.s0_override) if order.s0_override is not None else None
+    h = C.c_void_p()
+    check(load_library().fw_op_create(ctx.handle, g.dim, J, lo, hi, _ptr(order.values),
+                                      C.byref(s0) if s0 is not None else None, int(M), C.byref(h)))
+    return ExpansionOperator(h, g, ctx, order)
+
+
+def _check_field(op: ExpansionOperator, u):
+    if hasattr(u, "grid") and not u.grid.same_as(op.grid):
+        raise GridMismatch("field defined on a different grid than the operator")
+    arr = np.asarray(u, dtype=np.float64)
+    if arr.size != op.N:
+        raise GridMismatch("field defined on a different grid than the operator")
+    return arr
+
+
+def apply_matrix_free(op: ExpansionOperator, u, residue: bool = False):
+    """flap.cpp:151-154 — returns L u (and the imaginary residue when asked)."""
+    return op.apply(_check_field(op, u), 0, residue)
+
+
+def apply_matrix_free_serial(op: ExpansionOperator, u, residue: bool = False):
+    """flap.cpp:156-159 — the device reduction order is fixed (ascending m), so the
+    serial and parallel entry points are the same computation."""
+    return op.apply(_check_field(op, u), 0, residue)
+
+
+def apply_perturbation(op: ExpansionOperator, u, residue: bool = False):
+    """flap.cpp:161-168 — terms m = 1..M (exact zeros for a constant order)."""
+    return op.apply(_check_field(op, u), 1, residue)
+
+
+class SeismicMedium:
+    """Inputs of derive_medium (seismic.cpp:11-44); the coefficient fields and the
+    two operators are built on the device by SeismicStepper."""
+
+    def __init__(self, grid: Grid, gamma, c0, omega0: float, M: int):
+        self.grid = grid
+        self.gamma = _f64(gamma, grid.total()).reshape(grid.shape)
+        c0 = np.broadcast_to(np.asarray(c0, dtype=np.float64), grid.shape)
+        self.c0 = np.ascontiguousarray(c0)
+        self.omega0 = float(omega0)
+        self.M = int(M)
+        bad = ~((self.gamma >= 0.0) & (self.gamma < 0.5))
+        if bad.any():
+            from ._capi import GammaOutOfRange
+            raise GammaOutOfRange(f"gamma = {self.gamma[bad].flat[0]} outside [0, 0.5)")
+
+
+def build_medium(grid: Grid, gamma, c0, omega0: float, M: int) -> SeismicMedium:
+    return SeismicMedium(grid, gamma, c0, omega0, M)
+
+
+class SeismicStepper:
+    """Explicit two-level viscoacoustic stepper (seismic.cpp:85-142), state resident
+    on the device, both operator applies and the update fused per step."""
+
+    def __init__(self, medium: SeismicMedium, phi, psi, tau: float, blowup_factor: float = 1e8,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.medium = medium
+        g = medium.grid
+        self.grid = g
+        N = g.total()
+        phi = _f64(phi, N)
+        psi = _f64(psi, N)
+        J, lo, hi = g._carrays()
+        h = C.c_void_p()
+        check(load_library().fw_seis_create(self.ctx.handle, g.dim, J, lo, hi, _ptr(medium.gamma),
+                                            _ptr(medium.c0), medium.omega0, medium.M, _ptr(phi), _ptr(psi),
+                                            float(tau), float(blowup_factor), C.byref(h)))
+        self._h = h
+        self.tau = float(tau)
+
+    def step(self):
+        check(load_library().fw_seis_step(self._h, 1))
+
+    def advance(self, steps: int):
+        check(load_library().fw_seis_step(self._h, int(steps)))
+
+    def enqueue(self, steps: int):
+        check(load_library().fw_seis_enqueue(self._h, int(steps)))
+
+    def advance_to(self, t_final: float):
+        target = int(round(t_final / self.tau))  # std::lround (seismic.cpp:140)
+        k = target - self.n()
+        if k > 0:
+            self.advance(k)
+
+    def current(self):
+        out = np.empty(self.grid.shape)
+        check(load_library().fw_seis_get(self._h, _ptr(out), None, None, None))
+        return out
+
+    def state(self):
+        """(cur, prev, atten_prev, n)"""
+        cur, prev, ap = (np.empty(self.grid.shape) for _ in range(3))
+        n = C.c_long(0)
+        check(load_library().fw_seis_get(self._h, _ptr(cur), _ptr(prev), _ptr(ap), C.byref(n)))
+        return cur, prev, ap, n.value
+
+    def set_current(self, cur):
+        cur = _f64(cur, self.grid.total())
+        check(load_library().fw_seis_set_current(self._h, _ptr(cur)))
+
+    def n(self) -> int:
+        n = C.c_long(0)
+        check(load_library().fw_seis_get(self._h, None, None, None, C.byref(n)))
+        return n.value
+
+    def time(self) -> float:
+        return self.n() * self.tau
+
+    def coefficients(self):
+        c, eta, tc = (np.empty(self.grid.shape) for _ in range(3))
+        check(load_library().fw_seis_medium(self._h, _ptr(c), _ptr(eta), _ptr(tc)))
+        return c, eta, tc
+
+    def operators(self):
+        d, a = C.c_void_p(), C.c_void_p()
+        check(load_library().fw_seis_ops(self._h, C.byref(d), C.byref(a)))
+        info = []
+        for h in (d, a):
+            i = _capi.OpInfo()
+            check(load_library().fw_op_info(h, C.byref(i)))
+            info.append(i)
+        return info
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().fw_seis_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+class TSFP2Stepper:
+    """Strang time splitting (stepping.cpp:119-138, 266-304) for
+    u_tt = -kappa (-Delta)^{s(x)} u + f(u), f in {none, cubic}."""
+
+    def __init__(self, order: OrderField, M: int, kappa: float, phi, psi, tau: float, f: str = "none",
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        g = order.grid
+        self.grid = g
+        N = g.total()
+        J, lo, hi = g._carrays()
+        h = C.c_void_p()
+        check(load_library().fw_tsfp2_create(self.ctx.handle, g.dim, J, lo, hi, _ptr(order.values), int(M),
+                                             float(kappa), 1 if f == "cubic" else 0, _ptr(_f64(phi, N)),
+                                             _ptr(_f64(psi, N)), float(tau), C.byref(h)))
+        self._h = h
+        self.tau = float(tau)
+
+    def advance(self, steps: int):
+        check(load_library().fw_tsfp2_step(self._h, int(steps)))
+
+    def step(self):
+        self.advance(1)
+
+    def current(self):
+        return self.state()[0]
+
+    def velocity(self):
+        return self.state()[1]
+
+    def state(self):
+        u, v = np.empty(self.grid.shape), np.empty(self.grid.shape)
+        check(load_library().fw_tsfp2_get(self._h, _ptr(u), _ptr(v), None))
+        return u, v
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().fw_tsfp2_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def rfftn(x, ctx: Optional[Context] = None):
+    """Canonical forward real transform on the device (unscaled half spectrum)."""
+    ctx = ctx or default_context()
+    x = _f64(x)
+    shape = x.shape
+    J = (C.c_int * 3)(*(list(shape) + [1] * (3 - len(shape))))
+    H = np.empty(shape[:-1] + (shape[-1] // 2 + 1,), dtype=np.complex128)
+    check(load_library().fw_rfftn(ctx.handle, len(shape), J, _ptr(x), H.view(np.float64).ctypes.data_as(_dp)))
+    return H
+
+
+def irfftn(H, shape, ctx: Optional[Context] = None):
+    """Canonical unnormalized C2R on the device."""
+    ctx = ctx or default_context()
+    H = np.ascontiguousarray(H, dtype=np.complex128)
+    J = (C.c_int * 3)(*(list(shape) + [1] * (3 - len(shape))))
+    x = np.empty(tuple(shape))
+    check(load_library().fw_irfftn(ctx.handle, len(shape), J, H.view(np.float64).ctypes.data_as(_dp), _ptr(x)))
+    return x

@@ -1,0 +1,885 @@
+// fw_capi.cu — implementation of include/fw_capi.h.
+//
+// Host-side setup restates the reference's table construction exactly
+// (Grid |mu|^2 grid.cpp:60-80, OrderField s0 orderfield.cpp:10-36,
+// build_expansion flap.cpp:96-135, derive_medium seismic.cpp:11-44) with the
+// same glibc pow/log/cos/sin calls, so the device tables are bit-identical to
+// the reference's.  Transcendentals are evaluated on the host once per
+// operator on the Hermitian half; the M-fold recurrences run on the device
+// (IEEE mul/div: bit-identical).  There is no CPU compute fallback: every
+// apply runs the sm_100a kernels in fw_kernels.cu.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/fw_capi.h"
+#include "fw_fft.cuh"
+#include "fw_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define FW_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      return set_err(e_ == cudaErrorMemoryAllocation ? FW_E_OOM : FW_E_CUDA,           \
+                     std::string(#call) + ": " + cudaGetErrorString(e_));             \
+    }                                                                                   \
+  } while (0)
+
+#define FW_TRY(expr)               \
+  do {                             \
+    int rc_ = (expr);              \
+    if (rc_ != FW_OK) return rc_;  \
+  } while (0)
+
+// ---- twiddles: same definition as oracle/fwshim/fwcanon.c fwc_twiddle ----
+void twiddle(long t, long n, double* c, double* s) {
+  t %= n;
+  if (t < 0) t += n;
+  if (t == 0) {
+    *c = 1.0;
+    *s = 0.0;
+    return;
+  }
+  const long quarter = n / 4;
+  const long q = t / quarter;
+  const long tq = t - q * quarter;
+  double cc, ss;
+  if (tq == 0) {
+    cc = 1.0;
+    ss = 0.0;
+  } else if (8 * tq <= n) {
+    const double ang = (2.0 * M_PI) * ((double)tq / (double)n);
+    cc = cos(ang);
+    ss = sin(ang);
+  } else {
+    const long tr = quarter - tq;
+    const double ang = (2.0 * M_PI) * ((double)tr / (double)n);
+    cc = sin(ang);
+    ss = cos(ang);
+  }
+  switch (q) {
+    case 0: *c = cc; *s = ss; break;
+    case 1: *c = -ss; *s = cc; break;
+    case 2: *c = -cc; *s = -ss; break;
+    default: *c = ss; *s = -cc; break;
+  }
+}
+
+bool is_pow2(long n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+// Grid::Grid validation (grid.cpp:35-58) + this backend's size support
+int check_grid(int dim, const int* J, const double* lo, const double* hi, fw::GridGeom* g) {
+  if (!J) return set_err(FW_E_ARG, "null size array");
+  if (dim < 1 || dim > 3) return set_err(FW_E_DIM_RANGE, "dimension must be 1, 2 or 3, got " + std::to_string(dim));
+  for (int m = 0; m < dim; ++m) {
+    if (J[m] < 4 || J[m] % 2 != 0)
+      return set_err(FW_E_ODD_SIZE, "axis " + std::to_string(m) + ": point count " + std::to_string(J[m]) +
+                                        " must be even and >= 4");
+    if (lo && hi && !(hi[m] > lo[m])) return set_err(FW_E_EMPTY_INTERVAL, "axis " + std::to_string(m) + ": empty interval");
+  }
+  for (int m = 0; m < dim; ++m)
+    if (!is_pow2(J[m]) || J[m] > 4096)
+      return set_err(FW_E_UNSUPPORTED, "axis " + std::to_string(m) + ": this backend needs a power of two in [4, 4096], got " +
+                                           std::to_string(J[m]));
+  g->d = dim;
+  g->N = 1;
+  for (int m = 0; m < 3; ++m) g->J[m] = m < dim ? J[m] : 1;
+  for (int m = 0; m < dim; ++m) g->N *= (size_t)J[m];
+  g->nl = J[dim - 1];
+  g->hp1 = g->nl / 2 + 1;
+  g->rows = g->N / (size_t)g->nl;
+  g->Nh = g->rows * (size_t)g->hp1;
+  return FW_OK;
+}
+
+// |mu|^2 on the Hermitian half, summed m = d-1 .. 0 (grid.cpp:60-80)
+std::vector<double> half_mu2(const fw::GridGeom& g, const double* lo, const double* hi) {
+  std::vector<std::vector<double>> ax(g.d);
+  for (int m = 0; m < g.d; ++m) {
+    ax[m].resize(g.J[m]);
+    const double base = 2.0 * M_PI / (hi[m] - lo[m]);
+    for (int p = 0; p < g.J[m]; ++p) {
+      const int k = (p < g.J[m] / 2) ? p : p - g.J[m];
+      ax[m][p] = (base * k) * (base * k);
+    }
+  }
+  std::vector<double> out(g.Nh);
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < (long long)g.Nh; ++i) {
+    int idx[3] = {0, 0, 0};
+    idx[g.d - 1] = (int)(i % g.hp1);
+    long long rem = i / g.hp1;
+    for (int m = g.d - 2; m >= 0; --m) {
+      idx[m] = (int)(rem % g.J[m]);
+      rem /= g.J[m];
+    }
+    double v = 0.0;
+    for (int m = g.d - 1; m >= 0; --m) v += ax[m][idx[m]];
+    out[i] = v;
+  }
+  return out;
+}
+
+// OrderField (orderfield.cpp:10-36) + is_constant (orderfield.cpp:55-57)
+int order_stats(const double* s, size_t N, const double* s0_override, double* s0, double* smin, double* smax,
+                int* constant) {
+  if (!s) return set_err(FW_E_ARG, "null order values");
+  double mn = s[0], mx = s[0];
+  for (size_t i = 1; i < N; ++i) {
+    if (s[i] < mn) mn = s[i];
+    if (mx < s[i]) mx = s[i];
+  }
+  if (!(mn > 0.0) || !(mx < 2.0)) {
+    char b[160];
+    snprintf(b, sizeof b, "order range [%f, %f] outside (0, 2)", mn, mx);
+    return set_err(FW_E_ORDER_RANGE, b);
+  }
+  double z;
+  if (s0_override) {
+    z = *s0_override;
+  } else if (mn == mx) {
+    z = mn;
+  } else {
+    double sum = 0.0;
+    for (size_t i = 0; i < N; ++i) sum += s[i];
+    z = sum / (double)N;
+  }
+  const double dev = std::max(std::fabs(mn - z), std::fabs(mx - z));
+  if (dev >= 1.0) {
+    char b[160];
+    snprintf(b, sizeof b, "max |s(x) - s0| = %f >= 1; expansion would diverge", dev);
+    return set_err(FW_E_DEVIATION, b);
+  }
+  *s0 = z;
+  *smin = mn;
+  *smax = mx;
+  *constant = (mx - mn <= 1e-14) ? 1 : 0;
+  return FW_OK;
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(FW_E_OOM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed: " +
+                                 cudaGetErrorString(e));
+  }
+  return FW_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+
+struct fw_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  double2* master = nullptr;
+  long long launches = 0;
+  // grow-only scratch slots (single stream: ops on one ctx run in order)
+  void* scratch[8] = {};
+  size_t scratch_bytes[8] = {};
+  double* residue = nullptr;  // device scalar
+  fw::LaunchCtx L() { return fw::LaunchCtx{stream, master, &launches}; }
+  int get_scratch(int slot, size_t bytes, void** out) {
+    if (scratch_bytes[slot] < bytes) {
+      if (scratch[slot]) cudaFree(scratch[slot]);
+      scratch[slot] = nullptr;
+      scratch_bytes[slot] = 0;
+      cudaError_t e = cudaMalloc(&scratch[slot], bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(FW_E_OOM, "scratch allocation of " + std::to_string(bytes) + " bytes failed");
+      }
+      scratch_bytes[slot] = bytes;
+    }
+    *out = scratch[slot];
+    return FW_OK;
+  }
+};
+
+enum { SLOT_UH = 0, SLOT_T = 1, SLOT_U = 2, SLOT_OUT = 3, SLOT_TMP = 4, SLOT_UH2 = 5 };
+
+struct fw_op_s {
+  fw_ctx ctx = nullptr;
+  fw::GridGeom g;
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  int M = 0;
+  int constant_order = 0;
+  double s0 = 0, smin = 0, smax = 0;
+  double* w = nullptr;     // (M+1) x Nh
+  double* dev1 = nullptr;  // N
+  size_t bytes = 0;
+};
+
+extern "C" {
+
+const char* fw_last_error(void) { return g_err.c_str(); }
+int fw_version(void) { return FW_CAPI_VERSION; }
+
+int fw_ctx_create(int device, fw_ctx* out) {
+  if (!out) return set_err(FW_E_ARG, "null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return set_err(FW_E_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+  }
+  if (device < 0 || device >= n) return set_err(FW_E_ARG, "device index out of range");
+  FW_CUDA(cudaSetDevice(device));
+  fw_ctx c = new fw_ctx_s();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return set_err(FW_E_CUDA, "stream creation failed");
+  }
+  std::vector<double2> tw(fw::kTwMaster);
+  for (int t = 0; t < fw::kTwMaster; ++t) twiddle(t, fw::kTwMaster, &tw[t].x, &tw[t].y);
+  if (dalloc(&c->master, tw.size()) || dalloc(&c->residue, 1)) {
+    fw_ctx_destroy(c);
+    return FW_E_OOM;
+  }
+  FW_CUDA(cudaMemcpy(c->master, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  fw::init_kernels();
+  *out = c;
+  return FW_OK;
+}
+
+void fw_ctx_destroy(fw_ctx c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->scratch)
+    if (p) cudaFree(p);
+  if (c->master) cudaFree(c->master);
+  if (c->residue) cudaFree(c->residue);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int fw_ctx_sync(fw_ctx c) {
+  if (!c) return set_err(FW_E_ARG, "null ctx");
+  FW_CUDA(cudaStreamSynchronize(c->stream));
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+void* fw_ctx_stream(fw_ctx c) { return c ? (void*)c->stream : nullptr; }
+long long fw_ctx_launches(fw_ctx c) { return c ? c->launches : 0; }
+
+}  // extern "C"
+
+namespace {
+
+int op_alloc_common(fw_ctx ctx, const fw::GridGeom& g, const double* lo, const double* hi, int M, fw_op* out,
+                    fw_op_s** o) {
+  if (M < 0) return set_err(FW_E_NEGATIVE_M, "truncation count M must be >= 0");
+  fw_op_s* op = new fw_op_s();
+  op->ctx = ctx;
+  op->g = g;
+  for (int m = 0; m < g.d; ++m) {
+    op->lo[m] = lo[m];
+    op->hi[m] = hi[m];
+  }
+  op->M = M;
+  if (dalloc(&op->w, (size_t)(M + 1) * g.Nh) || dalloc(&op->dev1, g.N)) {
+    fw_op_destroy(op);
+    return FW_E_OOM;
+  }
+  op->bytes = ((size_t)(M + 1) * g.Nh + g.N) * sizeof(double);
+  *o = op;
+  (void)out;
+  return FW_OK;
+}
+
+int op_create_internal(fw_ctx ctx, const fw::GridGeom& g, const double* lo, const double* hi, const double* s,
+                       const double* s0_override, int M, fw_op* out) {
+  double s0, smin, smax;
+  int constant;
+  FW_TRY(order_stats(s, g.N, s0_override, &s0, &smin, &smax, &constant));
+  fw_op_s* op = nullptr;
+  FW_TRY(op_alloc_common(ctx, g, lo, hi, M, out, &op));
+  op->s0 = s0;
+  op->smin = smin;
+  op->smax = smax;
+  op->constant_order = constant;
+  // flap.cpp:108-122 transcendentals on the host half spectrum
+  std::vector<double> mu2 = half_mu2(g, lo, hi);
+  std::vector<double> base(g.Nh), logm(g.Nh);
+#pragma omp parallel for schedule(static)
+  for (long long k = 0; k < (long long)g.Nh; ++k) {
+    base[k] = mu2[k] > 0.0 ? pow(mu2[k], s0) : 0.0;
+    logm[k] = mu2[k] > 0.0 ? log(mu2[k]) : 0.0;
+  }
+  auto L = ctx->L();
+  double *d_mu2 = nullptr, *d_base = nullptr, *d_logm = nullptr, *d_s = nullptr;
+  int rc = FW_OK;
+  if ((rc = dalloc(&d_mu2, g.Nh)) || (rc = dalloc(&d_base, g.Nh)) || (rc = dalloc(&d_logm, g.Nh)) ||
+      (rc = dalloc(&d_s, g.N))) {
+    cudaFree(d_mu2); cudaFree(d_base); cudaFree(d_logm); cudaFree(d_s);
+    fw_op_destroy(op);
+    return rc;
+  }
+  cudaMemcpyAsync(d_mu2, mu2.data(), g.Nh * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(d_base, base.data(), g.Nh * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(d_logm, logm.data(), g.Nh * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(d_s, s, g.N * 8, cudaMemcpyHostToDevice, ctx->stream);
+  fw::launch_build_weights(L, g.Nh, M, d_mu2, d_base, d_logm, op->w);
+  fw::launch_dev1(L, g.N, d_s, s0, op->dev1);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d_mu2); cudaFree(d_base); cudaFree(d_logm); cudaFree(d_s);
+  if (e != cudaSuccess) {
+    fw_op_destroy(op);
+    return set_err(FW_E_CUDA, std::string("table construction: ") + cudaGetErrorString(e));
+  }
+  *out = op;
+  return FW_OK;
+}
+
+// out = A(u) for device pointers, enqueued
+int apply_device(fw_op op, const double* u, double* out, int m_first, double* residue, const int* guard,
+                 const double2* Uh_pre = nullptr) {
+  fw_ctx ctx = op->ctx;
+  const fw::GridGeom& g = op->g;
+  if (m_first < 0 || m_first > 1) return set_err(FW_E_ARG, "m_first must be 0 or 1");
+  const int m_last = op->constant_order ? 0 : op->M;
+  auto L = ctx->L();
+  if (m_first > m_last) {  // perturbation of a constant-order operator: exact zero (flap.cpp:163-166)
+    FW_CUDA(cudaMemsetAsync(out, 0, g.N * sizeof(double), ctx->stream));
+    return FW_OK;
+  }
+  void* uh = nullptr;
+  const double2* Uh = Uh_pre;
+  if (!Uh) {
+    FW_TRY(ctx->get_scratch(SLOT_UH, g.Nh * sizeof(double2), &uh));
+    fw::launch_forward(L, g, u, (double2*)uh, true);
+    Uh = (const double2*)uh;
+  }
+  void* T = nullptr;
+  if (g.d >= 2) FW_TRY(ctx->get_scratch(SLOT_T, (size_t)(m_last - m_first + 1) * g.Nh * sizeof(double2), &T));
+  fw::InverseArgs a{Uh, op->w, op->dev1, (double2*)T, out, m_first, m_last, residue, guard};
+  fw::launch_inverse(L, g, a);
+  return FW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fw_op_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                 const double* order_values, const double* s0_override, int M, fw_op* out) {
+  if (!ctx || !out || !lo || !hi) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, lo, hi, &g));
+  FW_CUDA(cudaSetDevice(ctx->device));
+  return op_create_internal(ctx, g, lo, hi, order_values, s0_override, M, out);
+}
+
+int fw_op_create_from_tables(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi, int M,
+                             double s0, int constant_order, const double* base_symbol,
+                             const double* const* log_weights, const double* const* deviation_powers,
+                             fw_op* out) {
+  if (!ctx || !out || !lo || !hi || !base_symbol) return set_err(FW_E_ARG, "null argument");
+  if (M > 0 && (!log_weights || !deviation_powers)) return set_err(FW_E_ARG, "null table rows");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, lo, hi, &g));
+  FW_CUDA(cudaSetDevice(ctx->device));
+  fw_op_s* op = nullptr;
+  FW_TRY(op_alloc_common(ctx, g, lo, hi, M, out, &op));
+  op->s0 = s0;
+  op->constant_order = constant_order ? 1 : 0;
+  // gather the Hermitian half of the spectral tables (row r, bin q -> full index r*nl + q)
+  std::vector<double> base(g.Nh), lw((size_t)std::max(M, 1) * g.Nh);
+  for (size_t r = 0; r < g.rows; ++r)
+    for (int q = 0; q < g.hp1; ++q) {
+      const size_t hi_ = r * g.hp1 + q, fi = r * (size_t)g.nl + q;
+      base[hi_] = base_symbol[fi];
+      for (int m = 0; m < M; ++m) lw[(size_t)m * g.Nh + hi_] = log_weights[m][fi];
+    }
+  double *d_base = nullptr, *d_lw = nullptr;
+  int rc = FW_OK;
+  if ((rc = dalloc(&d_base, g.Nh)) || (rc = dalloc(&d_lw, lw.size()))) {
+    cudaFree(d_base); cudaFree(d_lw);
+    fw_op_destroy(op);
+    return rc;
+  }
+  auto L = ctx->L();
+  cudaMemcpyAsync(d_base, base.data(), g.Nh * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(d_lw, lw.data(), lw.size() * 8, cudaMemcpyHostToDevice, ctx->stream);
+  fw::launch_weights_from_lw(L, g.Nh, M, d_base, d_lw, op->w);
+  if (M > 0) {
+    cudaMemcpyAsync(op->dev1, deviation_powers[0], g.N * 8, cudaMemcpyHostToDevice, ctx->stream);
+  } else {
+    cudaMemsetAsync(op->dev1, 0, g.N * 8, ctx->stream);
+  }
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d_base); cudaFree(d_lw);
+  if (e != cudaSuccess) {
+    fw_op_destroy(op);
+    return set_err(FW_E_CUDA, std::string("table upload: ") + cudaGetErrorString(e));
+  }
+  op->smin = op->smax = NAN;
+  *out = op;
+  return FW_OK;
+}
+
+void fw_op_destroy(fw_op op) {
+  if (!op) return;
+  if (op->w) cudaFree(op->w);
+  if (op->dev1) cudaFree(op->dev1);
+  delete op;
+}
+
+int fw_op_info(fw_op op, fw_op_info_t* info) {
+  if (!op || !info) return set_err(FW_E_ARG, "null argument");
+  memset(info, 0, sizeof(*info));
+  info->dim = op->g.d;
+  for (int m = 0; m < 3; ++m) {
+    info->J[m] = op->g.J[m];
+    info->lo[m] = op->lo[m];
+    info->hi[m] = op->hi[m];
+  }
+  info->M = op->M;
+  info->constant_order = op->constant_order;
+  info->s0 = op->s0;
+  info->smin = op->smin;
+  info->smax = op->smax;
+  info->N = op->g.N;
+  info->N_half = op->g.Nh;
+  info->device_bytes = op->bytes;
+  return FW_OK;
+}
+
+int fw_apply(fw_op op, const double* u_host, double* out_host, int m_first, double* imag_residue) {
+  if (!op || !u_host || !out_host) return set_err(FW_E_ARG, "null argument");
+  if (m_first < 0 || m_first > 1) return set_err(FW_E_ARG, "m_first must be 0 or 1");
+  fw_ctx ctx = op->ctx;
+  FW_CUDA(cudaSetDevice(ctx->device));
+  const fw::GridGeom& g = op->g;
+  void *du = nullptr, *dout = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_U, g.N * 8, &du));
+  FW_TRY(ctx->get_scratch(SLOT_OUT, g.N * 8, &dout));
+  FW_CUDA(cudaMemcpyAsync(du, u_host, g.N * 8, cudaMemcpyHostToDevice, ctx->stream));
+  FW_CUDA(cudaMemsetAsync(ctx->residue, 0, sizeof(double), ctx->stream));
+  FW_TRY(apply_device(op, (const double*)du, (double*)dout, m_first, imag_residue ? ctx->residue : nullptr, nullptr));
+  FW_CUDA(cudaMemcpyAsync(out_host, dout, g.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  double res = 0.0;
+  if (imag_residue) FW_CUDA(cudaMemcpyAsync(&res, ctx->residue, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
+  FW_CUDA(cudaGetLastError());
+  if (imag_residue) *imag_residue = res;
+  return FW_OK;
+}
+
+int fw_apply_device(fw_op op, const double* u_dev, double* out_dev, int m_first, double* imag_residue_dev) {
+  if (!op || !u_dev || !out_dev) return set_err(FW_E_ARG, "null argument");
+  FW_CUDA(cudaSetDevice(op->ctx->device));
+  FW_TRY(apply_device(op, u_dev, out_dev, m_first, imag_residue_dev, nullptr));
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_dev, double* const* out_dev) {
+  if (!ops || !u_dev || !out_dev || nfields < 0) return set_err(FW_E_ARG, "null argument");
+  for (int f = 0; f < nfields; ++f) {
+    if (!ops[f]) return set_err(FW_E_ARG, "null op in batch");
+    FW_TRY(apply_device(ops[f], u_dev[f], out_dev[f], 0, nullptr, nullptr));
+  }
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+int fw_rfftn(fw_ctx ctx, int dim, const int* J, const double* x_host, double* H_host) {
+  if (!ctx || !x_host || !H_host) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
+  void *dx = nullptr, *dH = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_U, g.N * 8, &dx));
+  FW_TRY(ctx->get_scratch(SLOT_UH, g.Nh * 16, &dH));
+  FW_CUDA(cudaMemcpyAsync(dx, x_host, g.N * 8, cudaMemcpyHostToDevice, ctx->stream));
+  fw::launch_forward(ctx->L(), g, (const double*)dx, (double2*)dH, false);
+  FW_CUDA(cudaMemcpyAsync(H_host, dH, g.Nh * 16, cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FW_OK;
+}
+
+int fw_irfftn(fw_ctx ctx, int dim, const int* J, const double* H_host, double* x_host) {
+  if (!ctx || !x_host || !H_host) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
+  void *dx = nullptr, *dH = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_OUT, g.N * 8, &dx));
+  FW_TRY(ctx->get_scratch(SLOT_UH, g.Nh * 16, &dH));
+  FW_CUDA(cudaMemcpyAsync(dH, H_host, g.Nh * 16, cudaMemcpyHostToDevice, ctx->stream));
+  fw::launch_irfft(ctx->L(), g, (double2*)dH, (double*)dx);
+  FW_CUDA(cudaMemcpyAsync(x_host, dx, g.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FW_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// SeismicStepper
+
+struct fw_seis_s {
+  fw_ctx ctx = nullptr;
+  fw::GridGeom g;
+  fw_op A1 = nullptr, A2 = nullptr;  // dispersion (1+gamma), attenuation (1/2+gamma)
+  double tau = 0, thr = 0;
+  double *c = nullptr, *eta = nullptr, *tc = nullptr;
+  double* ubuf[3] = {nullptr, nullptr, nullptr};
+  double* abuf[2] = {nullptr, nullptr};
+  double* l1 = nullptr;
+  int* flag = nullptr;
+  long n = 0;    // reported step count (SeismicStepper::n)
+  long lvl = 0;  // index of the current level for buffer rotation
+  double* cur() { return ubuf[lvl % 3]; }
+  double* prev() { return ubuf[(lvl + 2) % 3]; }
+  double* ap() { return abuf[(lvl + 1) % 2]; }
+};
+
+namespace {
+
+void seis_free(fw_seis s) {
+  if (!s) return;
+  fw_op_destroy(s->A1);
+  fw_op_destroy(s->A2);
+  for (double* p : {s->c, s->eta, s->tc, s->ubuf[0], s->ubuf[1], s->ubuf[2], s->abuf[0], s->abuf[1], s->l1})
+    if (p) cudaFree(p);
+  if (s->flag) cudaFree(s->flag);
+  delete s;
+}
+
+// one SeismicStepper::step (seismic.cpp:111-133), enqueued
+int seis_enqueue_step(fw_seis s) {
+  fw_ctx ctx = s->ctx;
+  const fw::GridGeom& g = s->g;
+  auto L = ctx->L();
+  void* uh = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_UH2, g.Nh * sizeof(double2), &uh));
+  double* cur = s->cur();
+  double* l2 = s->abuf[s->lvl % 2];
+  double* next = s->ubuf[(s->lvl + 1) % 3];
+  // shared forward transform of cur for both operators
+  fw::launch_forward(L, g, cur, (double2*)uh, true);
+  FW_TRY(apply_device(s->A1, cur, s->l1, 0, nullptr, nullptr, (const double2*)uh));
+  FW_TRY(apply_device(s->A2, cur, l2, 0, nullptr, s->flag, (const double2*)uh));
+  fw::launch_seis_update(L, g.N, s->tau, cur, s->prev(), s->ap(), s->l1, l2, s->c, s->eta, s->tc, next, s->thr,
+                         (int)(s->n + 1), s->flag);
+  s->n += 1;
+  s->lvl += 1;
+  return FW_OK;
+}
+
+int seis_check(fw_seis s) {
+  int flag = fw::kNoBlowup;
+  FW_CUDA(cudaMemcpyAsync(&flag, s->flag, sizeof(int), cudaMemcpyDeviceToHost, s->ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  FW_CUDA(cudaGetLastError());
+  if (flag != fw::kNoBlowup) {
+    // state is the one before the offending step; n() is the offending step
+    const long steps_after = s->n - flag;  // steps enqueued after the offending one (no-ops)
+    s->lvl -= steps_after + 1;
+    s->n = flag;
+    const int none = fw::kNoBlowup;
+    FW_CUDA(cudaMemcpyAsync(s->flag, &none, sizeof(int), cudaMemcpyHostToDevice, s->ctx->stream));
+    FW_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    char b[160];
+    snprintf(b, sizeof b, "sup|u| > %g at step %d", s->thr, flag);
+    return set_err(FW_E_BLOWUP, b);
+  }
+  return FW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fw_seis_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi, const double* gamma,
+                   const double* c0, double omega0, int M, const double* phi, const double* psi, double tau,
+                   double blowup_factor, fw_seis* out) {
+  if (!ctx || !out || !lo || !hi || !gamma || !c0 || !phi || !psi) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, lo, hi, &g));
+  FW_CUDA(cudaSetDevice(ctx->device));
+  const size_t N = g.N;
+  for (size_t j = 0; j < N; ++j)  // seismic.cpp:14-19
+    if (!(gamma[j] >= 0.0) || !(gamma[j] < 0.5)) {
+      char b[128];
+      snprintf(b, sizeof b, "gamma = %f outside [0, 0.5)", gamma[j]);
+      return set_err(FW_E_GAMMA_RANGE, b);
+    }
+  std::vector<double> c(N), eta(N), tc(N), ord1(N), ord2(N);
+  for (size_t j = 0; j < N; ++j) {  // seismic.cpp:30-39
+    const double gj = gamma[j];
+    const double cg = c0[j];
+    const double scale = pow(cg, 2.0 * gj) * pow(omega0, -2.0 * gj);
+    c[j] = cg * cos(0.5 * M_PI * gj);
+    eta[j] = -scale * cos(M_PI * gj);
+    tc[j] = -(scale / cg) * sin(M_PI * gj);
+    ord1[j] = 1.0 + gj;
+    ord2[j] = 0.5 + gj;
+  }
+  fw_seis s = new fw_seis_s();
+  s->ctx = ctx;
+  s->g = g;
+  s->tau = tau;
+  int rc = op_create_internal(ctx, g, lo, hi, ord1.data(), nullptr, M, &s->A1);
+  if (rc == FW_OK) rc = op_create_internal(ctx, g, lo, hi, ord2.data(), nullptr, M, &s->A2);
+  for (double** p : {&s->c, &s->eta, &s->tc, &s->ubuf[0], &s->ubuf[1], &s->ubuf[2], &s->abuf[0], &s->abuf[1], &s->l1})
+    if (rc == FW_OK) rc = dalloc(p, N);
+  if (rc == FW_OK) rc = dalloc(&s->flag, 1);
+  if (rc != FW_OK) {
+    seis_free(s);
+    return rc;
+  }
+  auto L = ctx->L();
+  cudaStream_t st = ctx->stream;
+  cudaMemcpyAsync(s->c, c.data(), N * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(s->eta, eta.data(), N * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(s->tc, tc.data(), N * 8, cudaMemcpyHostToDevice, st);
+  const int none = fw::kNoBlowup;
+  cudaMemcpyAsync(s->flag, &none, sizeof(int), cudaMemcpyHostToDevice, st);
+  // constructor (seismic.cpp:85-109): prev = phi; cur = Taylor start; atten_prev = A2(phi); n = 1
+  double sup = 0.0;
+  for (size_t j = 0; j < N; ++j) sup = std::max(sup, std::fabs(phi[j]));
+  s->thr = blowup_factor * std::max(sup, 1e-300);
+  s->lvl = 1;
+  s->n = 1;
+  double* d_phi = s->prev();    // ubuf[0]
+  double* d_psi = s->ubuf[2];   // temporary
+  double* d_l2psi = s->abuf[1]; // temporary
+  cudaMemcpyAsync(d_phi, phi, N * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_psi, psi, N * 8, cudaMemcpyHostToDevice, st);
+  rc = apply_device(s->A1, d_phi, s->l1, 0, nullptr, nullptr);
+  if (rc == FW_OK) rc = apply_device(s->A2, d_psi, d_l2psi, 0, nullptr, nullptr);
+  if (rc == FW_OK) {
+    fw::launch_seis_start(L, N, tau, d_phi, d_psi, s->c, s->eta, s->tc, s->l1, d_l2psi, s->cur());
+    rc = apply_device(s->A2, d_phi, s->ap(), 0, nullptr, nullptr);
+  }
+  if (rc == FW_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = set_err(FW_E_CUDA, std::string("seismic start: ") + cudaGetErrorString(e));
+  }
+  if (rc != FW_OK) {
+    seis_free(s);
+    return rc;
+  }
+  *out = s;
+  return FW_OK;
+}
+
+void fw_seis_destroy(fw_seis s) {
+  if (s && s->ctx) cudaStreamSynchronize(s->ctx->stream);
+  seis_free(s);
+}
+
+int fw_seis_enqueue(fw_seis s, int nsteps) {
+  if (!s || nsteps < 0) return set_err(FW_E_ARG, "bad argument");
+  for (int i = 0; i < nsteps; ++i) FW_TRY(seis_enqueue_step(s));
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+int fw_seis_step(fw_seis s, int nsteps) {
+  FW_TRY(fw_seis_enqueue(s, nsteps));
+  return seis_check(s);
+}
+
+int fw_seis_get(fw_seis s, double* cur_host, double* prev_host, double* atten_prev_host, long* n) {
+  if (!s) return set_err(FW_E_ARG, "null stepper");
+  FW_TRY(seis_check(s));
+  const size_t N = s->g.N;
+  cudaStream_t st = s->ctx->stream;
+  if (cur_host) FW_CUDA(cudaMemcpyAsync(cur_host, s->cur(), N * 8, cudaMemcpyDeviceToHost, st));
+  if (prev_host) FW_CUDA(cudaMemcpyAsync(prev_host, s->prev(), N * 8, cudaMemcpyDeviceToHost, st));
+  if (atten_prev_host) FW_CUDA(cudaMemcpyAsync(atten_prev_host, s->ap(), N * 8, cudaMemcpyDeviceToHost, st));
+  FW_CUDA(cudaStreamSynchronize(st));
+  if (n) *n = s->n;
+  return FW_OK;
+}
+
+int fw_seis_set_current(fw_seis s, const double* cur_host) {
+  if (!s || !cur_host) return set_err(FW_E_ARG, "null argument");
+  FW_CUDA(cudaMemcpyAsync(s->cur(), cur_host, s->g.N * 8, cudaMemcpyHostToDevice, s->ctx->stream));
+  return FW_OK;
+}
+
+const double* fw_seis_current_device(fw_seis s) { return s ? s->cur() : nullptr; }
+
+int fw_seis_ops(fw_seis s, fw_op* disp, fw_op* atten) {
+  if (!s) return set_err(FW_E_ARG, "null stepper");
+  if (disp) *disp = s->A1;
+  if (atten) *atten = s->A2;
+  return FW_OK;
+}
+
+int fw_seis_medium(fw_seis s, double* c, double* eta, double* tau_coef) {
+  if (!s) return set_err(FW_E_ARG, "null stepper");
+  const size_t N = s->g.N;
+  cudaStream_t st = s->ctx->stream;
+  if (c) FW_CUDA(cudaMemcpyAsync(c, s->c, N * 8, cudaMemcpyDeviceToHost, st));
+  if (eta) FW_CUDA(cudaMemcpyAsync(eta, s->eta, N * 8, cudaMemcpyDeviceToHost, st));
+  if (tau_coef) FW_CUDA(cudaMemcpyAsync(tau_coef, s->tc, N * 8, cudaMemcpyDeviceToHost, st));
+  FW_CUDA(cudaStreamSynchronize(st));
+  return FW_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// TSFP2 (stepping.cpp:119-138, 266-304)
+
+struct fw_tsfp2_s {
+  fw_ctx ctx = nullptr;
+  fw::GridGeom g;
+  fw_op A = nullptr;
+  double tau = 0, kappa = 1, thr = 0;
+  int cubic = 0;
+  double *u = nullptr, *v = nullptr, *pert = nullptr;
+  double *w = nullptr, *cw = nullptr, *sw = nullptr;
+  double2 *uh = nullptr, *vh = nullptr;
+  int* flag = nullptr;
+  long n = 0;
+};
+
+namespace {
+
+void tsfp2_free(fw_tsfp2 t) {
+  if (!t) return;
+  fw_op_destroy(t->A);
+  for (double* p : {t->u, t->v, t->pert, t->w, t->cw, t->sw})
+    if (p) cudaFree(p);
+  if (t->uh) cudaFree(t->uh);
+  if (t->vh) cudaFree(t->vh);
+  if (t->flag) cudaFree(t->flag);
+  delete t;
+}
+
+void osc_flow(fw_tsfp2 t) {  // oscillator_flow(tau/2), stepping.cpp:271-291
+  auto L = t->ctx->L();
+  fw::launch_forward(L, t->g, t->u, t->uh, true);
+  fw::launch_forward(L, t->g, t->v, t->vh, true);
+  fw::launch_osc_rotate(L, t->g.Nh, t->w, t->cw, t->sw, 0.5 * t->tau, t->uh, t->vh);
+  fw::launch_irfft(L, t->g, t->uh, t->u);
+  fw::launch_irfft(L, t->g, t->vh, t->v);
+}
+
+}  // namespace
+
+extern "C" {
+
+int fw_tsfp2_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                    const double* order_values, int M, double kappa, int f_kind, const double* phi,
+                    const double* psi, double tau, fw_tsfp2* out) {
+  if (!ctx || !out || !lo || !hi || !phi || !psi) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, lo, hi, &g));
+  FW_CUDA(cudaSetDevice(ctx->device));
+  fw_tsfp2 t = new fw_tsfp2_s();
+  t->ctx = ctx;
+  t->g = g;
+  t->tau = tau;
+  t->kappa = kappa;
+  t->cubic = f_kind == 1 ? 1 : 0;
+  int rc = op_create_internal(ctx, g, lo, hi, order_values, nullptr, M, &t->A);
+  for (double** p : {&t->u, &t->v, &t->pert})
+    if (rc == FW_OK) rc = dalloc(p, g.N);
+  for (double** p : {&t->w, &t->cw, &t->sw})
+    if (rc == FW_OK) rc = dalloc(p, g.Nh);
+  if (rc == FW_OK) rc = dalloc(&t->uh, g.Nh);
+  if (rc == FW_OK) rc = dalloc(&t->vh, g.Nh);
+  if (rc == FW_OK) rc = dalloc(&t->flag, 1);
+  if (rc != FW_OK) {
+    tsfp2_free(t);
+    return rc;
+  }
+  // osc_w (stepping.cpp:125-131) and the per-bin rotation for dt = tau/2 on the host (glibc cos/sin)
+  std::vector<double> mu2 = half_mu2(g, lo, hi);
+  std::vector<double> w(g.Nh), cw(g.Nh), sw(g.Nh);
+  const double dt = 0.5 * tau;
+  for (size_t k = 0; k < g.Nh; ++k) {
+    w[k] = mu2[k] > 0.0 ? sqrt(kappa) * pow(mu2[k], 0.5 * t->A->s0) : 0.0;
+    cw[k] = cos(w[k] * dt);
+    sw[k] = sin(w[k] * dt);
+  }
+  double sup = 0.0;
+  for (size_t j = 0; j < g.N; ++j) sup = std::max(sup, std::fabs(phi[j]));
+  t->thr = 1e8 * std::max(sup, 1e-300);
+  cudaStream_t st = ctx->stream;
+  cudaMemcpyAsync(t->w, w.data(), g.Nh * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(t->cw, cw.data(), g.Nh * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(t->sw, sw.data(), g.Nh * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(t->u, phi, g.N * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(t->v, psi, g.N * 8, cudaMemcpyHostToDevice, st);
+  const int none = fw::kNoBlowup;
+  cudaMemcpyAsync(t->flag, &none, sizeof(int), cudaMemcpyHostToDevice, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    tsfp2_free(t);
+    return set_err(FW_E_CUDA, std::string("tsfp2 setup: ") + cudaGetErrorString(e));
+  }
+  *out = t;
+  return FW_OK;
+}
+
+void fw_tsfp2_destroy(fw_tsfp2 t) {
+  if (t && t->ctx) cudaStreamSynchronize(t->ctx->stream);
+  tsfp2_free(t);
+}
+
+int fw_tsfp2_step(fw_tsfp2 t, int nsteps) {
+  if (!t || nsteps < 0) return set_err(FW_E_ARG, "bad argument");
+  auto L = t->ctx->L();
+  const bool kick = !(t->A->constant_order && !t->cubic);  // stepping.cpp:295
+  for (int i = 0; i < nsteps; ++i) {
+    osc_flow(t);
+    if (kick) {
+      FW_TRY(apply_device(t->A, t->u, t->pert, 1, nullptr, nullptr));
+      fw::launch_tsfp2_kick(L, t->g.N, t->tau, t->kappa, t->cubic, t->u, t->pert, t->v);
+    }
+    osc_flow(t);
+    t->n += 1;
+    fw::launch_sup_check(L, t->g.N, t->u, t->thr, (int)t->n, t->flag);
+  }
+  int flag = fw::kNoBlowup;
+  FW_CUDA(cudaMemcpyAsync(&flag, t->flag, sizeof(int), cudaMemcpyDeviceToHost, t->ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(t->ctx->stream));
+  FW_CUDA(cudaGetLastError());
+  if (flag != fw::kNoBlowup) {
+    char b[128];
+    snprintf(b, sizeof b, "sup|u| > %g at step %d", t->thr, flag);
+    return set_err(FW_E_BLOWUP, b);
+  }
+  return FW_OK;
+}
+
+int fw_tsfp2_get(fw_tsfp2 t, double* u_host, double* v_host, long* n) {
+  if (!t) return set_err(FW_E_ARG, "null stepper");
+  cudaStream_t st = t->ctx->stream;
+  if (u_host) FW_CUDA(cudaMemcpyAsync(u_host, t->u, t->g.N * 8, cudaMemcpyDeviceToHost, st));
+  if (v_host) FW_CUDA(cudaMemcpyAsync(v_host, t->v, t->g.N * 8, cudaMemcpyDeviceToHost, st));
+  FW_CUDA(cudaStreamSynchronize(st));
+  if (n) *n = t->n;
+  return FW_OK;
+}
+
+}  // extern "C"

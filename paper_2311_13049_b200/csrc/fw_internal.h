@@ -1,0 +1,78 @@
+// fw_internal.h — launch interface between the C-ABI (fw_capi.cu) and the
+// sm_100a kernels (fw_kernels.cu).  Internal; not part of the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace fw {
+
+struct GridGeom {
+  int d = 0;
+  int J[3] = {1, 1, 1};
+  size_t N = 0;      // real points
+  size_t Nh = 0;     // Hermitian half-spectrum bins: rows * (J[d-1]/2 + 1)
+  size_t rows = 0;   // N / J[d-1]
+  int nl = 0;        // last-axis length
+  int hp1 = 0;       // nl/2 + 1
+};
+
+struct LaunchCtx {
+  cudaStream_t stream = nullptr;
+  const double2* master = nullptr;  // master twiddle table (kTwMaster entries)
+  long long* launches = nullptr;    // host-side launch counter
+};
+
+// u (N reals) -> Uh (Nh bins), scaled by 1/N (flap.cpp:46-50)
+void launch_forward(const LaunchCtx& L, const GridGeom& g, const double* u, double2* Uh, bool scale);
+
+// Inverse + recombination of one operator (flap.cpp:52-91):
+//   out = sum_{m=m_first}^{m_last} dev_m .* Re IFFT(w_m .* Uh)  (ascending m)
+// w: (M+1) x Nh weights (w_0 = base symbol), dev1: s - s0 (N),
+// T: scratch (m_last-m_first+1) x Nh bins (d >= 2 only),
+// residue (nullable): max-accumulated max|Im|, guard (nullable): if *guard != kNoBlowup the
+// kernels writing `out` are no-ops.
+struct InverseArgs {
+  const double2* Uh;
+  const double* w;
+  const double* dev1;
+  double2* T;
+  double* out;
+  int m_first, m_last;
+  double* residue;
+  const int* guard;
+};
+void launch_inverse(const LaunchCtx& L, const GridGeom& g, const InverseArgs& a);
+
+constexpr int kNoBlowup = 0x7fffffff;
+
+// tables: w[m][k] = base[k] * lw_m[k] with the reference recurrences (flap.cpp:108-122)
+void launch_build_weights(const LaunchCtx& L, size_t Nh, int M, const double* mu2h, const double* base,
+                          const double* logm, double* w);
+// w[m][k] = base[k] * lw[m-1][k] from uploaded half log-weight rows
+void launch_weights_from_lw(const LaunchCtx& L, size_t Nh, int M, const double* base, const double* lw,
+                            double* w);
+// dev1[j] = s[j] - s0
+void launch_dev1(const LaunchCtx& L, size_t N, const double* s, double s0, double* dev1);
+
+// seismic Taylor start (seismic.cpp:100-106)
+void launch_seis_start(const LaunchCtx& L, size_t N, double tau, const double* phi, const double* psi,
+                       const double* c, const double* eta, const double* tc, const double* l1phi,
+                       const double* l2psi, double* cur);
+// seismic update (seismic.cpp:116-129); sets *flag = min(*flag, step) when |next| > thr
+void launch_seis_update(const LaunchCtx& L, size_t N, double tau, const double* cur, const double* prev,
+                        const double* ap, const double* l1, const double* l2, const double* c,
+                        const double* eta, const double* tc, double* next, double thr, int step, int* flag);
+
+// TSFP2 pieces (stepping.cpp:106-117, 271-300)
+void launch_osc_rotate(const LaunchCtx& L, size_t Nh, const double* w, const double* cw, const double* sw, double dt,
+                       double2* uh, double2* vh);
+// raise the dynamic shared-memory limit of the FFT kernels on the current device
+void init_kernels();
+void launch_tsfp2_kick(const LaunchCtx& L, size_t N, double tau, double kappa, int cubic, const double* u,
+                       const double* pert, double* v);
+// unscaled inverse of one spectrum to reals (C2C axes 0..d-2 + C2R), in place on H
+void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x);
+void launch_sup_check(const LaunchCtx& L, size_t N, const double* u, double thr, int step, int* flag);
+
+}  // namespace fw

@@ -136,8 +136,10 @@ def port_medium(J, gamma, c0, omega0):
     return c.reshape(tuple(J)), eta.reshape(tuple(J)), tc.reshape(tuple(J))
 
 
-def port_seismic(J, lo, hi, gamma, c0, omega0, M, phi, psi, tau, nsteps, blowup_factor=1e8):
-    """Returns (cur, prev, atten_prev, n)."""
+def port_seismic(J, lo, hi, gamma, c0, omega0, M, phi, psi, tau, nsteps, blowup_factor=1e8,
+                 allow_blowup=False):
+    """Returns (cur, prev, atten_prev, n) [+ rc when allow_blowup: on BlowupDetected (rc 7) the
+    state is the one before the offending step and n is the offending step]."""
     lib = restatement()
     J = _i32(J)
     N = int(np.prod(J))
@@ -146,8 +148,12 @@ def port_seismic(J, lo, hi, gamma, c0, omega0, M, phi, psi, tau, nsteps, blowup_
     rc = lib.fwo_seismic(len(J), J, _f64(lo), _f64(hi), _f64(gamma).ravel(), _f64(c0).ravel(),
                          float(omega0), int(M), _f64(phi).ravel(), _f64(psi).ravel(), float(tau),
                          float(blowup_factor), int(nsteps), cur, prev, ap, C.byref(n))
-    _chk(lib, rc, lib.fwo_last_error)
     shp = tuple(J)
+    if allow_blowup and rc == 7:
+        return cur.reshape(shp), prev.reshape(shp), ap.reshape(shp), n.value, rc
+    _chk(lib, rc, lib.fwo_last_error)
+    if allow_blowup:
+        return cur.reshape(shp), prev.reshape(shp), ap.reshape(shp), n.value, rc
     return cur.reshape(shp), prev.reshape(shp), ap.reshape(shp), n.value
 
 
@@ -275,8 +281,9 @@ def ref_medium(J, lo, hi, gamma, c0, omega0, M):
     return c.reshape(shp), eta.reshape(shp), tc.reshape(shp), z1.value, z2.value
 
 
-def ref_seismic(J, lo, hi, gamma, c0, omega0, M, phi, psi, tau, nsteps, blowup_factor=1e8):
-    """Returns (cur, n).  Raises OracleError(code 7) on BlowupDetected."""
+def ref_seismic(J, lo, hi, gamma, c0, omega0, M, phi, psi, tau, nsteps, blowup_factor=1e8,
+                allow_blowup=False):
+    """Returns (cur, n) [+ rc].  Raises OracleError(code 7) on BlowupDetected unless allow_blowup."""
     lib = reference()
     J = _i32(J)
     cur = np.empty(int(np.prod(J)))
@@ -284,8 +291,10 @@ def ref_seismic(J, lo, hi, gamma, c0, omega0, M, phi, psi, tau, nsteps, blowup_f
     rc = lib.ref_seismic(len(J), J, _f64(lo), _f64(hi), _f64(gamma).ravel(), _f64(c0).ravel(),
                          float(omega0), int(M), _f64(phi).ravel(), _f64(psi).ravel(), float(tau),
                          float(blowup_factor), int(nsteps), cur, C.byref(n))
+    if allow_blowup and rc == 7:
+        return cur.reshape(tuple(J)), n.value, rc
     _chk(lib, rc, lib.ref_last_error)
-    return cur.reshape(tuple(J)), n.value
+    return (cur.reshape(tuple(J)), n.value, rc) if allow_blowup else (cur.reshape(tuple(J)), n.value)
 
 
 def ref_tsfp2(J, lo, hi, s, M, kappa, cubic, phi, psi, tau, nsteps):

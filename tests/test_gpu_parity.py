@@ -1,0 +1,252 @@
+"""GPU parity: the sm_100a path (through the C-ABI) vs the CPU oracles.
+
+Tolerances (north star): relative L2 <= 1e-12 for one operator apply, <= 1e-10
+after the configured time steps, fp64.  Because the device FFT implements the
+same canonical algorithm as the oracle's FFTW shim, most cases
+are in fact bit-identical; those are asserted bitwise where stated.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from conftest import load_golden
+from paper_2311_13049_b200 import configs as cfgs
+
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-12
+STEP_TOL = 1e-10
+
+
+def fw():
+    import paper_2311_13049_b200 as m
+
+    return m
+
+
+def rel_l2(a, b):
+    nb = np.linalg.norm(np.ravel(b))
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / (nb if nb > 0 else 1.0))
+
+
+def grid_of(J, lo, hi):
+    return fw().Grid(list(zip(lo, hi)), J)
+
+
+def gpu_apply(J, lo, hi, s, u, M, m_first=0, s0=None):
+    m = fw()
+    op = m.build_expansion(m.OrderField(grid_of(J, lo, hi), s, s0), M)
+    out, res = op.apply(u, m_first, residue=True)
+    return out, res, op
+
+
+# ------------------------------------------------------------------- golden
+
+
+def test_golden_applies(manifest):
+    for key, c in manifest["cases"].items():
+        if c["kind"] != "apply":
+            continue
+        u, s = load_golden(c, "u"), load_golden(c, "s")
+        out, res, op = gpu_apply(tuple(c["J"]), c["lo"], c["hi"], s, u, c["M"])
+        assert op.s0 == c["s0"] and op.constant_order == c["constant_order"], key
+        assert np.array_equal(out, load_golden(c, "out")), (key, rel_l2(out, load_golden(c, "out")))
+        assert res == c["imag_residue"], key
+        pert, _, _ = gpu_apply(tuple(c["J"]), c["lo"], c["hi"], s, u, c["M"], m_first=1)
+        assert np.array_equal(pert, load_golden(c, "pert")), key
+
+
+def test_golden_seismic(manifest):
+    m = fw()
+    for key, c in manifest["cases"].items():
+        if c["kind"] != "seismic":
+            continue
+        J = tuple(c["J"])
+        g = grid_of(J, c["lo"], c["hi"])
+        phi, gamma = load_golden(c, "phi"), load_golden(c, "gamma")
+        l1, _, op1 = gpu_apply(J, c["lo"], c["hi"], 1.0 + gamma, phi, c["M"])
+        assert op1.s0 == c["s0_disp"]
+        assert rel_l2(l1, load_golden(c, "apply_disp")) <= APPLY_TOL, key
+        assert np.array_equal(l1, load_golden(c, "apply_disp")), key
+        l2, _, op2 = gpu_apply(J, c["lo"], c["hi"], 0.5 + gamma, phi, c["M"])
+        assert op2.s0 == c["s0_atten"]
+        assert np.array_equal(l2, load_golden(c, "apply_atten")), key
+        st = m.SeismicStepper(m.build_medium(g, gamma, np.ones(J), c["omega0"], c["M"]), phi, np.zeros(J), c["tau"])
+        cc, eta, tc = st.coefficients()
+        assert np.array_equal(cc, load_golden(c, "c")) and np.array_equal(eta, load_golden(c, "eta"))
+        assert np.array_equal(tc, load_golden(c, "tau_coef"))
+        st.advance(c["steps"])
+        assert st.n() == c["n"]
+        cur = st.current()
+        ref = load_golden(c, "cur")
+        assert rel_l2(cur, ref) <= STEP_TOL, key
+        assert np.array_equal(cur, ref), (key, rel_l2(cur, ref))
+
+
+def test_golden_tsfp2(manifest):
+    m = fw()
+    c = manifest["cases"]["tsfp2_256"]
+    J = tuple(c["J"])
+    st = m.TSFP2Stepper(m.OrderField(grid_of(J, c["lo"], c["hi"]), load_golden(c, "s")), c["M"], c["kappa"],
+                        load_golden(c, "phi"), np.zeros(J), c["tau"], f="cubic")
+    st.advance(c["steps"])
+    u, v = st.state()
+    assert np.array_equal(u, load_golden(c, "u")) and np.array_equal(v, load_golden(c, "v"))
+
+
+# ------------------------------------------------------- fresh seeded cases
+
+
+@pytest.mark.parametrize("J,lo,hi", [
+    ((4,), (0.0,), (1.0,)), ((8,), (-1.0,), (1.0,)), ((2048,), (-32.0,), (32.0,)), ((4096,), (-32.0,), (32.0,)),
+    ((4, 4), (0.0, 0.0), (1.0, 1.0)), ((8, 128), (-8.0, 0.0), (8.0, 2.0)), ((256, 64), (-8.0, -8.0), (8.0, 8.0)),
+    ((4, 8, 16), (0.0, 0.0, 0.0), (1.0, 2.0, 3.0)), ((32, 16, 64), (-4.0, -4.0, -4.0), (4.0, 4.0, 4.0)),
+])
+@pytest.mark.parametrize("M", [0, 3, 16])
+def test_apply_vs_restatement(J, lo, hi, M):
+    rng = np.random.default_rng(int(np.prod(J)) + M)
+    s = 1.0 + 0.3 * np.sin(np.pi * np.meshgrid(*[np.arange(n) for n in J], indexing="ij")[0] / 8.0)
+    u = rng.standard_normal(J)
+    for m_first in (0, 1):
+        ref, rres = O.port_apply(J, lo, hi, s, u, M, m_first=m_first)
+        got, gres, _ = gpu_apply(J, lo, hi, s, u, M, m_first)
+        assert rel_l2(got, ref) <= APPLY_TOL
+        assert np.array_equal(got, ref), rel_l2(got, ref)
+        assert gres == rres
+
+
+def test_c1_full_config():
+    """BASELINE configs[0]: both single applies at <= 1e-12 (bitwise) and 100 steps at <= 1e-10."""
+    m = fw()
+    cfg = cfgs.c1()
+    g = grid_of(cfg.J, cfg.lo, cfg.hi)
+    for s in cfgs.orders(cfg):
+        ref, _ = O.port_apply(cfg.J, cfg.lo, cfg.hi, s, cfg.phi, cfg.M)
+        got = m.apply_matrix_free(m.build_expansion(m.OrderField(g, s), cfg.M), cfg.phi)
+        assert rel_l2(got, ref) <= APPLY_TOL and np.array_equal(got, ref)
+    st = m.SeismicStepper(m.build_medium(g, cfg.gamma, cfg.c0, cfg.omega0, cfg.M), cfg.phi, cfg.psi, cfg.tau)
+    st.advance(cfg.steps)
+    cur, prev, ap, n = st.state()
+    rcur, rprev, rap, rn = O.port_seismic(cfg.J, cfg.lo, cfg.hi, cfg.gamma, cfg.c0, cfg.omega0, cfg.M, cfg.phi,
+                                          cfg.psi, cfg.tau, cfg.steps)
+    assert n == rn == 101
+    assert rel_l2(cur, rcur) <= STEP_TOL
+    assert np.array_equal(cur, rcur) and np.array_equal(prev, rprev) and np.array_equal(ap, rap)
+
+
+def test_constant_order_collapse_and_perturbation_zero():
+    """acceptance criterion 2 / test_flap.cpp:168-177, 208-212 on the device."""
+    m = fw()
+    J, lo, hi = (256,), (-32.0,), (32.0,)
+    g = grid_of(J, lo, hi)
+    u = np.random.default_rng(2024).standard_normal(J)
+    for s in (0.5, 1.0, 1.3):
+        for M in (0, 5, 15):
+            op = m.build_expansion(m.OrderField(g, np.full(J, s)), M)
+            assert op.constant_order
+            a = m.apply_matrix_free(op, u)
+            b = O.port_constant_order(J, lo, hi, u, s)
+            assert np.max(np.abs(a - b)) / np.max(np.abs(b)) <= 1e-13
+            p = m.apply_perturbation(op, u)
+            assert np.all(p == 0.0)
+
+
+def test_linearity_and_residue():
+    m = fw()
+    J, lo, hi = (256, 128), (-32.0, -8.0), (32.0, 8.0)
+    g = grid_of(J, lo, hi)
+    op = m.build_expansion(m.OrderField(g, cfgs.s1_profile(lo, hi, J)), 15)
+    rng = np.random.default_rng(902)
+    u, v = rng.standard_normal(J), rng.standard_normal(J)
+    lw = m.apply_matrix_free(op, 2.0 * u - 3.0 * v)
+    lu, res = m.apply_matrix_free(op, u, residue=True)
+    lv = m.apply_matrix_free(op, v)
+    assert np.max(np.abs(lw - (2.0 * lu - 3.0 * lv))) / np.max(np.abs(lw)) < 1e-12
+    assert res <= 1e-10 * np.linalg.norm(u)
+
+
+def test_from_tables_matches_build_expansion():
+    """Drop-in path: upload a host ExpansionOperator's tables (the reference's own,
+    when available) and get the same bits as building on the device."""
+    m = fw()
+    J, lo, hi = (32, 64), (-8.0, -8.0), (8.0, 8.0)
+    s = cfgs.s1_profile(lo, hi, J)
+    u = np.random.default_rng(3).standard_normal(J)
+    M = 12
+    if O.ref_available():
+        mu2, base, lw, dev, s0 = O.ref_tables(J, lo, hi, s, M)
+    else:
+        pytest.skip("reference tables need oracle/_ref")
+    op_t = m.ExpansionOperator.from_tables(grid_of(J, lo, hi), M, s0, False, base, lw, dev)
+    got = op_t.apply(u)
+    ref, _ = O.port_apply(J, lo, hi, s, u, M)
+    assert np.array_equal(got, ref)
+
+
+def test_error_behaviour():
+    m = fw()
+    g = grid_of((32,), (-8.0,), (8.0,))
+    with pytest.raises(m.NegativeM):
+        m.build_expansion(m.OrderField(g, np.ones(32)), -1)
+    with pytest.raises(m.OrderOutOfRange):
+        m.build_expansion(m.OrderField(g, np.full(32, 2.5)), 3)
+    with pytest.raises(m.DeviationTooLarge):
+        m.build_expansion(m.OrderField(g, np.linspace(0.05, 1.95, 32), 0.05), 3)
+    with pytest.raises(m.Unsupported):
+        m.build_expansion(m.OrderField(grid_of((12,), (0.0,), (1.0,)), np.ones(12)), 3)
+    op = m.build_expansion(m.OrderField(g, np.ones(32)), 3)
+    with pytest.raises(m.GridMismatch):
+        m.apply_matrix_free(op, np.ones(64))
+    with pytest.raises(m.GammaOutOfRange):
+        m.build_medium(g, np.full(32, 0.6), np.ones(32), 1.0, 4)
+
+
+def test_blowup_detection_matches_reference():
+    """A too-large time step blows up; the device flag reports the same offending
+    step as the reference's BlowupDetected (seismic.cpp:124-129), and the state is
+    the one before that step."""
+    m = fw()
+    J, lo, hi = (64,), (-4.0,), (4.0,)
+    x = lo[0] + np.arange(64) * (8.0 / 64)
+    phi = np.exp(-x**2)
+    gamma = np.full(J, 0.05)
+    tau = 0.2
+    cur_r, prev_r, ap_r, n_r, rc = O.port_seismic(J, lo, hi, gamma, np.ones(J), 1.0, 6, phi, np.zeros(J), tau, 500,
+                                                  allow_blowup=True)
+    assert rc == 7
+    if O.ref_available():
+        cur_x, n_x, rc_x = O.ref_seismic(J, lo, hi, gamma, np.ones(J), 1.0, 6, phi, np.zeros(J), tau, 500,
+                                         allow_blowup=True)
+        assert rc_x == 7 and n_x == n_r and np.array_equal(cur_x, cur_r)
+    st = m.SeismicStepper(m.build_medium(grid_of(J, lo, hi), gamma, np.ones(J), 1.0, 6), phi, np.zeros(J), tau)
+    with pytest.raises(m.BlowupDetected):
+        st.advance(500)
+    cur, prev, ap, n = st.state()
+    assert n == n_r
+    assert np.array_equal(cur, cur_r) and np.array_equal(prev, prev_r) and np.array_equal(ap, ap_r)
+
+
+def test_rfftn_irfftn_device_bitwise():
+    m = fw()
+    for shape in [(16,), (4096,), (64, 32), (8, 16, 32)]:
+        x = np.random.default_rng(len(shape)).standard_normal(shape)
+        H = m.rfftn(x)
+        assert np.array_equal(H, O.port_rfftn(x))
+        assert np.array_equal(m.irfftn(H, shape), O.port_irfftn(H, shape))
+
+
+def test_c2_full_size_properties():
+    """configs[1] at full size (1024^2): too big for a quick CPU apply, checked
+    through size-independent properties + a bitwise check of a row band."""
+    m = fw()
+    cfg = cfgs.c2()
+    g = grid_of(cfg.J, cfg.lo, cfg.hi)
+    s = 1.0 + cfg.gamma
+    op = m.build_expansion(m.OrderField(g, s), cfg.M)
+    a = m.apply_matrix_free(op, cfg.phi)
+    b = m.apply_matrix_free(op, 2.0 * cfg.phi)
+    assert np.array_equal(b, 2.0 * a)  # scaling by 2 is exact in fp64
+    full = m.apply_matrix_free(op, cfg.phi)
+    assert np.array_equal(a, full)  # deterministic
+    ref, _ = O.port_apply(cfg.J, cfg.lo, cfg.hi, s, cfg.phi, cfg.M)
+    assert rel_l2(a, ref) <= APPLY_TOL and np.array_equal(a, ref)
