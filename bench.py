@@ -1,0 +1,300 @@
+"""bench.py — throughput of the fused variable-order seismic step on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 2D periodic [-16,16)^2, 1024x1024, fp64,
+Gaussian pulse, two-layer Q medium, M = 16, dt = 5e-4.  One "step" is one
+SeismicStepper::step (seismic.cpp:111-133): two M-term operator applies of
+orders 1+gamma and 1/2+gamma sharing one forward transform, plus the fused update.
+
+  value   = 2 N (M+1) / t_step / 1e9   [Gpoint*term/s], inputs resident in HBM
+  e2e     = same metric through the public API with the wavefield copied host->device
+            (pinned) before and device->host after every step
+  roofline: HBM bytes of the step (SURVEY.md §8(d) model) / measured step time vs
+            MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline: the reference itself (oracle/_ref: reference sources + FFTW-API shim)
+            timed on this host's cores on a bounded number of C2 steps
+
+`--impl reference` times the reference CPU implementation of the same step.
+N > 1 (torchrun): every rank runs an independent C2 replica (weak scaling, no
+collective on the data path; C2 is a single-GPU configuration).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "VO frac-Laplacian Gpoint·term/s & time-steps/s; % of HBM roofline"
+UNIT = "Gpoint·term/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--size", type=int, default=1024, help="grid points per axis (C2 = 1024)")
+    p.add_argument("--cpu-baseline-steps", type=int, default=4)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_baseline(cfg, steps: int):
+    """Time the reference (oracle/_ref) — or, if it is not built, the C restatement —
+    on `steps` C2 steps on this host.  Checker code: only this leg imports oracle/."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import ctypes as C
+
+    import oracle_lib as O
+
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    units = 2 * cfg.N * (cfg.M + 1)
+    if O.ref_available():
+        lib = O.reference()
+        lib.ref_time_seismic.argtypes = [C.c_int, O._ip, O._dp, O._dp, O._dp, O._dp, C.c_double, C.c_int,
+                                         O._dp, O._dp, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                         C.c_void_p]
+        per = C.c_double(0.0)
+        rc = lib.ref_time_seismic(len(cfg.J), O._i32(cfg.J), O._f64(cfg.lo), O._f64(cfg.hi),
+                                  O._f64(cfg.gamma).ravel(), O._f64(cfg.c0).ravel(), cfg.omega0, cfg.M,
+                                  O._f64(cfg.phi).ravel(), O._f64(cfg.psi).ravel(), cfg.tau, 1, steps,
+                                  C.byref(per), None)
+        if rc != 0:
+            raise RuntimeError(lib.ref_last_error())
+        t = per.value
+        kind = "reference"
+        how = ("reference sources (proj/src, unmodified) + FFTW-API shim (FFTW absent in image), "
+               "OpenMP over the M+1 terms (flap.cpp:75-77)")
+    else:
+        t0 = time.perf_counter()
+        O.port_seismic(cfg.J, cfg.lo, cfg.hi, cfg.gamma, cfg.c0, cfg.omega0, cfg.M, cfg.phi, cfg.psi, cfg.tau,
+                       steps)
+        t = (time.perf_counter() - t0) / (steps + 1.5)  # construction = 3 applies ~ 1.5 steps
+        kind = "port"
+        how = "C restatement (oracle/fw_oracle.c), OpenMP over FFT lines"
+    return {"value": units / t / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{steps} SeismicStepper steps of C2 (1024^2, M=16) after 1 warm-up step; {how}",
+            "sec_per_step": t}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2311_13049_b200 import configs
+
+    cfg = configs.c2(args.size)
+    steps = max(1, min(args.steps, args.cpu_baseline_steps))
+    cb = cpu_baseline(cfg, steps)
+    v = cb["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": 1, "ms_per_step": cb["sec_per_step"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 seismic step ({args.size}^2, M=16, dt=5e-4)", "grid": [args.size] * 2,
+                       "M": cfg.M, "parallelism": "cpu (host cores)"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    rank, world, local = dist_env()
+    import torch
+
+    import paper_2311_13049_b200 as fw
+    from paper_2311_13049_b200 import configs
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.c2(args.size)
+    ctx = fw.Context(local)
+    grid = fw.Grid(list(zip(cfg.lo, cfg.hi)), cfg.J)
+    med = fw.build_medium(grid, cfg.gamma, cfg.c0, cfg.omega0, cfg.M)
+    st = fw.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau, ctx=ctx)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        ctx.sync()
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- device-resident throughput ----
+    st.advance(args.warmup)
+    barrier()
+    l0 = ctx.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        st.enqueue(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+    launches = ctx.launches() - l0
+    st.n()  # raises BlowupDetected if the device flag fired
+    ms = e0.elapsed_time(e1) / args.steps
+    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t_max.item())
+    units = 2 * cfg.N * (cfg.M + 1)
+    value = world * units / (ms * 1e-3) / 1e9
+
+    # ---- end to end through the public API (pinned host wavefield round trip per step) ----
+    import ctypes as C
+
+    lib = fw.load_library()
+    host = torch.empty(cfg.N, dtype=torch.float64, pin_memory=True)
+    hp = C.cast(C.c_void_p(host.data_ptr()), C.POINTER(C.c_double))
+    check = fw._capi.check
+    check(lib.fw_seis_get(st._h, hp, None, None, None))
+    e2e_steps = max(3, min(args.steps, 50))
+    for _ in range(2):
+        check(lib.fw_seis_set_current(st._h, hp))
+        check(lib.fw_seis_step(st._h, 1))
+        check(lib.fw_seis_get(st._h, hp, None, None, None))
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(e2e_steps):
+        check(lib.fw_seis_set_current(st._h, hp))
+        check(lib.fw_seis_step(st._h, 1))
+        check(lib.fw_seis_get(st._h, hp, None, None, None))
+    e3.record(stream)
+    e3.synchronize()
+    ms_e2e = e2.elapsed_time(e3) / e2e_steps
+    t2 = torch.tensor([ms_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = world * units / (float(t2.item()) * 1e-3) / 1e9
+
+    if rank == 0:
+        hbm, peak_src = peaks()
+        B_step = configs.bytes_per_seismic_step(cfg.N, cfg.N_half, cfg.M, table_model=True)
+        achieved = B_step / (ms * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get(f"c2_step_{args.size}")
+        except Exception:
+            pass
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 seismic step ({args.size}^2, M=16, dt=5e-4; BASELINE configs[1])",
+                       "grid": list(cfg.J), "M": cfg.M, "tau": cfg.tau,
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                       "l2": "working set (2 ops x 17 w-tables + term scratch + state) ~0.45 GB > 126 MB L2; no flush"},
+            "time_steps_per_s": world * 1e3 / ms,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "kernel": "whole seismic step (all launches of one step)",
+                         "bytes_model": "SURVEY.md 8(d) B_step = 2 B_apply - 8N + 72N (table-streaming model)",
+                         "algorithmic_bytes_per_step": B_step, "peak_source": peak_src},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * cfg.N,
+                    "d2h_bytes_per_step": 8 * cfg.N, "ms_per_step": float(t2.item()),
+                    "path": "fw_seis_set_current (pinned H2D) + fw_seis_step + fw_seis_get (D2H)"},
+            "gpu_launches": int(launches),
+            "launches_per_step": launches / args.steps,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                cb = cpu_baseline(cfg, args.cpu_baseline_steps)
+                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as e:  # reported, never fatal
+                line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
