@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -20,6 +21,7 @@
 #include "../../include/fw_capi.h"
 #include "fw_fft.cuh"
 #include "fw_internal.h"
+#include "fw_step2d.h"
 
 namespace {
 
@@ -197,6 +199,10 @@ struct fw_ctx_s {
   void* scratch[8] = {};
   size_t scratch_bytes[8] = {};
   double* residue = nullptr;  // device scalar
+  int nsm = 148;
+  bool force_generic = false;                 // FW_FORCE_GENERIC=1: multi-pass kernels only
+  unsigned long long* counters = nullptr;     // persistent-kernel counters (2 sets)
+  int cset = 0;
   fw::LaunchCtx L() { return fw::LaunchCtx{stream, master, &launches}; }
   int get_scratch(int slot, size_t bytes, void** out) {
     if (scratch_bytes[slot] < bytes) {
@@ -215,7 +221,7 @@ struct fw_ctx_s {
   }
 };
 
-enum { SLOT_UH = 0, SLOT_T = 1, SLOT_U = 2, SLOT_OUT = 3, SLOT_TMP = 4, SLOT_UH2 = 5 };
+enum { SLOT_UH = 0, SLOT_T = 1, SLOT_U = 2, SLOT_OUT = 3, SLOT_TMP = 4, SLOT_UH2 = 5, SLOT_Y2D = 6, SLOT_T2D = 7 };
 
 struct fw_op_s {
   fw_ctx ctx = nullptr;
@@ -226,7 +232,10 @@ struct fw_op_s {
   double s0 = 0, smin = 0, smax = 0;
   double* w = nullptr;     // (M+1) x Nh
   double* dev1 = nullptr;  // N
+  double* w2d = nullptr;   // persistent 2D kernel: [M+1][groups][J0][4] weights
+  double* devt = nullptr;  // persistent 2D kernel: [M][N] deviation powers (s-s0)^m
   size_t bytes = 0;
+  bool step2d = false;
 };
 
 extern "C" {
@@ -257,6 +266,14 @@ int fw_ctx_create(int device, fw_ctx* out) {
     return FW_E_OOM;
   }
   FW_CUDA(cudaMemcpy(c->master, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  const char* fg = getenv("FW_FORCE_GENERIC");
+  c->force_generic = fg && fg[0] == '1';
+  if (dalloc(&c->counters, 2 * (size_t)fw::kStep2dCStride)) {
+    fw_ctx_destroy(c);
+    return FW_E_OOM;
+  }
+  FW_CUDA(cudaMemset(c->counters, 0, 2 * (size_t)fw::kStep2dCStride * sizeof(unsigned long long)));
   fw::init_kernels();
   *out = c;
   return FW_OK;
@@ -270,6 +287,7 @@ void fw_ctx_destroy(fw_ctx c) {
     if (p) cudaFree(p);
   if (c->master) cudaFree(c->master);
   if (c->residue) cudaFree(c->residue);
+  if (c->counters) cudaFree(c->counters);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -304,6 +322,15 @@ int op_alloc_common(fw_ctx ctx, const fw::GridGeom& g, const double* lo, const d
     return FW_E_OOM;
   }
   op->bytes = ((size_t)(M + 1) * g.Nh + g.N) * sizeof(double);
+  if (g.d == 2 && fw::step2d_supported(g.J[0], g.J[1], ctx->nsm) && M <= 64) {
+    const size_t nw = (size_t)(M + 1) * fw::step2d_col_groups(g.J[1]) * g.J[0] * fw::kStep2dCG;
+    if (dalloc(&op->w2d, nw) || dalloc(&op->devt, (size_t)std::max(M, 1) * g.N)) {
+      fw_op_destroy(op);
+      return FW_E_OOM;
+    }
+    op->bytes += (nw + (size_t)M * g.N) * sizeof(double);
+    op->step2d = true;
+  }
   *o = op;
   (void)out;
   return FW_OK;
@@ -343,6 +370,10 @@ int op_create_internal(fw_ctx ctx, const fw::GridGeom& g, const double* lo, cons
   cudaMemcpyAsync(d_s, s, g.N * 8, cudaMemcpyHostToDevice, ctx->stream);
   fw::launch_build_weights(L, g.Nh, M, d_mu2, d_base, d_logm, op->w);
   fw::launch_dev1(L, g.N, d_s, s0, op->dev1);
+  if (op->step2d) {
+    fw::launch_w_to_2d(ctx->stream, g.J[0], g.J[1], M, op->w, op->w2d);
+    fw::launch_dev_tables(ctx->stream, g.N, M, op->dev1, op->devt);
+  }
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   cudaFree(d_mu2); cudaFree(d_base); cudaFree(d_logm); cudaFree(d_s);
   if (e != cudaSuccess) {
@@ -352,6 +383,43 @@ int op_create_internal(fw_ctx ctx, const fw::GridGeom& g, const double* lo, cons
   *out = op;
   return FW_OK;
 }
+
+// persistent single-launch 2D kernel (fw_step2d.cu); ops[0..nops) share grid and M
+int launch_persistent(fw_ctx ctx, fw_op const* ops, int nops, int m_first, const double* u, double* const* outs,
+                      double* residue, fw::Step2DParams* extra) {
+  const fw::GridGeom& g = ops[0]->g;
+  const int m_last = ops[0]->constant_order ? 0 : ops[0]->M;
+  void *Y = nullptr, *T = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_Y2D, g.Nh * sizeof(double2), &Y));
+  FW_TRY(ctx->get_scratch(SLOT_T2D, 3 * g.Nh * sizeof(double2), &T));
+  fw::Step2DParams p = extra ? *extra : fw::Step2DParams{};
+  p.J0 = g.J[0];
+  p.J1 = g.J[1];
+  p.M = m_last;
+  p.m_first = m_first;
+  p.nops = nops;
+  p.nterms_total = nops * (m_last + 1 - m_first);
+  p.u = u;
+  p.Y = (double2*)Y;
+  p.T = (double2*)T;
+  for (int o = 0; o < nops; ++o) {
+    p.w[o] = ops[o]->w2d;
+    p.dev[o] = ops[o]->devt;
+    p.out[o] = outs[o];
+  }
+  p.residue = residue;
+  p.master = ctx->master;
+  p.counters = ctx->counters;
+  p.cset = ctx->cset;
+  p.cstride = fw::kStep2dCStride;
+  ctx->cset ^= 1;
+  cudaError_t e = fw::launch_step2d(p, ctx->stream, ctx->nsm);
+  if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("persistent 2D launch: ") + cudaGetErrorString(e));
+  ctx->launches += 1;
+  return FW_OK;
+}
+
+bool use_persistent(fw_op op) { return op->step2d && !op->ctx->force_generic; }
 
 // out = A(u) for device pointers, enqueued
 int apply_device(fw_op op, const double* u, double* out, int m_first, double* residue, const int* guard,
@@ -364,6 +432,11 @@ int apply_device(fw_op op, const double* u, double* out, int m_first, double* re
   if (m_first > m_last) {  // perturbation of a constant-order operator: exact zero (flap.cpp:163-166)
     FW_CUDA(cudaMemsetAsync(out, 0, g.N * sizeof(double), ctx->stream));
     return FW_OK;
+  }
+  if (!Uh_pre && !guard && use_persistent(op)) {
+    fw_op ops[1] = {op};
+    double* outs[1] = {out};
+    return launch_persistent(ctx, ops, 1, m_first, u, outs, residue, nullptr);
   }
   void* uh = nullptr;
   const double2* Uh = Uh_pre;
@@ -429,6 +502,10 @@ int fw_op_create_from_tables(fw_ctx ctx, int dim, const int* J, const double* lo
   } else {
     cudaMemsetAsync(op->dev1, 0, g.N * 8, ctx->stream);
   }
+  if (op->step2d) {
+    fw::launch_w_to_2d(ctx->stream, g.J[0], g.J[1], M, op->w, op->w2d);
+    fw::launch_dev_tables(ctx->stream, g.N, M, op->dev1, op->devt);
+  }
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   cudaFree(d_base); cudaFree(d_lw);
   if (e != cudaSuccess) {
@@ -444,6 +521,8 @@ void fw_op_destroy(fw_op op) {
   if (!op) return;
   if (op->w) cudaFree(op->w);
   if (op->dev1) cudaFree(op->dev1);
+  if (op->w2d) cudaFree(op->w2d);
+  if (op->devt) cudaFree(op->devt);
   delete op;
 }
 
@@ -573,11 +652,31 @@ int seis_enqueue_step(fw_seis s) {
   fw_ctx ctx = s->ctx;
   const fw::GridGeom& g = s->g;
   auto L = ctx->L();
-  void* uh = nullptr;
-  FW_TRY(ctx->get_scratch(SLOT_UH2, g.Nh * sizeof(double2), &uh));
   double* cur = s->cur();
   double* l2 = s->abuf[s->lvl % 2];
   double* next = s->ubuf[(s->lvl + 1) % 3];
+  if (use_persistent(s->A1) && use_persistent(s->A2) && s->A1->constant_order == s->A2->constant_order) {
+    fw::Step2DParams x{};
+    x.seismic = 1;
+    x.prev = s->prev();
+    x.ap = s->ap();
+    x.c = s->c;
+    x.eta = s->eta;
+    x.tc = s->tc;
+    x.next = next;
+    x.tau = s->tau;
+    x.thr = s->thr;
+    x.step = (int)(s->n + 1);
+    x.flag = s->flag;
+    fw_op ops[2] = {s->A1, s->A2};
+    double* outs[2] = {s->l1, l2};
+    FW_TRY(launch_persistent(ctx, ops, 2, 0, cur, outs, nullptr, &x));
+    s->n += 1;
+    s->lvl += 1;
+    return FW_OK;
+  }
+  void* uh = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_UH2, g.Nh * sizeof(double2), &uh));
   // shared forward transform of cur for both operators
   fw::launch_forward(L, g, cur, (double2*)uh, true);
   FW_TRY(apply_device(s->A1, cur, s->l1, 0, nullptr, nullptr, (const double2*)uh));
@@ -601,6 +700,9 @@ int seis_check(fw_seis s) {
     s->n = flag;
     const int none = fw::kNoBlowup;
     FW_CUDA(cudaMemcpyAsync(s->flag, &none, sizeof(int), cudaMemcpyHostToDevice, s->ctx->stream));
+    // launches skipped by the flag did not clear their counter sets: reset both
+    FW_CUDA(cudaMemsetAsync(s->ctx->counters, 0, 2 * (size_t)fw::kStep2dCStride * sizeof(unsigned long long),
+                            s->ctx->stream));
     FW_CUDA(cudaStreamSynchronize(s->ctx->stream));
     char b[160];
     snprintf(b, sizeof b, "sup|u| > %g at step %d", s->thr, flag);

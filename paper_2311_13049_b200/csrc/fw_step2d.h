@@ -1,0 +1,43 @@
+// fw_step2d.h — parameters of the persistent 2D step kernel (fw_step2d.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace fw {
+
+constexpr int kStep2dMaxTerms = 2 * 65;                 // nops <= 2, M <= 64
+constexpr int kStep2dCStride = 1 + 2 * kStep2dMaxTerms;  // counters per set
+
+struct Step2DParams {
+  int J0, J1;
+  int M, m_first, nops, nterms_total;
+  const double* u;          // input field (cur)
+  double2* Y;               // J0 x (J1/2+1) forward scratch
+  double2* T;               // KRING x J0 x (J1/2+1) term ring
+  const double* w[2];       // per op: [M+1][ngroups][J0][CG] weights
+  const double* dev[2];     // per op: [M][J0][J1] deviation powers m = 1..M
+  double* out[2];           // per op result (seismic: out[0] = L1, out[1] = new L2prev)
+  double* residue;          // nullable, max-accumulated
+  const double2* master;    // twiddle master table
+  unsigned long long* counters;  // 2 sets x kStep2dCStride, zero-initialised
+  int cset, cstride;
+  // seismic update
+  int seismic;
+  const double *prev, *ap, *c, *eta, *tc;
+  double* next;
+  double tau, thr;
+  int step;
+  int* flag;
+};
+
+bool step2d_supported(int J0, int J1, int nsm);
+int step2d_col_groups(int J1);
+constexpr int kStep2dCG = 4;
+cudaError_t launch_step2d(const Step2DParams& p, cudaStream_t st, int nsm);
+
+// table relayouts for the persistent kernel
+void launch_w_to_2d(cudaStream_t st, int J0, int J1, int M, const double* w, double* w2d);
+void launch_dev_tables(cudaStream_t st, size_t N, int M, const double* dev1, double* dev);
+
+}  // namespace fw

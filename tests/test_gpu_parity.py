@@ -250,3 +250,76 @@ def test_c2_full_size_properties():
     assert np.array_equal(a, full)  # deterministic
     ref, _ = O.port_apply(cfg.J, cfg.lo, cfg.hi, s, cfg.phi, cfg.M)
     assert rel_l2(a, ref) <= APPLY_TOL and np.array_equal(a, ref)
+
+
+# ------------------------------------------- persistent 2D kernel vs multi-pass path
+
+
+def generic_context():
+    import os
+
+    m = fw()
+    os.environ["FW_FORCE_GENERIC"] = "1"
+    try:
+        return m.Context(0)
+    finally:
+        del os.environ["FW_FORCE_GENERIC"]
+
+
+@pytest.mark.parametrize("J", [(256, 256), (512, 512), (512, 1024), (1024, 512), (1024, 1024)])
+def test_persistent_2d_apply_bitwise(J):
+    """The single-launch persistent kernel (fw_step2d.cu) and the multi-pass kernels
+    implement the same canonical arithmetic: identical bits, both m_first values."""
+    m = fw()
+    lo, hi = (-16.0, -16.0), (16.0, 16.0)
+    g = grid_of(J, lo, hi)
+    rng = np.random.default_rng(J[0] + J[1])
+    s = 1.0 + 0.4 * cfgs.mode_sum(lo, hi, J, *cfgs.random_modes(rng, 6, 3, 2)) / 6.0
+    s = np.clip(s, 0.6, 1.4)
+    u = rng.standard_normal(J)
+    gctx = generic_context()
+    op_p = m.build_expansion(m.OrderField(g, s), 16)
+    op_g = m.build_expansion(m.OrderField(g, s), 16, ctx=gctx)
+    for m_first in (0, 1):
+        a, ra = op_p.apply(u, m_first, residue=True)
+        b, rb = op_g.apply(u, m_first, residue=True)
+        assert np.array_equal(a, b), rel_l2(a, b)
+        assert ra == rb
+    if J == (256, 256):
+        ref, rres = O.port_apply(J, lo, hi, s, u, 16)
+        assert np.array_equal(op_p.apply(u), ref)
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_persistent_2d_seismic_bitwise(n):
+    m = fw()
+    cfg = cfgs.c2(n)
+    g = grid_of(cfg.J, cfg.lo, cfg.hi)
+    med = m.build_medium(g, cfg.gamma, cfg.c0, cfg.omega0, cfg.M)
+    st_p = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau)
+    st_g = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau, ctx=generic_context())
+    st_p.advance(7)
+    st_g.advance(7)
+    for a, b in zip(st_p.state(), st_g.state()):
+        assert np.array_equal(a, b)
+    if n == 256:
+        rcur, rprev, rap, rn = O.port_seismic(cfg.J, cfg.lo, cfg.hi, cfg.gamma, cfg.c0, cfg.omega0, cfg.M,
+                                              cfg.phi, cfg.psi, cfg.tau, 7)
+        cur, prev, ap, n_ = st_p.state()
+        assert n_ == rn and np.array_equal(cur, rcur) and np.array_equal(ap, rap)
+
+
+def test_c2_200_steps_vs_multipass():
+    """configs[1] exactly as configured (1024^2, M=16, 200 steps): persistent vs multi-pass
+    bitwise, and rel L2 <= 1e-10 trivially satisfied."""
+    m = fw()
+    cfg = cfgs.c2()
+    g = grid_of(cfg.J, cfg.lo, cfg.hi)
+    med = m.build_medium(g, cfg.gamma, cfg.c0, cfg.omega0, cfg.M)
+    st_p = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau)
+    st_g = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau, ctx=generic_context())
+    st_p.advance(cfg.steps)
+    st_g.advance(cfg.steps)
+    a, b = st_p.current(), st_g.current()
+    assert st_p.n() == cfg.steps + 1
+    assert rel_l2(a, b) <= STEP_TOL and np.array_equal(a, b)
