@@ -1,24 +1,26 @@
 // fw_step2d.cu — persistent single-launch 2D apply / seismic step for sm_100a.
 //
 // One cooperative launch of one CTA per SM does the whole seismic step (or one
-// operator apply) on a J0 x J1 grid:
+// operator apply) on a J0 x J1 grid (half spectrum H = J1/2 + 1 columns):
 //
-//   F1  every CTA: R2C of its rows of u (J1 reals)           -> Y (global, L2)
+//   F1  every CTA: R2C of its rows of u                        -> Y (global, L2)
 //   --- grid counter ---
 //   F2  column CTAs: C2C of their CG columns of Y, x 1/N       -> uhat (SHARED MEMORY, kept)
-//   for t = (op, m), m = 0..M of every operator, pipelined through a K-slot ring:
-//     C(t) column CTAs: (w_m .* uhat) -> inverse C2C (columns) -> T[t mod K] (global, L2)
-//     R(t) every CTA : T rows -> C2R in shared memory -> acc += (s-s0)^m .* x (registers)
-//   update (seismic): next = 2cur - prev + tau^2 c^2 (eta L1 + tau_c (L2 - L2prev)/tau)
+//   for t = (op, m), m = m_first..M of every operator, pipelined through a K-slot ring:
+//     C(t) column CTAs: (w_m .* uhat) -> inverse C2C          -> T[t mod K] (global, L2)
+//     R(t) every CTA : T rows -> C2R (pre-processing fused into the first pass)
+//                      -> acc += (s-s0)^m .* x  (accumulators in registers,
+//                      (s-s0)^m rows staged into shared memory by cp.async)
+//   update (seismic.cpp:116-129) from the registers: next, new L2prev, blow-up flag
 //
-// The Hermitian half-spectrum term intermediate is the only global round trip
-// per term (it must cross SMs: a 2D FFT is an all-to-all); the forward spectrum
-// and the accumulators never leave the SM.  Producer/consumer ordering between
-// CTAs uses monotone per-term counters (release atomics / acquire loads); the
-// ring lets column work run up to K-1 terms ahead of row work.  Arithmetic is
-// the canonical FFT of fw_fft.cuh (same radix plan, twiddles, fma placement) so
-// results are bit-identical to the multi-pass path and to the CPU oracle.
-#include <cooperative_groups.h>
+// The term intermediate T is the only global round trip per term (a 2D FFT is
+// an all-to-all across SMs); the forward spectrum and the accumulators never
+// leave the SM.  CTAs order themselves with monotone per-term counters
+// (red.release / ld.acquire); the ring lets column work run K-1 terms ahead of
+// row work.  Arithmetic is the canonical FFT of fw_fft.cuh (radix plan, twiddle
+// values, fma placement), so results are bit-identical to the multi-pass path
+// and to the CPU oracle.  Twiddles of every pass live in shared memory in a
+// [k][r-1] layout (odd stride: conflict-free).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,7 +31,7 @@
 namespace fw {
 namespace s2d {
 
-constexpr int NT = 256;  // threads per CTA (8 warps; up to 255 registers each)
+constexpr int NT = 256;  // threads per CTA (8 warps, up to 255 registers each)
 constexpr int KRING = 3;
 
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
@@ -39,6 +41,10 @@ __host__ __device__ constexpr int radix(int n, int i) {
 }
 __host__ __device__ constexpr int pprod(int n, int i) { return i == 0 ? 1 : pprod(n, i - 1) * radix(n, i - 1); }
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+// per-pass twiddle table sizes / offsets of an N-point plan (pass 0 has none)
+__host__ __device__ constexpr int twsize(int n, int pass) { return pass == 0 ? 0 : pprod(n, pass) * (radix(n, pass) - 1); }
+__host__ __device__ constexpr int twoff(int n, int pass) { return pass <= 1 ? 0 : twoff(n, pass - 1) + twsize(n, pass - 1); }
+__host__ __device__ constexpr int twtotal(int n) { return twoff(n, npass(n) - 1) + twsize(n, npass(n) - 1); }
 
 // ---------------------------------------------------------------- sync helpers
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -49,14 +55,12 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// all threads: wait until *cnt >= target
 __device__ __forceinline__ void wait_counter(const unsigned long long* cnt, unsigned long long target) {
   if (threadIdx.x == 0) {
-    while (ld_acquire(cnt) < target) __nanosleep(32);
+    while (ld_acquire(cnt) < target) __nanosleep(20);
   }
   __syncthreads();
 }
-// all threads' global writes done -> publish
 __device__ __forceinline__ void signal_counter(unsigned long long* cnt) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -64,24 +68,30 @@ __device__ __forceinline__ void signal_counter(unsigned long long* cnt) {
     red_release_add(cnt, 1ull);
   }
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int DIR>
-__device__ __forceinline__ double2 tw_smem(const double2* tw, int idx) {
-  const double2 w = tw[idx];
+__device__ __forceinline__ double2 dirw(double2 w) {
   return make_double2(w.x, DIR < 0 ? -w.y : w.y);
 }
 
-// Stockham butterfly of pass PASS of an N-point C2C on register array a (butterfly i)
-template <int N, int PASS, int DIR, int TWN>
+// Stockham butterfly of pass PASS (N-point plan) on register array a (butterfly i);
+// tw = this N's per-pass table block.
+template <int N, int PASS, int DIR>
 __device__ __forceinline__ void butterfly(double2* a, int i, const double2* tw) {
   constexpr int R = radix(N, PASS);
   constexpr int p = pprod(N, PASS);
   if constexpr (p > 1) {
     const int k = i & (p - 1);
-    constexpr int ts = N / (p * R);
+    const double2* t = tw + twoff(N, PASS) + k * (R - 1);
 #pragma unroll
     for (int r = 1; r < R; ++r) {
-      const double2 w = tw_smem<DIR>(tw, r * k * ts * (TWN / N));
+      const double2 w = dirw<DIR>(t[r - 1]);
       a[r] = cmulw(a[r], w.x, w.y);
     }
   }
@@ -101,11 +111,8 @@ __device__ __forceinline__ int padq(int q) {
   return q + (q >> PADSH);
 }
 
-// butterfly b of a pass over `nl` lines -> (line, i).  LINE_FAST: lines interleave
-// fastest (adjacent columns, coalesced global access); else butterflies of one line
-// are contiguous.
 template <int T, bool LINE_FAST, int NLC>
-__device__ __forceinline__ void bmap(int b, int nl, int& l, int& i) {
+__device__ __forceinline__ void bmap(int b, int& l, int& i) {
   if constexpr (LINE_FAST) {
     l = b % NLC;
     i = b / NLC;
@@ -115,9 +122,8 @@ __device__ __forceinline__ void bmap(int b, int nl, int& l, int& i) {
   }
 }
 
-// Middle pass PASS (p > 1, not the last) of an N-point C2C over nl lines, in
-// place in shared memory: every thread loads its butterflies, barrier, writes.
-template <int N, int PASS, int DIR, int TWN, int PADSH, int LS, bool LINE_FAST, int NLMAX>
+// Middle pass PASS of an N-point C2C over nl lines, in place in shared memory.
+template <int N, int PASS, int DIR, int PADSH, int LS, bool LINE_FAST, int NLMAX>
 __device__ __forceinline__ void smem_pass(double2* buf, int nl, const double2* tw) {
   constexpr int R = radix(N, PASS);
   constexpr int T = N / R;
@@ -127,7 +133,7 @@ __device__ __forceinline__ void smem_pass(double2* buf, int nl, const double2* t
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     int l, i;
-    bmap<T, LINE_FAST, NLMAX>(tid + j * NT, nl, l, i);
+    bmap<T, LINE_FAST, NLMAX>(tid + j * NT, l, i);
     if (l < nl && i < T) {
 #pragma unroll
       for (int r = 0; r < R; ++r) a[j][r] = buf[l * LS + padq<PADSH>(i + r * T)];
@@ -137,9 +143,9 @@ __device__ __forceinline__ void smem_pass(double2* buf, int nl, const double2* t
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     int l, i;
-    bmap<T, LINE_FAST, NLMAX>(tid + j * NT, nl, l, i);
+    bmap<T, LINE_FAST, NLMAX>(tid + j * NT, l, i);
     if (l < nl && i < T) {
-      butterfly<N, PASS, DIR, TWN>(a[j], i, tw);
+      butterfly<N, PASS, DIR>(a[j], i, tw);
 #pragma unroll
       for (int r = 0; r < R; ++r) buf[l * LS + padq<PADSH>(out_index<N, PASS>(i, r))] = a[j][r];
     }
@@ -150,23 +156,28 @@ __device__ __forceinline__ void smem_pass(double2* buf, int nl, const double2* t
 // --------------------------------------------------------------------------
 template <int J0, int J1, int CG, int RMAX>
 struct Geo {
-  static constexpr int H = J1 / 2 + 1;                // half-spectrum columns
-  static constexpr int h = J1 / 2;                    // row C2C length
-  static constexpr int TWN = (J0 > J1 ? J0 : J1);     // smem twiddle table length
-  static constexpr int NG = (H + CG - 1) / CG;        // column groups
-  static constexpr int PADC = ilog2c(radix(J0, 0));   // column pad shift
-  static constexpr int PADR = ilog2c(radix(h, 0));    // row pad shift
-  static constexpr int LSU = J0 + (CG == 4 ? 2 : CG == 2 ? 4 : 1);  // uhat line stride
+  static constexpr int H = J1 / 2 + 1;               // half-spectrum columns
+  static constexpr int h = J1 / 2;                   // row C2C length
+  static constexpr int NG = (H + CG - 1) / CG;       // column groups
+  static constexpr int PADC = ilog2c(radix(J0, 0));  // column pad shift
+  static constexpr int PADR = ilog2c(radix(h, 0));   // row pad shift
+  static constexpr int LSU = J0 + (CG == 4 ? 2 : CG == 2 ? 4 : 1);
   static constexpr int LSC0 = J0 + (J0 >> PADC);
-  static constexpr int LSC = LSC0 + ((10 - LSC0 % 8) % 8);          // == 2 mod 8
-  static constexpr int LSR = h + 1 + ((h + 1) >> PADR) + 7;
+  static constexpr int LSC = LSC0 + ((10 - LSC0 % 8) % 8);  // == 2 mod 8
+  static constexpr int LSR = h + (h >> PADR) + 2;
   static constexpr int PC = npass(J0);
   static constexpr int PR = npass(h);
-  static constexpr size_t SMEM_TW = sizeof(double2) * TWN;
+  static constexpr int RL = radix(h, PR - 1);  // last row pass
+  static constexpr int TL = h / RL;
+  static constexpr int NBL = cdiv(RMAX * TL, NT);  // last-pass butterflies per thread
+  static constexpr int TWC = twtotal(J0);
+  static constexpr int TWR = twtotal(h);
+  static constexpr int TWP = h + 1;  // W_J1^k, k = 0..h
+  static constexpr size_t SMEM_TW = sizeof(double2) * (TWC + TWR + TWP);
   static constexpr size_t SMEM_U = sizeof(double2) * CG * LSU;
   static constexpr size_t SMEM_W = sizeof(double2) * (CG * LSC > RMAX * LSR ? CG * LSC : RMAX * LSR);
-  static constexpr size_t SMEM_A = sizeof(double) * RMAX * J1;  // row accumulators
-  static constexpr size_t SMEM = SMEM_TW + SMEM_U + SMEM_W + SMEM_A;
+  static constexpr size_t SMEM_D = sizeof(double) * RMAX * J1;  // (s-s0)^m staging
+  static constexpr size_t SMEM = SMEM_TW + SMEM_U + SMEM_W + SMEM_D;
   static_assert(PC <= 3 && PR <= 3 && PR >= 2 && PC >= 2, "2 or 3 passes per FFT");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
@@ -174,18 +185,18 @@ struct Geo {
 // ---------------------------------------------------------------- column FFT
 // J0-point C2C of the CTA's CG columns (lines interleaved fastest).  Pass 0 reads
 // src(cc, q); the last pass writes sink(cc, q, value) in natural order q.
-template <int J0, int CG, int DIR, int TWN, int PADSH, int LSC, class Src, class Sink>
+template <int J0, int CG, int DIR, int PADSH, int LSC, class Src, class Sink>
 __device__ __forceinline__ void column_fft(double2* cbuf, const double2* tw, int ncols, Src src, Sink sink) {
   constexpr int P = npass(J0);
   const int tid = threadIdx.x;
-  {  // pass 0 (p = 1): source -> registers -> smem at j = i*R + r
+  {
     constexpr int R = radix(J0, 0);
     constexpr int T = J0 / R;
     constexpr int NB = cdiv(CG * T, NT);
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       int cc, i;
-      bmap<T, true, CG>(tid + j * NT, CG, cc, i);
+      bmap<T, true, CG>(tid + j * NT, cc, i);
       if (i < T && cc < ncols) {
         double2 a[R];
 #pragma unroll
@@ -197,8 +208,8 @@ __device__ __forceinline__ void column_fft(double2* cbuf, const double2* tw, int
     }
     __syncthreads();
   }
-  if constexpr (P == 3) smem_pass<J0, 1, DIR, TWN, PADSH, LSC, true, CG>(cbuf, CG, tw);
-  {  // last pass: smem -> registers -> sink (outputs i + r*T)
+  if constexpr (P == 3) smem_pass<J0, 1, DIR, PADSH, LSC, true, CG>(cbuf, CG, tw);
+  {
     constexpr int PL = P - 1;
     constexpr int R = radix(J0, PL);
     constexpr int T = J0 / R;
@@ -206,12 +217,12 @@ __device__ __forceinline__ void column_fft(double2* cbuf, const double2* tw, int
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       int cc, i;
-      bmap<T, true, CG>(tid + j * NT, CG, cc, i);
+      bmap<T, true, CG>(tid + j * NT, cc, i);
       if (i < T && cc < ncols) {
         double2 a[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) a[r] = cbuf[cc * LSC + padq<PADSH>(i + r * T)];
-        butterfly<J0, PL, DIR, TWN>(a, i, tw);
+        butterfly<J0, PL, DIR>(a, i, tw);
 #pragma unroll
         for (int r = 0; r < R; ++r) sink(cc, i + r * T, a[r]);
       }
@@ -219,82 +230,27 @@ __device__ __forceinline__ void column_fft(double2* cbuf, const double2* tw, int
   }
 }
 
-// ---------------------------------------------------------------- row C2C
-// nl rows of h points in rbuf (padded).  Pass 0 (from smem, in place), middle pass,
-// and the last pass handed butterfly by butterfly to fin(l, i, a) (outputs
-// q = i + r*T_last).  PASS0_IN_PLACE=false when pass 0 sources were already
-// transformed by the caller.
-template <int h, int DIR, int TWN, int PADSH, int LSR, int RMAX, class Fin>
-__device__ __forceinline__ void row_c2c(double2* rbuf, const double2* tw, int nl, Fin fin) {
-  constexpr int P = npass(h);
-  {  // pass 0, in place (p = 1)
-    constexpr int R = radix(h, 0);
-    constexpr int T = h / R;
-    constexpr int NB = cdiv(RMAX * T, NT);
-    const int tid = threadIdx.x;
-    double2 a[NB][R];
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const int b = tid + j * NT, l = b / T, i = b % T;
-      if (l < nl) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) a[j][r] = rbuf[l * LSR + padq<PADSH>(i + r * T)];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const int b = tid + j * NT, l = b / T, i = b % T;
-      if (l < nl) {
-        Dft<R, DIR>::run(a[j]);
-#pragma unroll
-        for (int r = 0; r < R; ++r) rbuf[l * LSR + padq<PADSH>(i * R + r)] = a[j][r];
-      }
-    }
-    __syncthreads();
-  }
-  if constexpr (P == 3) smem_pass<h, 1, DIR, TWN, PADSH, LSR, false, RMAX>(rbuf, nl, tw);
-  {
-    constexpr int PL = P - 1;
-    constexpr int R = radix(h, PL);
-    constexpr int T = h / R;
-    constexpr int NB = cdiv(RMAX * T, NT);
-    const int tid = threadIdx.x;
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const int b = tid + j * NT, l = b / T, i = b % T;
-      if (l < nl) {
-        double2 a[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) a[r] = rbuf[l * LSR + padq<PADSH>(i + r * T)];
-        butterfly<h, PL, DIR, TWN>(a, i, tw);
-        fin(l, i, a);
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ double2 post_r2c(double2 A, double2 Bz, int k, const double2* tw, int twmul) {
-  // X[k] from Z[k], Z[h-k] (fwcanon fwc_r2c), 1 <= k < h
+// R2C post-processing X[k] from Z[k], Z[h-k] (fwcanon fwc_r2c), 1 <= k < h
+__device__ __forceinline__ double2 post_r2c(double2 A, double2 Bz, double2 wk) {
   const double2 B = make_double2(Bz.x, -Bz.y);
   const double2 E = make_double2((A.x + B.x) * 0.5, (A.y + B.y) * 0.5);
   const double2 D = make_double2((A.x - B.x) * 0.5, (A.y - B.y) * 0.5);
   const double2 O = make_double2(D.y, -D.x);
-  const double2 w = tw_smem<-1>(tw, k * twmul);
+  const double2 w = dirw<-1>(wk);
   const double2 t = cmulw(O, w.x, w.y);
   return make_double2(E.x + t.x, E.y + t.y);
 }
 
-__device__ __forceinline__ double2 pre_c2r(double2 A, double2 Xhk, int k, const double2* tw, int twmul) {
+// C2R pre-processing Z[k] from X[k], X[h-k] (fwcanon fwc_c2r)
+__device__ __forceinline__ double2 pre_c2r(double2 A, double2 Xhk, bool k0, double2 wk) {
   double2 B = make_double2(Xhk.x, -Xhk.y);
-  if (k == 0) {
+  if (k0) {
     A.y = 0.0;
     B.y = 0.0;
   }
   const double2 E = make_double2(A.x + B.x, A.y + B.y);
   const double2 D = make_double2(A.x - B.x, A.y - B.y);
-  const double2 w = tw_smem<+1>(tw, k * twmul);
-  const double2 O = cmulw(D, w.x, w.y);
+  const double2 O = cmulw(D, wk.x, wk.y);
   return make_double2(E.x - O.y, E.y + O.x);
 }
 
@@ -302,12 +258,14 @@ __device__ __forceinline__ double2 pre_c2r(double2 A, double2 Xhk, int k, const 
 template <int J0, int J1, int CG, int RMAX>
 __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
   using G = Geo<J0, J1, CG, RMAX>;
-  constexpr int H = G::H, h = G::h, TWN = G::TWN;
+  constexpr int H = G::H, h = G::h;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* tw = reinterpret_cast<double2*>(smem_raw);
+  double2* twc = reinterpret_cast<double2*>(smem_raw);  // column plan tables
+  double2* twr = twc + G::TWC;                          // row plan tables
+  double2* twp = twr + G::TWR;                          // W_J1^k
   double2* uhat = reinterpret_cast<double2*>(smem_raw + G::SMEM_TW);
   double2* work = reinterpret_cast<double2*>(smem_raw + G::SMEM_TW + G::SMEM_U);
-  double* accs = reinterpret_cast<double*>(smem_raw + G::SMEM_TW + G::SMEM_U + G::SMEM_W);
+  double* devs = reinterpret_cast<double*>(smem_raw + G::SMEM_TW + G::SMEM_U + G::SMEM_W);
   const int tid = threadIdx.x;
   const int b = blockIdx.x;
   const int nblk = gridDim.x;
@@ -323,8 +281,21 @@ __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
   unsigned long long* cC = cnt + 1;
   unsigned long long* cR = cnt + 1 + prm.nterms_total;
 
-  for (int e = tid; e < TWN; e += NT) tw[e] = prm.master[e * (kTwMaster / TWN)];
-  for (int e = tid; e < RMAX * J1; e += NT) accs[e] = 0.0;
+  // twiddle tables (values = master entries, identical to fw_fft.cuh's twiddle())
+  {
+    auto fill = [&](double2* dst, int off, int p, int R) {
+      const int n = p * (R - 1);
+      for (int e = tid; e < n; e += NT) {
+        const int k = e / (R - 1), r = e % (R - 1) + 1;
+        dst[off + e] = prm.master[(r * k) * (kTwMaster / (p * R))];
+      }
+    };
+    if constexpr (G::PC >= 2) fill(twc, twoff(J0, 1), pprod(J0, 1), radix(J0, 1));
+    if constexpr (G::PC >= 3) fill(twc, twoff(J0, 2), pprod(J0, 2), radix(J0, 2));
+    if constexpr (G::PR >= 2) fill(twr, twoff(h, 1), pprod(h, 1), radix(h, 1));
+    if constexpr (G::PR >= 3) fill(twr, twoff(h, 2), pprod(h, 2), radix(h, 2));
+    for (int e = tid; e <= h; e += NT) twp[e] = prm.master[e * (kTwMaster / J1)];
+  }
 
   const int r0 = (int)(((long long)b * J0) / nblk);
   const int r1 = (int)(((long long)(b + 1) * J0) / nblk);
@@ -336,33 +307,52 @@ __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
 
   // ------------------------------------------------ F1: forward rows -> Y
   {
+    constexpr int R0 = radix(h, 0);
+    constexpr int T0 = h / R0;
+    constexpr int NB0 = cdiv(RMAX * T0, NT);
     const double2* u2 = reinterpret_cast<const double2*>(prm.u);
-    for (int e = tid; e < nrows * h; e += NT) {  // packed pairs z_j = x_2j + i x_2j+1
-      const int l = e / h, j = e % h;
-      work[l * G::LSR + padq<G::PADR>(j)] = u2[(size_t)(r0 + l) * h + j];
+#pragma unroll
+    for (int j = 0; j < NB0; ++j) {  // pass 0 straight from global: packed pairs z_q = x_2q + i x_2q+1
+      const int bb = tid + j * NT, l = bb / T0, i = bb % T0;
+      if (l < nrows) {
+        double2 a[R0];
+#pragma unroll
+        for (int r = 0; r < R0; ++r) a[r] = u2[(size_t)(r0 + l) * h + i + r * T0];
+        Dft<R0, -1>::run(a);
+#pragma unroll
+        for (int r = 0; r < R0; ++r) work[l * G::LSR + padq<G::PADR>(i * R0 + r)] = a[r];
+      }
     }
     __syncthreads();
-    row_c2c<h, -1, TWN, G::PADR, G::LSR, RMAX>(work, tw, nrows, [&](int l, int i, double2* a) {
-      constexpr int R = radix(h, npass(h) - 1);
-      constexpr int T = h / R;
+    if constexpr (G::PR == 3) smem_pass<h, 1, -1, G::PADR, G::LSR, false, RMAX>(work, nrows, twr);
 #pragma unroll
-      for (int r = 0; r < R; ++r) work[l * G::LSR + padq<G::PADR>(i + r * T)] = a[r];  // same slots it read
-    });
+    for (int j = 0; j < G::NBL; ++j) {  // last pass, written back to the slots it read
+      const int bb = tid + j * NT, l = bb / G::TL, i = bb % G::TL;
+      if (l < nrows) {
+        double2 a[G::RL];
+#pragma unroll
+        for (int r = 0; r < G::RL; ++r) a[r] = work[l * G::LSR + padq<G::PADR>(i + r * G::TL)];
+        butterfly<h, G::PR - 1, -1>(a, i, twr);
+#pragma unroll
+        for (int r = 0; r < G::RL; ++r) work[l * G::LSR + padq<G::PADR>(i + r * G::TL)] = a[r];
+      }
+    }
     __syncthreads();
     constexpr int NP = h / 2 + 1;
-    for (int e = tid; e < nrows * NP; e += NT) {  // post-process pairs (k, h-k)
-      const int l = e / NP, j = e % NP;
+    for (int l = 0; l < nrows; ++l) {  // post-process pairs (k, h-k)
       const double2* Z = work + l * G::LSR;
       double2* Yr = prm.Y + (size_t)(r0 + l) * H;
-      if (j == 0) {
-        const double2 z0 = Z[0];
-        __stcg(&Yr[0], make_double2(z0.x + z0.y, 0.0));
-        __stcg(&Yr[h], make_double2(z0.x - z0.y, 0.0));
-      } else {
-        const double2 A = Z[padq<G::PADR>(j)];
-        const double2 B = Z[padq<G::PADR>(h - j)];
-        __stcg(&Yr[j], post_r2c(A, B, j, tw, TWN / J1));
-        if (j != h - j) __stcg(&Yr[h - j], post_r2c(B, A, h - j, tw, TWN / J1));
+      for (int jj = tid; jj < NP; jj += NT) {
+        if (jj == 0) {
+          const double2 z0 = Z[0];
+          __stcg(&Yr[0], make_double2(z0.x + z0.y, 0.0));
+          __stcg(&Yr[h], make_double2(z0.x - z0.y, 0.0));
+        } else {
+          const double2 A = Z[padq<G::PADR>(jj)];
+          const double2 B = Z[padq<G::PADR>(h - jj)];
+          __stcg(&Yr[jj], post_r2c(A, B, twp[jj]));
+          if (jj != h - jj) __stcg(&Yr[h - jj], post_r2c(B, A, twp[h - jj]));
+        }
       }
     }
     signal_counter(cY);
@@ -373,8 +363,8 @@ __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
     wait_counter(cY, (unsigned long long)nblk);
     const double inv = 1.0 / ((double)J0 * (double)J1);
     const double2* Y = prm.Y;
-    column_fft<J0, CG, -1, TWN, G::PADC, G::LSC>(
-        work, tw, ncols, [&](int cc, int q) { return __ldcg(&Y[(size_t)q * H + c0 + cc]); },
+    column_fft<J0, CG, -1, G::PADC, G::LSC>(
+        work, twc, ncols, [&](int cc, int q) { return __ldcg(&Y[(size_t)q * H + c0 + cc]); },
         [&](int cc, int q, double2 v) { uhat[cc * G::LSU + q] = make_double2(v.x * inv, v.y * inv); });
     __syncthreads();
   }
@@ -391,8 +381,8 @@ __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
     const int m = prm.m_first + t % nterms;
     const double* w = prm.w[op] + ((size_t)m * G::NG + b) * (size_t)J0 * CG;  // [m][g][k0][CG]
     double2* T = prm.T + (size_t)(t % KRING) * J0 * H;
-    column_fft<J0, CG, +1, TWN, G::PADC, G::LSC>(
-        work, tw, ncols,
+    column_fft<J0, CG, +1, G::PADC, G::LSC>(
+        work, twc, ncols,
         [&](int cc, int q) {
           const double2 v = uhat[cc * G::LSU + q];
           const double wk = __ldg(&w[(size_t)q * CG + cc]);
@@ -402,65 +392,113 @@ __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
     signal_counter(&cC[t]);
   };
 
+  double acc[G::NBL][G::RL][2];
+#pragma unroll
+  for (int j = 0; j < G::NBL; ++j)
+#pragma unroll
+    for (int r = 0; r < G::RL; ++r) acc[j][r][0] = acc[j][r][1] = 0.0;
+
   double rmax = 0.0;
   auto row_term = [&](int t) {
     wait_counter(&cC[t], (unsigned long long)G::NG);
     const int op = t / nterms;
     const int m = prm.m_first + t % nterms;
     const double2* T = prm.T + (size_t)(t % KRING) * J0 * H;
-    for (int e = tid; e < nrows * H; e += NT) {
-      const int l = e / H, k = e - l * H;
-      work[l * G::LSR + padq<G::PADR>(k)] = __ldcg(&T[(size_t)(r0 + l) * H + k]);
+    if (m >= 1) {  // stage (s-s0)^m rows asynchronously
+      const double* dv = prm.dev[op] + (size_t)(m - 1) * J0 * J1 + (size_t)r0 * J1;
+      const int nchunk = nrows * J1 / 2;
+      for (int e = tid; e < nchunk; e += NT) cp_async16(devs + 2 * e, dv + 2 * e);
+      cp_async_commit();
     }
-    __syncthreads();
-    if (prm.residue && tid < nrows) {
-      const double rr = fabs(work[tid * G::LSR].y) + fabs(work[tid * G::LSR + padq<G::PADR>(h)].y);
-      rmax = fmax(rmax, rr);
-    }
-    constexpr int NP = h / 2 + 1;
-    for (int e = tid; e < nrows * NP; e += NT) {  // C2R pre-processing, pairs (k, h-k) in place
-      const int l = e / NP, j = e % NP;
-      double2* X = work + l * G::LSR;
-      if (j == 0) {
-        X[0] = pre_c2r(X[0], X[padq<G::PADR>(h)], 0, tw, TWN / J1);
-      } else {
-        const double2 A = X[padq<G::PADR>(j)], B = X[padq<G::PADR>(h - j)];
-        X[padq<G::PADR>(j)] = pre_c2r(A, B, j, tw, TWN / J1);
-        if (j != h - j) X[padq<G::PADR>(h - j)] = pre_c2r(B, A, h - j, tw, TWN / J1);
-      }
-    }
-    __syncthreads();
-    const double* dv = (m >= 1) ? prm.dev[op] + (size_t)(m - 1) * J0 * J1 + (size_t)r0 * J1 : nullptr;
-    row_c2c<h, +1, TWN, G::PADR, G::LSR, RMAX>(work, tw, nrows, [&](int l, int i, double2* a) {
-      constexpr int R = radix(h, npass(h) - 1);
-      constexpr int T = h / R;
-      double2* ar = reinterpret_cast<double2*>(accs + l * J1);
+    {  // pass 0 with the C2R pre-processing fused: unit i pairs butterflies i and T0-i
+      constexpr int R0 = radix(h, 0);
+      constexpr int T0 = h / R0;
+      constexpr int NU = T0 / 2 + 1;  // units per row
+      constexpr int NBU = cdiv(RMAX * NU, NT);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int q = i + r * T;  // x[2q], x[2q+1]
-        double v0 = a[r].x, v1 = a[r].y;
-        if (dv) {
-          const double2 d = __ldg(reinterpret_cast<const double2*>(dv + (size_t)l * J1) + q);
-          v0 = d.x * v0;
-          v1 = d.y * v1;
+      for (int j = 0; j < NBU; ++j) {
+        const int bb = tid + j * NT, l = bb / NU, i = bb % NU;
+        if (l < nrows) {
+          const double2* X = T + (size_t)(r0 + l) * H;
+          const int i2 = T0 - i;  // mirror butterfly; for i == 0 this walks X[T0 (r+1)], ending at X[h]
+          double2 XA[R0], XB[R0];
+#pragma unroll
+          for (int r = 0; r < R0; ++r) XA[r] = __ldcg(&X[i + r * T0]);
+#pragma unroll
+          for (int r = 0; r < R0; ++r) XB[r] = __ldcg(&X[i2 + r * T0]);
+          double2 a[R0];
+          if (i == 0) {
+            if (prm.residue) rmax = fmax(rmax, fabs(XA[0].y) + fabs(XB[R0 - 1].y));
+#pragma unroll
+            for (int r = 0; r < R0; ++r)  // k = r*T0, h-k = (R0-r)*T0 = XB[R0-1-r]
+              a[r] = pre_c2r(XA[r], XB[R0 - 1 - r], r == 0, twp[r * T0]);
+            Dft<R0, +1>::run(a);
+#pragma unroll
+            for (int r = 0; r < R0; ++r) work[l * G::LSR + padq<G::PADR>(r)] = a[r];
+          } else {
+            // butterfly i: k = i + r*T0, h-k = (T0-i) + (R0-1-r)*T0 -> XB[R0-1-r]
+#pragma unroll
+            for (int r = 0; r < R0; ++r) a[r] = pre_c2r(XA[r], XB[R0 - 1 - r], false, twp[i + r * T0]);
+            Dft<R0, +1>::run(a);
+#pragma unroll
+            for (int r = 0; r < R0; ++r) work[l * G::LSR + padq<G::PADR>(i * R0 + r)] = a[r];
+            if (i2 != i) {  // butterfly T0-i: k = i2 + r*T0, h-k = i + (R0-1-r)*T0 -> XA[R0-1-r]
+#pragma unroll
+              for (int r = 0; r < R0; ++r) a[r] = pre_c2r(XB[r], XA[R0 - 1 - r], false, twp[i2 + r * T0]);
+              Dft<R0, +1>::run(a);
+#pragma unroll
+              for (int r = 0; r < R0; ++r) work[l * G::LSR + padq<G::PADR>(i2 * R0 + r)] = a[r];
+            }
+          }
         }
-        double p0 = 0.0, p1 = 0.0;
-        p0 += v0;
-        p1 += v1;
-        double2 acc = ar[q];
-        acc.x += p0;
-        acc.y += p1;
-        ar[q] = acc;
-      }
-    });
-    signal_counter(&cR[t]);
-    if (m == M && !(prm.seismic && op == prm.nops - 1)) {  // operator complete: hand the accumulator over
-      double* o = prm.out[op] + (size_t)r0 * J1;
-      for (int e = tid; e < nrows * J1; e += NT) {
-        o[e] = accs[e];
-        accs[e] = 0.0;
       }
       __syncthreads();
+    }
+    if constexpr (G::PR == 3) smem_pass<h, 1, +1, G::PADR, G::LSR, false, RMAX>(work, nrows, twr);
+    if (m >= 1) {
+      cp_async_wait_all();
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < G::NBL; ++j) {  // last pass + recombination in registers
+      const int bb = tid + j * NT, l = bb / G::TL, i = bb % G::TL;
+      if (l < nrows) {
+        double2 a[G::RL];
+#pragma unroll
+        for (int r = 0; r < G::RL; ++r) a[r] = work[l * G::LSR + padq<G::PADR>(i + r * G::TL)];
+        butterfly<h, G::PR - 1, +1>(a, i, twr);
+        const double2* dv2 = reinterpret_cast<const double2*>(devs + l * J1);
+#pragma unroll
+        for (int r = 0; r < G::RL; ++r) {
+          const int q = i + r * G::TL;  // x[2q], x[2q+1]
+          double v0 = a[r].x, v1 = a[r].y;
+          if (m >= 1) {
+            const double2 d = dv2[q];
+            v0 = d.x * v0;
+            v1 = d.y * v1;
+          }
+          double p0 = 0.0, p1 = 0.0;
+          p0 += v0;
+          p1 += v1;
+          acc[j][r][0] += p0;
+          acc[j][r][1] += p1;
+        }
+      }
+    }
+    signal_counter(&cR[t]);
+    if (m == M && !(prm.seismic && op == prm.nops - 1)) {  // operator complete: hand over
+#pragma unroll
+      for (int j = 0; j < G::NBL; ++j) {
+        const int bb = tid + j * NT, l = bb / G::TL, i = bb % G::TL;
+        if (l < nrows) {
+          double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)(r0 + l) * J1);
+#pragma unroll
+          for (int r = 0; r < G::RL; ++r) {
+            o[i + r * G::TL] = make_double2(acc[j][r][0], acc[j][r][1]);
+            acc[j][r][0] = acc[j][r][1] = 0.0;
+          }
+        }
+      }
     }
   };
 
@@ -470,34 +508,41 @@ __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
     row_term(t);
     if (t + KRING - 1 < ntot) column_term(t + KRING - 1);
   }
-  if (prm.residue && tid < nrows && rmax > 0.0)
+  if (prm.residue && rmax > 0.0)
     atomicMax(reinterpret_cast<unsigned long long*>(prm.residue), (unsigned long long)__double_as_longlong(rmax));
 
   // ------------------------------------------------ seismic update (seismic.cpp:116-129)
   if (prm.seismic) {
     bool bad = false;
-    const size_t base = (size_t)r0 * J1;
-    const double2* cur = reinterpret_cast<const double2*>(prm.u + base);
-    const double2* prev = reinterpret_cast<const double2*>(prm.prev + base);
-    const double2* ap = reinterpret_cast<const double2*>(prm.ap + base);
-    const double2* l1 = reinterpret_cast<const double2*>(prm.out[0] + base);
-    const double2* c = reinterpret_cast<const double2*>(prm.c + base);
-    const double2* eta = reinterpret_cast<const double2*>(prm.eta + base);
-    const double2* tc = reinterpret_cast<const double2*>(prm.tc + base);
-    double2* nx = reinterpret_cast<double2*>(prm.next + base);
-    double2* l2o = reinterpret_cast<double2*>(prm.out[1] + base);
-    const double2* al = reinterpret_cast<const double2*>(accs);
     const double tau = prm.tau;
     const double t2 = tau * tau;
-    for (int q = tid; q < nrows * J1 / 2; q += NT) {
-      const double2 vc = cur[q], vp = prev[q], va = ap[q], v1 = __ldcg(&l1[q]), cc = c[q], ve = eta[q], vt = tc[q];
-      const double2 l2 = al[q];
-      const double c2x = cc.x * cc.x, c2y = cc.y * cc.y;
-      const double nx0 = 2.0 * vc.x - vp.x + t2 * c2x * (ve.x * v1.x + vt.x * (l2.x - va.x) / tau);
-      const double nx1 = 2.0 * vc.y - vp.y + t2 * c2y * (ve.y * v1.y + vt.y * (l2.y - va.y) / tau);
-      nx[q] = make_double2(nx0, nx1);
-      l2o[q] = l2;
-      bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
+#pragma unroll
+    for (int j = 0; j < G::NBL; ++j) {
+      const int bb = tid + j * NT, l = bb / G::TL, i = bb % G::TL;
+      if (l < nrows) {
+        const size_t rowoff = (size_t)(r0 + l) * J1;
+        const double2* cur = reinterpret_cast<const double2*>(prm.u + rowoff);
+        const double2* prev = reinterpret_cast<const double2*>(prm.prev + rowoff);
+        const double2* ap = reinterpret_cast<const double2*>(prm.ap + rowoff);
+        const double2* l1 = reinterpret_cast<const double2*>(prm.out[0] + rowoff);
+        const double2* c = reinterpret_cast<const double2*>(prm.c + rowoff);
+        const double2* eta = reinterpret_cast<const double2*>(prm.eta + rowoff);
+        const double2* tc = reinterpret_cast<const double2*>(prm.tc + rowoff);
+        double2* nx = reinterpret_cast<double2*>(prm.next + rowoff);
+        double2* l2o = reinterpret_cast<double2*>(prm.out[1] + rowoff);
+#pragma unroll
+        for (int r = 0; r < G::RL; ++r) {
+          const int q = i + r * G::TL;
+          const double2 vc = cur[q], vp = prev[q], va = ap[q], v1 = l1[q], cc = c[q], ve = eta[q], vt = tc[q];
+          const double l2x = acc[j][r][0], l2y = acc[j][r][1];
+          const double c2x = cc.x * cc.x, c2y = cc.y * cc.y;
+          const double nx0 = 2.0 * vc.x - vp.x + t2 * c2x * (ve.x * v1.x + vt.x * (l2x - va.x) / tau);
+          const double nx1 = 2.0 * vc.y - vp.y + t2 * c2y * (ve.y * v1.y + vt.y * (l2y - va.y) / tau);
+          nx[q] = make_double2(nx0, nx1);
+          l2o[q] = make_double2(l2x, l2y);
+          bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
+        }
+      }
     }
     if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicMin(prm.flag, prm.step);
   }
@@ -506,6 +551,7 @@ __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
 template <int J0, int J1, int CG, int RMAX>
 cudaError_t launch_t(const Step2DParams& p, cudaStream_t st, int nblk) {
   using G = Geo<J0, J1, CG, RMAX>;
+  if ((J0 + nblk - 1) / nblk > RMAX || G::NG > nblk) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_step2d<J0, J1, CG, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
@@ -521,22 +567,20 @@ bool step2d_supported(int J0, int J1, int nsm) {
   if (!((J0 == 1024 && J1 == 1024) || (J0 == 512 && J1 == 512) || (J0 == 256 && J1 == 256) ||
         (J0 == 512 && J1 == 1024) || (J0 == 1024 && J1 == 512)))
     return false;
-  // every CTA must own at most RMAX rows and the column groups must fit the grid
   const int H = J1 / 2 + 1;
-  const int CG = 4;
-  const int ng = (H + CG - 1) / CG;
-  return ng <= nsm && (J0 + nsm - 1) / nsm <= 8;
+  const int ng = (H + kStep2dCG - 1) / kStep2dCG;
+  return nsm >= 148 && ng <= nsm;
 }
 
-int step2d_col_groups(int J1) { return (J1 / 2 + 1 + 3) / 4; }
+int step2d_col_groups(int J1) { return (J1 / 2 + 1 + kStep2dCG - 1) / kStep2dCG; }
 
 cudaError_t launch_step2d(const Step2DParams& p, cudaStream_t st, int nsm) {
   const int J0 = p.J0, J1 = p.J1;
-  if (J0 == 1024 && J1 == 1024) return s2d::launch_t<1024, 1024, 4, 8>(p, st, nsm);
-  if (J0 == 512 && J1 == 512) return s2d::launch_t<512, 512, 4, 8>(p, st, nsm);
-  if (J0 == 256 && J1 == 256) return s2d::launch_t<256, 256, 4, 8>(p, st, nsm);
-  if (J0 == 512 && J1 == 1024) return s2d::launch_t<512, 1024, 4, 8>(p, st, nsm);
-  if (J0 == 1024 && J1 == 512) return s2d::launch_t<1024, 512, 4, 8>(p, st, nsm);
+  if (J0 == 1024 && J1 == 1024) return s2d::launch_t<1024, 1024, 4, 7>(p, st, nsm);
+  if (J0 == 512 && J1 == 512) return s2d::launch_t<512, 512, 4, 4>(p, st, nsm);
+  if (J0 == 256 && J1 == 256) return s2d::launch_t<256, 256, 4, 2>(p, st, nsm);
+  if (J0 == 512 && J1 == 1024) return s2d::launch_t<512, 1024, 4, 4>(p, st, nsm);
+  if (J0 == 1024 && J1 == 512) return s2d::launch_t<1024, 512, 4, 7>(p, st, nsm);
   return cudaErrorInvalidValue;
 }
 
