@@ -1,26 +1,28 @@
-// fw_step2d.cu — persistent single-launch 2D apply / seismic step for sm_100a.
+// fw_step2d.cu — persistent, warp-specialised single-launch 2D apply / seismic step (sm_100a).
 //
 // One cooperative launch of one CTA per SM does the whole seismic step (or one
-// operator apply) on a J0 x J1 grid (half spectrum H = J1/2 + 1 columns):
+// operator apply) on a J0 x J1 grid (half spectrum H = J1/2 + 1 columns).  CTA b
+// owns 4 half-spectrum columns (group b) and RMAX rows.  Its warps are
+// specialised and progress independently (no CTA-wide barrier after setup):
 //
-//   F1  every CTA: R2C of its rows of u                        -> Y (global, L2)
-//   --- grid counter ---
-//   F2  column CTAs: C2C of their CG columns of Y, x 1/N       -> uhat (SHARED MEMORY, kept)
-//   for t = (op, m), m = m_first..M of every operator, pipelined through a K-slot ring:
-//     C(t) column CTAs: (w_m .* uhat) -> inverse C2C          -> T[t mod K] (global, L2)
-//     R(t) every CTA : T rows -> C2R (pre-processing fused into the first pass)
-//                      -> acc += (s-s0)^m .* x  (accumulators in registers,
-//                      (s-s0)^m rows staged into shared memory by cp.async)
-//   update (seismic.cpp:116-129) from the registers: next, new L2prev, blow-up flag
+//   column warps (4, one column each)            row warps (RMAX, one row each)
+//   F2: wait all rows -> C2C of its column of     F1: R2C of its row of u -> Y row
+//       Y (x 1/N) -> uhat column (SHARED MEM,     R(t), t = (op, m) in order:
+//       kept for the whole step)                     wait all columns of T[t%3];
+//   C(t), t = (op, m) in order:                      C2R with the pre-processing
+//       wait T slot free (rows of t-3 done);         fused into its loads; acc +=
+//       IFFT(w_m .* uhat) ; the 4 warps                (s-s0)^m .* x in registers
+//       transpose through smem and store           update (seismic.cpp:116-129)
+//       64-byte row chunks of T[t%3]                  from the registers
 //
-// The term intermediate T is the only global round trip per term (a 2D FFT is
-// an all-to-all across SMs); the forward spectrum and the accumulators never
-// leave the SM.  CTAs order themselves with monotone per-term counters
-// (red.release / ld.acquire); the ring lets column work run K-1 terms ahead of
-// row work.  Arithmetic is the canonical FFT of fw_fft.cuh (radix plan, twiddle
-// values, fma placement), so results are bit-identical to the multi-pass path
-// and to the CPU oracle.  Twiddles of every pass live in shared memory in a
-// [k][r-1] layout (odd stride: conflict-free).
+// Producer/consumer ordering between warps of all CTAs uses monotone counters
+// counted in rows / columns (red.release.gpu / ld.acquire.gpu), two counter sets
+// alternating between launches.  Only the term intermediate T round-trips
+// through global memory (a 2D FFT is an all-to-all across SMs).
+// Arithmetic is the canonical FFT of fw_fft.cuh (radix plan, twiddle values,
+// fma placement): results are bit-identical to the multi-pass path and to the
+// CPU oracle.  Per-pass twiddle tables live in shared memory in a [k][r-1]
+// layout (odd stride, conflict-free).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,8 +33,8 @@
 namespace fw {
 namespace s2d {
 
-constexpr int NT = 256;  // threads per CTA (8 warps, up to 255 registers each)
 constexpr int KRING = 3;
+constexpr int NWC = 4;  // column warps per CTA (= columns per CTA)
 
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
 __host__ __device__ constexpr int npass(int n) { return (ilog2c(n) + 3) / 4; }
@@ -41,7 +43,6 @@ __host__ __device__ constexpr int radix(int n, int i) {
 }
 __host__ __device__ constexpr int pprod(int n, int i) { return i == 0 ? 1 : pprod(n, i - 1) * radix(n, i - 1); }
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
-// per-pass twiddle table sizes / offsets of an N-point plan (pass 0 has none)
 __host__ __device__ constexpr int twsize(int n, int pass) { return pass == 0 ? 0 : pprod(n, pass) * (radix(n, pass) - 1); }
 __host__ __device__ constexpr int twoff(int n, int pass) { return pass <= 1 ? 0 : twoff(n, pass - 1) + twsize(n, pass - 1); }
 __host__ __device__ constexpr int twtotal(int n) { return twoff(n, npass(n) - 1) + twsize(n, npass(n) - 1); }
@@ -55,33 +56,28 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void wait_counter(const unsigned long long* cnt, unsigned long long target) {
-  if (threadIdx.x == 0) {
+// whole warp waits until *cnt >= target
+__device__ __forceinline__ void warp_wait(const unsigned long long* cnt, unsigned long long target) {
+  if ((threadIdx.x & 31) == 0) {
     while (ld_acquire(cnt) < target) __nanosleep(20);
   }
-  __syncthreads();
+  __syncwarp();
 }
-__device__ __forceinline__ void signal_counter(unsigned long long* cnt) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
+// the warp's global writes are done -> publish v
+__device__ __forceinline__ void warp_signal(unsigned long long* cnt, unsigned long long v) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
     __threadfence();
-    red_release_add(cnt, 1ull);
+    red_release_add(cnt, v);
   }
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void colbar() { asm volatile("bar.sync 1, %0;" ::"n"(NWC * 32) : "memory"); }
 
 template <int DIR>
 __device__ __forceinline__ double2 dirw(double2 w) {
   return make_double2(w.x, DIR < 0 ? -w.y : w.y);
 }
 
-// Stockham butterfly of pass PASS (N-point plan) on register array a (butterfly i);
-// tw = this N's per-pass table block.
 template <int N, int PASS, int DIR>
 __device__ __forceinline__ void butterfly(double2* a, int i, const double2* tw) {
   constexpr int R = radix(N, PASS);
@@ -111,123 +107,28 @@ __device__ __forceinline__ int padq(int q) {
   return q + (q >> PADSH);
 }
 
-template <int T, bool LINE_FAST, int NLC>
-__device__ __forceinline__ void bmap(int b, int& l, int& i) {
-  if constexpr (LINE_FAST) {
-    l = b % NLC;
-    i = b / NLC;
-  } else {
-    l = b / T;
-    i = b % T;
-  }
-}
-
-// Middle pass PASS of an N-point C2C over nl lines, in place in shared memory.
-template <int N, int PASS, int DIR, int PADSH, int LS, bool LINE_FAST, int NLMAX>
-__device__ __forceinline__ void smem_pass(double2* buf, int nl, const double2* tw) {
+// Middle pass PASS of an N-point C2C held by ONE warp in buf (padded), in place.
+template <int N, int PASS, int DIR, int PADSH>
+__device__ __forceinline__ void warp_pass(double2* buf, const double2* tw) {
   constexpr int R = radix(N, PASS);
   constexpr int T = N / R;
-  constexpr int NB = cdiv(NLMAX * T, NT);
-  const int tid = threadIdx.x;
+  constexpr int NB = T / 32;
+  static_assert(T % 32 == 0, "warp pass needs >= 32 butterflies");
+  const int lane = threadIdx.x & 31;
   double2 a[NB][R];
 #pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    int l, i;
-    bmap<T, LINE_FAST, NLMAX>(tid + j * NT, l, i);
-    if (l < nl && i < T) {
+  for (int j = 0; j < NB; ++j)
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[j][r] = buf[l * LS + padq<PADSH>(i + r * T)];
-    }
-  }
-  __syncthreads();
+    for (int r = 0; r < R; ++r) a[j][r] = buf[padq<PADSH>(lane + 32 * j + r * T)];
+  __syncwarp();
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
-    int l, i;
-    bmap<T, LINE_FAST, NLMAX>(tid + j * NT, l, i);
-    if (l < nl && i < T) {
-      butterfly<N, PASS, DIR>(a[j], i, tw);
+    const int i = lane + 32 * j;
+    butterfly<N, PASS, DIR>(a[j], i, tw);
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[l * LS + padq<PADSH>(out_index<N, PASS>(i, r))] = a[j][r];
-    }
+    for (int r = 0; r < R; ++r) buf[padq<PADSH>(out_index<N, PASS>(i, r))] = a[j][r];
   }
-  __syncthreads();
-}
-
-// --------------------------------------------------------------------------
-template <int J0, int J1, int CG, int RMAX>
-struct Geo {
-  static constexpr int H = J1 / 2 + 1;               // half-spectrum columns
-  static constexpr int h = J1 / 2;                   // row C2C length
-  static constexpr int NG = (H + CG - 1) / CG;       // column groups
-  static constexpr int PADC = ilog2c(radix(J0, 0));  // column pad shift
-  static constexpr int PADR = ilog2c(radix(h, 0));   // row pad shift
-  static constexpr int LSU = J0 + (CG == 4 ? 2 : CG == 2 ? 4 : 1);
-  static constexpr int LSC0 = J0 + (J0 >> PADC);
-  static constexpr int LSC = LSC0 + ((10 - LSC0 % 8) % 8);  // == 2 mod 8
-  static constexpr int LSR = h + (h >> PADR) + 2;
-  static constexpr int PC = npass(J0);
-  static constexpr int PR = npass(h);
-  static constexpr int RL = radix(h, PR - 1);  // last row pass
-  static constexpr int TL = h / RL;
-  static constexpr int NBL = cdiv(RMAX * TL, NT);  // last-pass butterflies per thread
-  static constexpr int TWC = twtotal(J0);
-  static constexpr int TWR = twtotal(h);
-  static constexpr int TWP = h + 1;  // W_J1^k, k = 0..h
-  static constexpr size_t SMEM_TW = sizeof(double2) * (TWC + TWR + TWP);
-  static constexpr size_t SMEM_U = sizeof(double2) * CG * LSU;
-  static constexpr size_t SMEM_W = sizeof(double2) * (CG * LSC > RMAX * LSR ? CG * LSC : RMAX * LSR);
-  static constexpr size_t SMEM_D = sizeof(double) * RMAX * J1;  // (s-s0)^m staging
-  static constexpr size_t SMEM = SMEM_TW + SMEM_U + SMEM_W + SMEM_D;
-  static_assert(PC <= 3 && PR <= 3 && PR >= 2 && PC >= 2, "2 or 3 passes per FFT");
-  static_assert(SMEM <= 227 * 1024, "shared memory budget");
-};
-
-// ---------------------------------------------------------------- column FFT
-// J0-point C2C of the CTA's CG columns (lines interleaved fastest).  Pass 0 reads
-// src(cc, q); the last pass writes sink(cc, q, value) in natural order q.
-template <int J0, int CG, int DIR, int PADSH, int LSC, class Src, class Sink>
-__device__ __forceinline__ void column_fft(double2* cbuf, const double2* tw, int ncols, Src src, Sink sink) {
-  constexpr int P = npass(J0);
-  const int tid = threadIdx.x;
-  {
-    constexpr int R = radix(J0, 0);
-    constexpr int T = J0 / R;
-    constexpr int NB = cdiv(CG * T, NT);
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      int cc, i;
-      bmap<T, true, CG>(tid + j * NT, cc, i);
-      if (i < T && cc < ncols) {
-        double2 a[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) a[r] = src(cc, i + r * T);
-        Dft<R, DIR>::run(a);
-#pragma unroll
-        for (int r = 0; r < R; ++r) cbuf[cc * LSC + padq<PADSH>(i * R + r)] = a[r];
-      }
-    }
-    __syncthreads();
-  }
-  if constexpr (P == 3) smem_pass<J0, 1, DIR, PADSH, LSC, true, CG>(cbuf, CG, tw);
-  {
-    constexpr int PL = P - 1;
-    constexpr int R = radix(J0, PL);
-    constexpr int T = J0 / R;
-    constexpr int NB = cdiv(CG * T, NT);
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      int cc, i;
-      bmap<T, true, CG>(tid + j * NT, cc, i);
-      if (i < T && cc < ncols) {
-        double2 a[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) a[r] = cbuf[cc * LSC + padq<PADSH>(i + r * T)];
-        butterfly<J0, PL, DIR>(a, i, tw);
-#pragma unroll
-        for (int r = 0; r < R; ++r) sink(cc, i + r * T, a[r]);
-      }
-    }
-  }
+  __syncwarp();
 }
 
 // R2C post-processing X[k] from Z[k], Z[h-k] (fwcanon fwc_r2c), 1 <= k < h
@@ -254,35 +155,107 @@ __device__ __forceinline__ double2 pre_c2r(double2 A, double2 Xhk, bool k0, doub
   return make_double2(E.x - O.y, E.y + O.x);
 }
 
+// joint column-transpose area: element (k0, cc) of the CTA's 4 columns, XOR swizzled
+__device__ __forceinline__ int jidx(int k0, int cc) { return k0 * 4 + (cc ^ ((k0 >> 1) & 3)); }
+
 // --------------------------------------------------------------------------
-template <int J0, int J1, int CG, int RMAX>
-__global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
-  using G = Geo<J0, J1, CG, RMAX>;
-  constexpr int H = G::H, h = G::h;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* twc = reinterpret_cast<double2*>(smem_raw);  // column plan tables
-  double2* twr = twc + G::TWC;                          // row plan tables
-  double2* twp = twr + G::TWR;                          // W_J1^k
-  double2* uhat = reinterpret_cast<double2*>(smem_raw + G::SMEM_TW);
-  double2* work = reinterpret_cast<double2*>(smem_raw + G::SMEM_TW + G::SMEM_U);
-  double* devs = reinterpret_cast<double*>(smem_raw + G::SMEM_TW + G::SMEM_U + G::SMEM_W);
+template <int J0, int J1, int RMAX>
+struct Geo {
+  static constexpr int H = J1 / 2 + 1;
+  static constexpr int h = J1 / 2;
+  static constexpr int NG = (H + NWC - 1) / NWC;
+  static constexpr int NT = 32 * (NWC + RMAX);
+  static constexpr int PADC = ilog2c(radix(J0, 0));
+  static constexpr int PADR = ilog2c(radix(h, 0));
+  static constexpr int LCOL = J0 + (J0 >> PADC) + 2;  // per column-warp work buffer
+  static constexpr int LROW = h + (h >> PADR) + 2;    // per row-warp work buffer
+  static constexpr int PC = npass(J0);
+  static constexpr int PR = npass(h);
+  static constexpr int TWC = twtotal(J0);
+  static constexpr int TWR = twtotal(h);
+  static constexpr int TWP = h + 1;
+  static constexpr size_t OFF_TWR = TWC;
+  static constexpr size_t OFF_TWP = TWC + TWR;
+  static constexpr size_t OFF_U = TWC + TWR + TWP;         // uhat [4][J0]
+  static constexpr size_t OFF_CW = OFF_U + (size_t)NWC * J0;  // column work [4][LCOL]
+  static constexpr size_t OFF_RW = OFF_CW + (size_t)NWC * LCOL;  // row work [RMAX][LROW]
+  static constexpr size_t NELEM = OFF_RW + (size_t)RMAX * LROW;
+  static constexpr size_t SMEM = NELEM * sizeof(double2);
+  static_assert(PC >= 2 && PC <= 3 && PR >= 2 && PR <= 3, "2 or 3 passes per FFT");
+  static_assert(NWC * LCOL >= 4 * J0 && NWC * J0 >= 4 * J0, "joint transpose area");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(h / radix(h, 0) == 64 || h / radix(h, 0) == 32, "row pass-0 lane mapping");
+};
+
+// ---------------------------------------------------------------- column warp: J0-point C2C
+// pass 0 from src(q) (q = i + r*T0); the last pass writes each butterfly's outputs
+// back to the slots it read, so `work` ends holding the column in natural order
+// (padded).  The caller passes `sync0` to separate pass 0 from the rest when the
+// source is shared with other warps.
+template <int J0, int DIR, int PADSH, class Src, class Sync0>
+__device__ __forceinline__ void column_c2c(double2* work, const double2* tw, Src src, Sync0 sync0) {
+  constexpr int P = npass(J0);
+  const int lane = threadIdx.x & 31;
+  {
+    constexpr int R = radix(J0, 0);
+    constexpr int T = J0 / R;
+#pragma unroll
+    for (int j = 0; j < T / 32; ++j) {
+      const int i = lane + 32 * j;
+      double2 a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = src(i + r * T);
+      Dft<R, DIR>::run(a);
+#pragma unroll
+      for (int r = 0; r < R; ++r) work[padq<PADSH>(i * R + r)] = a[r];
+    }
+    sync0();
+    __syncwarp();
+  }
+  if constexpr (P == 3) warp_pass<J0, 1, DIR, PADSH>(work, tw);
+  {
+    constexpr int PL = P - 1;
+    constexpr int R = radix(J0, PL);
+    constexpr int T = J0 / R;
+#pragma unroll
+    for (int j = 0; j < T / 32; ++j) {
+      const int i = lane + 32 * j;
+      double2 a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = work[padq<PADSH>(i + r * T)];
+      butterfly<J0, PL, DIR>(a, i, tw);
+#pragma unroll
+      for (int r = 0; r < R; ++r) work[padq<PADSH>(i + r * T)] = a[r];
+    }
+    __syncwarp();
+  }
+}
+
+// --------------------------------------------------------------------------
+template <int J0, int J1, int RMAX>
+__global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2DParams prm) {
+  using G = Geo<J0, J1, RMAX>;
+  constexpr int H = G::H, h = G::h, NT = G::NT;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* twc = sm;
+  double2* twr = sm + G::OFF_TWR;
+  double2* twp = sm + G::OFF_TWP;
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.x;
   const int nblk = gridDim.x;
 
-  // counters: this launch uses set `cset`, and clears the other set for the next launch
   unsigned long long* cnt = prm.counters + (size_t)prm.cset * prm.cstride;
   if (b == 0) {
     unsigned long long* other = prm.counters + (size_t)(prm.cset ^ 1) * prm.cstride;
     for (int e = tid; e < prm.cstride; e += NT) other[e] = 0ull;
   }
   if (prm.flag && *prm.flag != kNoBlowup) return;  // uniform across CTAs
-  unsigned long long* cY = cnt;
-  unsigned long long* cC = cnt + 1;
-  unsigned long long* cR = cnt + 1 + prm.nterms_total;
+  unsigned long long* cY = cnt;                          // rows forward-transformed
+  unsigned long long* cC = cnt + 1;                      // columns of T[t] stored
+  unsigned long long* cR = cnt + 1 + prm.nterms_total;  // rows of T[t] consumed
 
-  // twiddle tables (values = master entries, identical to fw_fft.cuh's twiddle())
-  {
+  {  // twiddle tables (values = master entries, identical to fw_fft.cuh's twiddle())
     auto fill = [&](double2* dst, int off, int p, int R) {
       const int n = p * (R - 1);
       for (int e = tid; e < n; e += NT) {
@@ -290,282 +263,285 @@ __global__ void __launch_bounds__(NT, 1) k_step2d(const Step2DParams prm) {
         dst[off + e] = prm.master[(r * k) * (kTwMaster / (p * R))];
       }
     };
-    if constexpr (G::PC >= 2) fill(twc, twoff(J0, 1), pprod(J0, 1), radix(J0, 1));
+    fill(twc, twoff(J0, 1), pprod(J0, 1), radix(J0, 1));
     if constexpr (G::PC >= 3) fill(twc, twoff(J0, 2), pprod(J0, 2), radix(J0, 2));
-    if constexpr (G::PR >= 2) fill(twr, twoff(h, 1), pprod(h, 1), radix(h, 1));
+    fill(twr, twoff(h, 1), pprod(h, 1), radix(h, 1));
     if constexpr (G::PR >= 3) fill(twr, twoff(h, 2), pprod(h, 2), radix(h, 2));
     for (int e = tid; e <= h; e += NT) twp[e] = prm.master[e * (kTwMaster / J1)];
   }
-
-  const int r0 = (int)(((long long)b * J0) / nblk);
-  const int r1 = (int)(((long long)(b + 1) * J0) / nblk);
-  const int nrows = r1 - r0;
-  const bool has_cols = b < G::NG;
-  const int c0 = b * CG;
-  const int ncols = has_cols ? min(CG, H - c0) : 0;
   __syncthreads();
 
-  // ------------------------------------------------ F1: forward rows -> Y
-  {
-    constexpr int R0 = radix(h, 0);
-    constexpr int T0 = h / R0;
-    constexpr int NB0 = cdiv(RMAX * T0, NT);
-    const double2* u2 = reinterpret_cast<const double2*>(prm.u);
-#pragma unroll
-    for (int j = 0; j < NB0; ++j) {  // pass 0 straight from global: packed pairs z_q = x_2q + i x_2q+1
-      const int bb = tid + j * NT, l = bb / T0, i = bb % T0;
-      if (l < nrows) {
-        double2 a[R0];
-#pragma unroll
-        for (int r = 0; r < R0; ++r) a[r] = u2[(size_t)(r0 + l) * h + i + r * T0];
-        Dft<R0, -1>::run(a);
-#pragma unroll
-        for (int r = 0; r < R0; ++r) work[l * G::LSR + padq<G::PADR>(i * R0 + r)] = a[r];
-      }
-    }
-    __syncthreads();
-    if constexpr (G::PR == 3) smem_pass<h, 1, -1, G::PADR, G::LSR, false, RMAX>(work, nrows, twr);
-#pragma unroll
-    for (int j = 0; j < G::NBL; ++j) {  // last pass, written back to the slots it read
-      const int bb = tid + j * NT, l = bb / G::TL, i = bb % G::TL;
-      if (l < nrows) {
-        double2 a[G::RL];
-#pragma unroll
-        for (int r = 0; r < G::RL; ++r) a[r] = work[l * G::LSR + padq<G::PADR>(i + r * G::TL)];
-        butterfly<h, G::PR - 1, -1>(a, i, twr);
-#pragma unroll
-        for (int r = 0; r < G::RL; ++r) work[l * G::LSR + padq<G::PADR>(i + r * G::TL)] = a[r];
-      }
-    }
-    __syncthreads();
-    constexpr int NP = h / 2 + 1;
-    for (int l = 0; l < nrows; ++l) {  // post-process pairs (k, h-k)
-      const double2* Z = work + l * G::LSR;
-      double2* Yr = prm.Y + (size_t)(r0 + l) * H;
-      for (int jj = tid; jj < NP; jj += NT) {
-        if (jj == 0) {
-          const double2 z0 = Z[0];
-          __stcg(&Yr[0], make_double2(z0.x + z0.y, 0.0));
-          __stcg(&Yr[h], make_double2(z0.x - z0.y, 0.0));
-        } else {
-          const double2 A = Z[padq<G::PADR>(jj)];
-          const double2 B = Z[padq<G::PADR>(h - jj)];
-          __stcg(&Yr[jj], post_r2c(A, B, twp[jj]));
-          if (jj != h - jj) __stcg(&Yr[h - jj], post_r2c(B, A, twp[h - jj]));
-        }
-      }
-    }
-    signal_counter(cY);
-  }
-
-  // ------------------------------------------------ F2: forward columns -> uhat (smem)
-  if (has_cols) {
-    wait_counter(cY, (unsigned long long)nblk);
-    const double inv = 1.0 / ((double)J0 * (double)J1);
-    const double2* Y = prm.Y;
-    column_fft<J0, CG, -1, G::PADC, G::LSC>(
-        work, twc, ncols, [&](int cc, int q) { return __ldcg(&Y[(size_t)q * H + c0 + cc]); },
-        [&](int cc, int q, double2 v) { uhat[cc * G::LSU + q] = make_double2(v.x * inv, v.y * inv); });
-    __syncthreads();
-  }
-
-  // ------------------------------------------------ terms
   const int M = prm.M;
   const int nterms = M + 1 - prm.m_first;
   const int ntot = prm.nops * nterms;
 
-  auto column_term = [&](int t) {
-    if (!has_cols) return;
-    if (t >= KRING) wait_counter(&cR[t - KRING], (unsigned long long)nblk);
-    const int op = t / nterms;
-    const int m = prm.m_first + t % nterms;
-    const double* w = prm.w[op] + ((size_t)m * G::NG + b) * (size_t)J0 * CG;  // [m][g][k0][CG]
-    double2* T = prm.T + (size_t)(t % KRING) * J0 * H;
-    column_fft<J0, CG, +1, G::PADC, G::LSC>(
-        work, twc, ncols,
-        [&](int cc, int q) {
-          const double2 v = uhat[cc * G::LSU + q];
-          const double wk = __ldg(&w[(size_t)q * CG + cc]);
-          return make_double2(wk * v.x, wk * v.y);
-        },
-        [&](int cc, int q, double2 v) { __stcg(&T[(size_t)q * H + c0 + cc], v); });
-    signal_counter(&cC[t]);
-  };
+  if (warp < NWC) {
+    // ============================================ column warps
+    if (b >= G::NG) return;
+    const int cw = warp;
+    const int c0 = b * NWC;
+    const int c = c0 + cw;
+    const int ncols = min(NWC, H - c0);
+    const bool valid = c < H;
+    double2* uhat = sm + G::OFF_U + (size_t)cw * J0;
+    double2* work = sm + G::OFF_CW + (size_t)cw * G::LCOL;
+    double2* works = sm + G::OFF_CW;  // the 4 column work buffers (line stride LCOL)
+    double2* joint_u = sm + G::OFF_U;  // F2 staging (uhat not yet valid)
+    const int ct = tid;                // 0..127 within the column warps
 
-  double acc[G::NBL][G::RL][2];
-#pragma unroll
-  for (int j = 0; j < G::NBL; ++j)
-#pragma unroll
-    for (int r = 0; r < G::RL; ++r) acc[j][r][0] = acc[j][r][1] = 0.0;
+    // ---- F2: forward columns -> uhat
+    warp_wait(cY, (unsigned long long)J0);
+    colbar();  // all 4 column warps have seen every row
+    for (int e = ct; e < J0 * 4; e += NWC * 32) {
+      const int k0 = e >> 2, cc = e & 3;
+      joint_u[jidx(k0, cc)] = (c0 + cc < H) ? __ldcg(&prm.Y[(size_t)k0 * H + c0 + cc]) : make_double2(0.0, 0.0);
+    }
+    colbar();
+    // pass 0 reads joint_u (shared by the 4 warps): barrier before uhat is overwritten
+    column_c2c<J0, -1, G::PADC>(work, twc, [&](int q) { return joint_u[jidx(q, cw)]; }, [] { colbar(); });
+    {
+      const double inv = 1.0 / ((double)J0 * (double)J1);
+      for (int q = lane; q < J0; q += 32) {
+        const double2 v = work[padq<G::PADC>(q)];
+        uhat[q] = make_double2(v.x * inv, v.y * inv);
+      }
+      __syncwarp();
+    }
 
+    // ---- C(t): inverse columns -> T[t % KRING]
+    for (int t = 0; t < ntot; ++t) {
+      const int op = t / nterms;
+      const int m = prm.m_first + t % nterms;
+      if (t >= KRING) warp_wait(&cR[t - KRING], (unsigned long long)J0);
+      const double* w = prm.w[op] + ((size_t)m * (G::NG * NWC) + c) * J0;  // [m][c][k0]
+      column_c2c<J0, +1, G::PADC>(
+          work, twc,
+          [&](int q) {
+            const double2 v = uhat[q];
+            const double wk = valid ? __ldg(&w[q]) : 0.0;
+            return make_double2(wk * v.x, wk * v.y);
+          },
+          [] {});
+      colbar();  // the 4 columns are complete in the 4 work buffers
+      double2* T = prm.T + (size_t)(t % KRING) * J0 * H;
+      for (int e = ct; e < J0 * 4; e += NWC * 32) {  // 64-byte row chunks of the 4 columns
+        const int k0 = e >> 2, cc = e & 3;
+        if (cc < ncols) __stcg(&T[(size_t)k0 * H + c0 + cc], works[cc * G::LCOL + padq<G::PADC>(k0)]);
+      }
+      colbar();  // stores issued by all 128 threads; work buffers free again
+      if (ct == 0) {
+        __threadfence();
+        red_release_add(&cC[t], (unsigned long long)ncols);
+      }
+    }
+    return;
+  }
+
+  // ============================================ row warps
+  const int rw = warp - NWC;
+  const int r0 = (int)(((long long)b * J0) / nblk);
+  const int r1 = (int)(((long long)(b + 1) * J0) / nblk);
+  if (rw >= r1 - r0) return;
+  const int row = r0 + rw;
+  double2* work = sm + G::OFF_RW + (size_t)rw * G::LROW;
+  constexpr int R0 = radix(h, 0);
+  constexpr int T0 = h / R0;
+  constexpr int RL = radix(h, G::PR - 1);
+  constexpr int TL = h / RL;
+  constexpr int NBL = TL / 32;
+  static_assert(TL % 32 == 0, "row last pass");
+
+  // ---- F1: R2C of the row -> Y
+  {
+    const double2* u2 = reinterpret_cast<const double2*>(prm.u) + (size_t)row * h;
+#pragma unroll
+    for (int j = 0; j < T0 / 32; ++j) {
+      const int i = lane + 32 * j;
+      double2 a[R0];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) a[r] = u2[i + r * T0];
+      Dft<R0, -1>::run(a);
+#pragma unroll
+      for (int r = 0; r < R0; ++r) work[padq<G::PADR>(i * R0 + r)] = a[r];
+    }
+    __syncwarp();
+    if constexpr (G::PR == 3) warp_pass<h, 1, -1, G::PADR>(work, twr);
+#pragma unroll
+    for (int j = 0; j < NBL; ++j) {
+      const int i = lane + 32 * j;
+      double2 a[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) a[r] = work[padq<G::PADR>(i + r * TL)];
+      butterfly<h, G::PR - 1, -1>(a, i, twr);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) work[padq<G::PADR>(i + r * TL)] = a[r];
+    }
+    __syncwarp();
+    double2* Yr = prm.Y + (size_t)row * H;
+    for (int jj = lane; jj <= h / 2; jj += 32) {
+      if (jj == 0) {
+        const double2 z0 = work[0];
+        __stcg(&Yr[0], make_double2(z0.x + z0.y, 0.0));
+        __stcg(&Yr[h], make_double2(z0.x - z0.y, 0.0));
+      } else {
+        const double2 A = work[padq<G::PADR>(jj)];
+        const double2 B = work[padq<G::PADR>(h - jj)];
+        __stcg(&Yr[jj], post_r2c(A, B, twp[jj]));
+        if (jj != h - jj) __stcg(&Yr[h - jj], post_r2c(B, A, twp[h - jj]));
+      }
+    }
+    warp_signal(cY, 1ull);
+  }
+
+  // ---- R(t): C2R + recombination
+  double acc[NBL][RL][2];
+#pragma unroll
+  for (int j = 0; j < NBL; ++j)
+#pragma unroll
+    for (int r = 0; r < RL; ++r) acc[j][r][0] = acc[j][r][1] = 0.0;
   double rmax = 0.0;
-  auto row_term = [&](int t) {
-    wait_counter(&cC[t], (unsigned long long)G::NG);
+
+  for (int t = 0; t < ntot; ++t) {
     const int op = t / nterms;
     const int m = prm.m_first + t % nterms;
-    const double2* T = prm.T + (size_t)(t % KRING) * J0 * H;
-    if (m >= 1) {  // stage (s-s0)^m rows asynchronously
-      const double* dv = prm.dev[op] + (size_t)(m - 1) * J0 * J1 + (size_t)r0 * J1;
-      const int nchunk = nrows * J1 / 2;
-      for (int e = tid; e < nchunk; e += NT) cp_async16(devs + 2 * e, dv + 2 * e);
-      cp_async_commit();
-    }
-    {  // pass 0 with the C2R pre-processing fused: unit i pairs butterflies i and T0-i
-      constexpr int R0 = radix(h, 0);
-      constexpr int T0 = h / R0;
-      constexpr int NU = T0 / 2 + 1;  // units per row
-      constexpr int NBU = cdiv(RMAX * NU, NT);
+    warp_wait(&cC[t], (unsigned long long)H);
+    const double2* X = prm.T + (size_t)(t % KRING) * J0 * H + (size_t)row * H;
+    // pass 0 with the pre-processing fused.  Butterfly i needs X[i + r T0] and
+    // X[h - i - r T0] = X[(T0 - i) + (R0-1-r) T0]: lane L takes butterflies L and
+    // T0-L (lane 0: butterflies 0 and T0/2, both self-contained) -- every X once.
+    static_assert(T0 == 64, "pass-0 pairing assumes 64 butterflies");
+    {
+      const int i1 = lane;                        // 0..31
+      const int i2 = (lane == 0) ? T0 / 2 : T0 - lane;
+      double2 XA[R0], XB[R0];
 #pragma unroll
-      for (int j = 0; j < NBU; ++j) {
-        const int bb = tid + j * NT, l = bb / NU, i = bb % NU;
-        if (l < nrows) {
-          const double2* X = T + (size_t)(r0 + l) * H;
-          const int i2 = T0 - i;  // mirror butterfly; for i == 0 this walks X[T0 (r+1)], ending at X[h]
-          double2 XA[R0], XB[R0];
+      for (int r = 0; r < R0; ++r) XA[r] = __ldcg(&X[i1 + r * T0]);
 #pragma unroll
-          for (int r = 0; r < R0; ++r) XA[r] = __ldcg(&X[i + r * T0]);
+      for (int r = 0; r < R0; ++r) XB[r] = __ldcg(&X[i2 + r * T0]);
+      double2 xh = make_double2(0.0, 0.0);
+      if (lane == 0) xh = __ldcg(&X[h]);
+      double2 a[R0];
+      if (lane == 0) {
+        if (prm.residue) rmax = fmax(rmax, fabs(XA[0].y) + fabs(xh.y));
+        // butterfly 0: k = r T0, h-k = (R0-r) T0 -> XA[R0-r] (r >= 1), X[h] (r = 0)
 #pragma unroll
-          for (int r = 0; r < R0; ++r) XB[r] = __ldcg(&X[i2 + r * T0]);
-          double2 a[R0];
-          if (i == 0) {
-            if (prm.residue) rmax = fmax(rmax, fabs(XA[0].y) + fabs(XB[R0 - 1].y));
+        for (int r = 0; r < R0; ++r) a[r] = pre_c2r(XA[r], r == 0 ? xh : XA[R0 - r], r == 0, twp[r * T0]);
+        Dft<R0, +1>::run(a);
 #pragma unroll
-            for (int r = 0; r < R0; ++r)  // k = r*T0, h-k = (R0-r)*T0 = XB[R0-1-r]
-              a[r] = pre_c2r(XA[r], XB[R0 - 1 - r], r == 0, twp[r * T0]);
-            Dft<R0, +1>::run(a);
+        for (int r = 0; r < R0; ++r) work[padq<G::PADR>(r)] = a[r];
+        // butterfly T0/2 (self-mirror): h-k = T0/2 + (R0-1-r) T0 -> XB[R0-1-r]
 #pragma unroll
-            for (int r = 0; r < R0; ++r) work[l * G::LSR + padq<G::PADR>(r)] = a[r];
-          } else {
-            // butterfly i: k = i + r*T0, h-k = (T0-i) + (R0-1-r)*T0 -> XB[R0-1-r]
+        for (int r = 0; r < R0; ++r) a[r] = pre_c2r(XB[r], XB[R0 - 1 - r], false, twp[T0 / 2 + r * T0]);
+        Dft<R0, +1>::run(a);
 #pragma unroll
-            for (int r = 0; r < R0; ++r) a[r] = pre_c2r(XA[r], XB[R0 - 1 - r], false, twp[i + r * T0]);
-            Dft<R0, +1>::run(a);
+        for (int r = 0; r < R0; ++r) work[padq<G::PADR>((T0 / 2) * R0 + r)] = a[r];
+      } else {
 #pragma unroll
-            for (int r = 0; r < R0; ++r) work[l * G::LSR + padq<G::PADR>(i * R0 + r)] = a[r];
-            if (i2 != i) {  // butterfly T0-i: k = i2 + r*T0, h-k = i + (R0-1-r)*T0 -> XA[R0-1-r]
+        for (int r = 0; r < R0; ++r) a[r] = pre_c2r(XA[r], XB[R0 - 1 - r], false, twp[i1 + r * T0]);
+        Dft<R0, +1>::run(a);
 #pragma unroll
-              for (int r = 0; r < R0; ++r) a[r] = pre_c2r(XB[r], XA[R0 - 1 - r], false, twp[i2 + r * T0]);
-              Dft<R0, +1>::run(a);
+        for (int r = 0; r < R0; ++r) work[padq<G::PADR>(i1 * R0 + r)] = a[r];
 #pragma unroll
-              for (int r = 0; r < R0; ++r) work[l * G::LSR + padq<G::PADR>(i2 * R0 + r)] = a[r];
-            }
-          }
-        }
+        for (int r = 0; r < R0; ++r) a[r] = pre_c2r(XB[r], XA[R0 - 1 - r], false, twp[i2 + r * T0]);
+        Dft<R0, +1>::run(a);
+#pragma unroll
+        for (int r = 0; r < R0; ++r) work[padq<G::PADR>(i2 * R0 + r)] = a[r];
       }
-      __syncthreads();
+      warp_signal(&cR[t], 1ull);  // this row of T[t] has been consumed: the slot may be reused
     }
-    if constexpr (G::PR == 3) smem_pass<h, 1, +1, G::PADR, G::LSR, false, RMAX>(work, nrows, twr);
-    if (m >= 1) {
-      cp_async_wait_all();
-      __syncthreads();
-    }
+    if constexpr (G::PR == 3) warp_pass<h, 1, +1, G::PADR>(work, twr);
+    const double* dv = (m >= 1) ? prm.dev[op] + (size_t)(m - 1) * J0 * J1 + (size_t)row * J1 : nullptr;
 #pragma unroll
-    for (int j = 0; j < G::NBL; ++j) {  // last pass + recombination in registers
-      const int bb = tid + j * NT, l = bb / G::TL, i = bb % G::TL;
-      if (l < nrows) {
-        double2 a[G::RL];
+    for (int j = 0; j < NBL; ++j) {
+      const int i = lane + 32 * j;
+      double2 a[RL];
 #pragma unroll
-        for (int r = 0; r < G::RL; ++r) a[r] = work[l * G::LSR + padq<G::PADR>(i + r * G::TL)];
-        butterfly<h, G::PR - 1, +1>(a, i, twr);
-        const double2* dv2 = reinterpret_cast<const double2*>(devs + l * J1);
+      for (int r = 0; r < RL; ++r) a[r] = work[padq<G::PADR>(i + r * TL)];
+      double2 d[RL];
+      if (dv) {
 #pragma unroll
-        for (int r = 0; r < G::RL; ++r) {
-          const int q = i + r * G::TL;  // x[2q], x[2q+1]
-          double v0 = a[r].x, v1 = a[r].y;
-          if (m >= 1) {
-            const double2 d = dv2[q];
-            v0 = d.x * v0;
-            v1 = d.y * v1;
-          }
-          double p0 = 0.0, p1 = 0.0;
-          p0 += v0;
-          p1 += v1;
-          acc[j][r][0] += p0;
-          acc[j][r][1] += p1;
+        for (int r = 0; r < RL; ++r) d[r] = __ldg(reinterpret_cast<const double2*>(dv) + i + r * TL);
+      }
+      butterfly<h, G::PR - 1, +1>(a, i, twr);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        double v0 = a[r].x, v1 = a[r].y;
+        if (dv) {
+          v0 = d[r].x * v0;
+          v1 = d[r].y * v1;
         }
+        double p0 = 0.0, p1 = 0.0;
+        p0 += v0;
+        p1 += v1;
+        acc[j][r][0] += p0;
+        acc[j][r][1] += p1;
       }
     }
-    signal_counter(&cR[t]);
+    __syncwarp();  // work buffer reads done before the next term's pass 0 writes
     if (m == M && !(prm.seismic && op == prm.nops - 1)) {  // operator complete: hand over
+      double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)row * J1);
 #pragma unroll
-      for (int j = 0; j < G::NBL; ++j) {
-        const int bb = tid + j * NT, l = bb / G::TL, i = bb % G::TL;
-        if (l < nrows) {
-          double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)(r0 + l) * J1);
+      for (int j = 0; j < NBL; ++j)
 #pragma unroll
-          for (int r = 0; r < G::RL; ++r) {
-            o[i + r * G::TL] = make_double2(acc[j][r][0], acc[j][r][1]);
-            acc[j][r][0] = acc[j][r][1] = 0.0;
-          }
+        for (int r = 0; r < RL; ++r) {
+          o[lane + 32 * j + r * TL] = make_double2(acc[j][r][0], acc[j][r][1]);
+          acc[j][r][0] = acc[j][r][1] = 0.0;
         }
-      }
     }
-  };
-
-  // pipeline: C(0..K-2) ; for t: R(t), C(t+K-1)
-  for (int t = 0; t < KRING - 1 && t < ntot; ++t) column_term(t);
-  for (int t = 0; t < ntot; ++t) {
-    row_term(t);
-    if (t + KRING - 1 < ntot) column_term(t + KRING - 1);
   }
   if (prm.residue && rmax > 0.0)
     atomicMax(reinterpret_cast<unsigned long long*>(prm.residue), (unsigned long long)__double_as_longlong(rmax));
 
-  // ------------------------------------------------ seismic update (seismic.cpp:116-129)
+  // ---- seismic update (seismic.cpp:116-129)
   if (prm.seismic) {
     bool bad = false;
     const double tau = prm.tau;
     const double t2 = tau * tau;
+    const size_t rowoff = (size_t)row * J1;
+    const double2* cur = reinterpret_cast<const double2*>(prm.u + rowoff);
+    const double2* prev = reinterpret_cast<const double2*>(prm.prev + rowoff);
+    const double2* ap = reinterpret_cast<const double2*>(prm.ap + rowoff);
+    const double2* l1 = reinterpret_cast<const double2*>(prm.out[0] + rowoff);
+    const double2* c = reinterpret_cast<const double2*>(prm.c + rowoff);
+    const double2* eta = reinterpret_cast<const double2*>(prm.eta + rowoff);
+    const double2* tc = reinterpret_cast<const double2*>(prm.tc + rowoff);
+    double2* nx = reinterpret_cast<double2*>(prm.next + rowoff);
+    double2* l2o = reinterpret_cast<double2*>(prm.out[1] + rowoff);
 #pragma unroll
-    for (int j = 0; j < G::NBL; ++j) {
-      const int bb = tid + j * NT, l = bb / G::TL, i = bb % G::TL;
-      if (l < nrows) {
-        const size_t rowoff = (size_t)(r0 + l) * J1;
-        const double2* cur = reinterpret_cast<const double2*>(prm.u + rowoff);
-        const double2* prev = reinterpret_cast<const double2*>(prm.prev + rowoff);
-        const double2* ap = reinterpret_cast<const double2*>(prm.ap + rowoff);
-        const double2* l1 = reinterpret_cast<const double2*>(prm.out[0] + rowoff);
-        const double2* c = reinterpret_cast<const double2*>(prm.c + rowoff);
-        const double2* eta = reinterpret_cast<const double2*>(prm.eta + rowoff);
-        const double2* tc = reinterpret_cast<const double2*>(prm.tc + rowoff);
-        double2* nx = reinterpret_cast<double2*>(prm.next + rowoff);
-        double2* l2o = reinterpret_cast<double2*>(prm.out[1] + rowoff);
+    for (int j = 0; j < NBL; ++j)
 #pragma unroll
-        for (int r = 0; r < G::RL; ++r) {
-          const int q = i + r * G::TL;
-          const double2 vc = cur[q], vp = prev[q], va = ap[q], v1 = l1[q], cc = c[q], ve = eta[q], vt = tc[q];
-          const double l2x = acc[j][r][0], l2y = acc[j][r][1];
-          const double c2x = cc.x * cc.x, c2y = cc.y * cc.y;
-          const double nx0 = 2.0 * vc.x - vp.x + t2 * c2x * (ve.x * v1.x + vt.x * (l2x - va.x) / tau);
-          const double nx1 = 2.0 * vc.y - vp.y + t2 * c2y * (ve.y * v1.y + vt.y * (l2y - va.y) / tau);
-          nx[q] = make_double2(nx0, nx1);
-          l2o[q] = make_double2(l2x, l2y);
-          bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
-        }
+      for (int r = 0; r < RL; ++r) {
+        const int q = lane + 32 * j + r * TL;
+        const double2 vc = cur[q], vp = prev[q], va = ap[q], v1 = l1[q], cc = c[q], ve = eta[q], vt = tc[q];
+        const double l2x = acc[j][r][0], l2y = acc[j][r][1];
+        const double c2x = cc.x * cc.x, c2y = cc.y * cc.y;
+        const double nx0 = 2.0 * vc.x - vp.x + t2 * c2x * (ve.x * v1.x + vt.x * (l2x - va.x) / tau);
+        const double nx1 = 2.0 * vc.y - vp.y + t2 * c2y * (ve.y * v1.y + vt.y * (l2y - va.y) / tau);
+        nx[q] = make_double2(nx0, nx1);
+        l2o[q] = make_double2(l2x, l2y);
+        bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
       }
-    }
-    if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicMin(prm.flag, prm.step);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(prm.flag, prm.step);
   }
 }
 
-template <int J0, int J1, int CG, int RMAX>
+template <int J0, int J1, int RMAX>
 cudaError_t launch_t(const Step2DParams& p, cudaStream_t st, int nblk) {
-  using G = Geo<J0, J1, CG, RMAX>;
+  using G = Geo<J0, J1, RMAX>;
   if ((J0 + nblk - 1) / nblk > RMAX || G::NG > nblk) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_step2d<J0, J1, CG, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    cudaFuncSetAttribute(k_step2d<J0, J1, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     attr = true;
   }
   void* args[] = {(void*)&p};
-  return cudaLaunchCooperativeKernel((void*)k_step2d<J0, J1, CG, RMAX>, dim3(nblk), dim3(NT), args, G::SMEM, st);
+  return cudaLaunchCooperativeKernel((void*)k_step2d<J0, J1, RMAX>, dim3(nblk), dim3(G::NT), args, G::SMEM, st);
 }
 
 }  // namespace s2d
 
 bool step2d_supported(int J0, int J1, int nsm) {
-  if (!((J0 == 1024 && J1 == 1024) || (J0 == 512 && J1 == 512) || (J0 == 256 && J1 == 256) ||
-        (J0 == 512 && J1 == 1024) || (J0 == 1024 && J1 == 512)))
+  if (!((J0 == 1024 && J1 == 1024) || (J0 == 512 && J1 == 1024)))
     return false;
   const int H = J1 / 2 + 1;
   const int ng = (H + kStep2dCG - 1) / kStep2dCG;
@@ -576,11 +552,8 @@ int step2d_col_groups(int J1) { return (J1 / 2 + 1 + kStep2dCG - 1) / kStep2dCG;
 
 cudaError_t launch_step2d(const Step2DParams& p, cudaStream_t st, int nsm) {
   const int J0 = p.J0, J1 = p.J1;
-  if (J0 == 1024 && J1 == 1024) return s2d::launch_t<1024, 1024, 4, 7>(p, st, nsm);
-  if (J0 == 512 && J1 == 512) return s2d::launch_t<512, 512, 4, 4>(p, st, nsm);
-  if (J0 == 256 && J1 == 256) return s2d::launch_t<256, 256, 4, 2>(p, st, nsm);
-  if (J0 == 512 && J1 == 1024) return s2d::launch_t<512, 1024, 4, 4>(p, st, nsm);
-  if (J0 == 1024 && J1 == 512) return s2d::launch_t<1024, 512, 4, 7>(p, st, nsm);
+  if (J0 == 1024 && J1 == 1024) return s2d::launch_t<1024, 1024, 7>(p, st, nsm);
+  if (J0 == 512 && J1 == 1024) return s2d::launch_t<512, 1024, 4>(p, st, nsm);
   return cudaErrorInvalidValue;
 }
 
@@ -588,18 +561,15 @@ cudaError_t launch_step2d(const Step2DParams& p, cudaStream_t st, int nsm) {
 
 namespace fw {
 namespace {
-// w[m][k0][c] (c < H) -> w2d[m][g][k0][CG] (zero padded past H)
-__global__ void k_w_to_2d(int J0, int H, int NG, int M, const double* __restrict__ w, double* __restrict__ w2d) {
-  const long long total = (long long)(M + 1) * NG * J0 * kStep2dCG;
+// w[m][k0][c] (c < H) -> w2d[m][c][k0] (column-major per term; columns past H zero)
+__global__ void k_w_to_2d(int J0, int H, int NC, int M, const double* __restrict__ w, double* __restrict__ w2d) {
+  const long long total = (long long)(M + 1) * NC * J0;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const int cc = (int)(e % kStep2dCG);
-    long long r = e / kStep2dCG;
-    const int k0 = (int)(r % J0);
-    r /= J0;
-    const int g = (int)(r % NG);
-    const int m = (int)(r / NG);
-    const int c = g * kStep2dCG + cc;
+    const int k0 = (int)(e % J0);
+    const long long r = e / J0;
+    const int c = (int)(r % NC);
+    const int m = (int)(r / NC);
     w2d[e] = c < H ? w[((long long)m * J0 + k0) * H + c] : 0.0;
   }
 }
@@ -618,8 +588,8 @@ __global__ void k_dev_tables(long long N, int M, const double* __restrict__ dev1
 
 void launch_w_to_2d(cudaStream_t st, int J0, int J1, int M, const double* w, double* w2d) {
   const int H = J1 / 2 + 1;
-  const int NG = (H + kStep2dCG - 1) / kStep2dCG;
-  k_w_to_2d<<<148 * 8, 256, 0, st>>>(J0, H, NG, M, w, w2d);
+  const int NC = ((H + kStep2dCG - 1) / kStep2dCG) * kStep2dCG;
+  k_w_to_2d<<<148 * 8, 256, 0, st>>>(J0, H, NC, M, w, w2d);
 }
 
 void launch_dev_tables(cudaStream_t st, size_t N, int M, const double* dev1, double* dev) {
