@@ -67,6 +67,9 @@ int fw_ctx_sync(fw_ctx ctx);
 void* fw_ctx_stream(fw_ctx ctx);
 /* number of kernels this context has launched so far (diagnostics / bench) */
 long long fw_ctx_launches(fw_ctx ctx);
+/* diagnostics: persistent-kernel phase timestamps (needs FW_TRACE=1 at context creation);
+ * out receives 2 x 16 x 136 x 4 unsigned 64-bit globaltimer values */
+int fw_ctx_trace(fw_ctx ctx, unsigned long long* out);
 
 /* ---- operator: ExpansionOperator resident on the device ----
  * grid: dim in {1,2,3}, J[dim] points per axis (even, >= 4; this backend needs

@@ -202,6 +202,7 @@ struct fw_ctx_s {
   int nsm = 148;
   bool force_generic = false;                 // FW_FORCE_GENERIC=1: multi-pass kernels only
   unsigned long long* counters = nullptr;     // persistent-kernel counters (2 sets)
+  unsigned long long* trace = nullptr;        // FW_TRACE=1: persistent-kernel phase timestamps
   int cset = 0;
   fw::LaunchCtx L() { return fw::LaunchCtx{stream, master, &launches}; }
   int get_scratch(int slot, size_t bytes, void** out) {
@@ -274,6 +275,11 @@ int fw_ctx_create(int device, fw_ctx* out) {
     return FW_E_OOM;
   }
   FW_CUDA(cudaMemset(c->counters, 0, 2 * (size_t)fw::kStep2dCStride * sizeof(unsigned long long)));
+  const char* tr = getenv("FW_TRACE");
+  if (tr && tr[0] == '1') {
+    const size_t n = 2 * 16 * 136 * 4;
+    if (dalloc(&c->trace, n) == FW_OK) cudaMemset(c->trace, 0, n * sizeof(unsigned long long));
+  }
   fw::init_kernels();
   *out = c;
   return FW_OK;
@@ -288,6 +294,7 @@ void fw_ctx_destroy(fw_ctx c) {
   if (c->master) cudaFree(c->master);
   if (c->residue) cudaFree(c->residue);
   if (c->counters) cudaFree(c->counters);
+  if (c->trace) cudaFree(c->trace);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -300,6 +307,14 @@ int fw_ctx_sync(fw_ctx c) {
 }
 
 void* fw_ctx_stream(fw_ctx c) { return c ? (void*)c->stream : nullptr; }
+
+/* diagnostics: copy the persistent-kernel trace (2 x 16 x 136 x 4 u64) to host; FW_E_ARG if tracing is off */
+int fw_ctx_trace(fw_ctx c, unsigned long long* out) {
+  if (!c || !c->trace || !out) return set_err(FW_E_ARG, "tracing disabled (set FW_TRACE=1 before fw_ctx_create)");
+  FW_CUDA(cudaStreamSynchronize(c->stream));
+  FW_CUDA(cudaMemcpy(out, c->trace, 2 * 16 * 136 * 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return FW_OK;
+}
 long long fw_ctx_launches(fw_ctx c) { return c ? c->launches : 0; }
 
 }  // extern "C"
@@ -410,6 +425,7 @@ int launch_persistent(fw_ctx ctx, fw_op const* ops, int nops, int m_first, const
   p.residue = residue;
   p.master = ctx->master;
   p.counters = ctx->counters;
+  p.trace = ctx->trace;
   p.cset = ctx->cset;
   p.cstride = fw::kStep2dCStride;
   ctx->cset ^= 1;

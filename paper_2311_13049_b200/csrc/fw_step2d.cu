@@ -71,7 +71,30 @@ __device__ __forceinline__ void warp_signal(unsigned long long* cnt, unsigned lo
     red_release_add(cnt, v);
   }
 }
-__device__ __forceinline__ void colbar() { asm volatile("bar.sync 1, %0;" ::"n"(NWC * 32) : "memory"); }
+// named barriers: 1..4 = the warp pair of column p, 5 = all 8 column warps
+__device__ __forceinline__ void colbar() { asm volatile("bar.sync 5, 256;" ::: "memory"); }
+__device__ __forceinline__ void pairbar(int p) { asm volatile("bar.sync %0, 64;" ::"r"(1 + p) : "memory"); }
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// optional instrumentation: trace[(sel*16 + warp)*136 + t][4] = globaltimer at phase marks
+#define FW_TRACE(t, slot)                                                                              \
+  do {                                                                                                 \
+    if (prm.trace && (threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 100))               \
+      prm.trace[(((size_t)(blockIdx.x == 0 ? 0 : 1) * 16 + (threadIdx.x >> 5)) * 136 + (t)) * 4 + (slot)] = \
+          gtimer();                                                                                    \
+  } while (0)
 
 template <int DIR>
 __device__ __forceinline__ double2 dirw(double2 w) {
@@ -164,9 +187,9 @@ struct Geo {
   static constexpr int H = J1 / 2 + 1;
   static constexpr int h = J1 / 2;
   static constexpr int NG = (H + NWC - 1) / NWC;
-  static constexpr int NT = 32 * (NWC + RMAX);
+  static constexpr int NT = 512;  // 8 column warps (2 per column) + 8 row warps
   static constexpr int PADC = ilog2c(radix(J0, 0));
-  static constexpr int PADR = ilog2c(radix(h, 0));
+  static constexpr int PADR = 4;
   static constexpr int LCOL = J0 + (J0 >> PADC) + 2;  // per column-warp work buffer
   static constexpr int LROW = h + (h >> PADR) + 2;    // per row-warp work buffer
   static constexpr int PC = npass(J0);
@@ -184,42 +207,60 @@ struct Geo {
   static_assert(PC >= 2 && PC <= 3 && PR >= 2 && PR <= 3, "2 or 3 passes per FFT");
   static_assert(NWC * LCOL >= 4 * J0 && NWC * J0 >= 4 * J0, "joint transpose area");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
-  static_assert(h / radix(h, 0) == 64 || h / radix(h, 0) == 32, "row pass-0 lane mapping");
+  static_assert(RMAX <= 8, "at most 8 row warps");
 };
 
-// ---------------------------------------------------------------- column warp: J0-point C2C
-// pass 0 from src(q) (q = i + r*T0); the last pass writes each butterfly's outputs
-// back to the slots it read, so `work` ends holding the column in natural order
-// (padded).  The caller passes `sync0` to separate pass 0 from the rest when the
-// source is shared with other warps.
-template <int J0, int DIR, int PADSH, class Src, class Sync0>
-__device__ __forceinline__ void column_c2c(double2* work, const double2* tw, Src src, Sync0 sync0) {
+// ---------------------------------------------------------------- column pair: J0-point C2C
+// Two warps (64 threads, ct2 = 0..63, pair barrier `pbar`) transform one column.
+// Pass 0 reads src(q) (q = i + r*T0); the last pass writes each butterfly's
+// outputs back to the slots it read, so `work` ends holding the column in
+// natural order (padded).  `sync0` separates pass 0 from the rest (the caller's
+// barrier when the pass-0 source is shared with other warps).
+template <int J0, int DIR, int PADSH, class Src, class Sync0, class PBar>
+__device__ __forceinline__ void column_c2c(double2* work, const double2* tw, int ct2, Src src, Sync0 sync0,
+                                           PBar pbar) {
   constexpr int P = npass(J0);
-  const int lane = threadIdx.x & 31;
   {
     constexpr int R = radix(J0, 0);
     constexpr int T = J0 / R;
+    static_assert(T == 64, "column pass 0: one butterfly per pair thread");
+    const int i = ct2;
+    double2 a[R];
 #pragma unroll
-    for (int j = 0; j < T / 32; ++j) {
-      const int i = lane + 32 * j;
-      double2 a[R];
+    for (int r = 0; r < R; ++r) a[r] = src(i + r * T);
+    Dft<R, DIR>::run(a);
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[r] = src(i + r * T);
-      Dft<R, DIR>::run(a);
-#pragma unroll
-      for (int r = 0; r < R; ++r) work[padq<PADSH>(i * R + r)] = a[r];
-    }
+    for (int r = 0; r < R; ++r) work[padq<PADSH>(i * R + r)] = a[r];
     sync0();
-    __syncwarp();
   }
-  if constexpr (P == 3) warp_pass<J0, 1, DIR, PADSH>(work, tw);
+  if constexpr (P == 3) {  // middle pass, in place across the pair
+    constexpr int R = radix(J0, 1);
+    constexpr int T = J0 / R;
+    constexpr int NB = T / 64;
+    static_assert(T % 64 == 0, "column middle pass");
+    double2 a[NB][R];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[j][r] = work[padq<PADSH>(ct2 + 64 * j + r * T)];
+    pbar();
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int i = ct2 + 64 * j;
+      butterfly<J0, 1, DIR>(a[j], i, tw);
+#pragma unroll
+      for (int r = 0; r < R; ++r) work[padq<PADSH>(out_index<J0, 1>(i, r))] = a[j][r];
+    }
+    pbar();
+  }
   {
     constexpr int PL = P - 1;
     constexpr int R = radix(J0, PL);
     constexpr int T = J0 / R;
+    static_assert(T % 64 == 0, "column last pass");
 #pragma unroll
-    for (int j = 0; j < T / 32; ++j) {
-      const int i = lane + 32 * j;
+    for (int j = 0; j < T / 64; ++j) {
+      const int i = ct2 + 64 * j;
       double2 a[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) a[r] = work[padq<PADSH>(i + r * T)];
@@ -227,7 +268,6 @@ __device__ __forceinline__ void column_c2c(double2* work, const double2* tw, Src
 #pragma unroll
       for (int r = 0; r < R; ++r) work[padq<PADSH>(i + r * T)] = a[r];
     }
-    __syncwarp();
   }
 }
 
@@ -275,70 +315,79 @@ __global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2
   const int nterms = M + 1 - prm.m_first;
   const int ntot = prm.nops * nterms;
 
-  if (warp < NWC) {
-    // ============================================ column warps
+  if (warp < 2 * NWC) {
+    // ============================================ column warps (pairs)
+    setmaxnreg_dec<96>();
     if (b >= G::NG) return;
-    const int cw = warp;
+    const int cw = warp >> 1;              // column of the pair
+    const int ct2 = ((warp & 1) << 5) | lane;  // 0..63 within the pair
     const int c0 = b * NWC;
     const int c = c0 + cw;
     const int ncols = min(NWC, H - c0);
     const bool valid = c < H;
     double2* uhat = sm + G::OFF_U + (size_t)cw * J0;
     double2* work = sm + G::OFF_CW + (size_t)cw * G::LCOL;
-    double2* works = sm + G::OFF_CW;  // the 4 column work buffers (line stride LCOL)
+    double2* works = sm + G::OFF_CW;   // the 4 column work buffers (line stride LCOL)
     double2* joint_u = sm + G::OFF_U;  // F2 staging (uhat not yet valid)
-    const int ct = tid;                // 0..127 within the column warps
+    const int ct = tid;                // 0..255 within the column warps
+    auto pb = [cw] { pairbar(cw); };
 
     // ---- F2: forward columns -> uhat
     warp_wait(cY, (unsigned long long)J0);
-    colbar();  // all 4 column warps have seen every row
-    for (int e = ct; e < J0 * 4; e += NWC * 32) {
+    colbar();  // all column warps have seen every row
+    for (int e = ct; e < J0 * 4; e += 2 * NWC * 32) {
       const int k0 = e >> 2, cc = e & 3;
       joint_u[jidx(k0, cc)] = (c0 + cc < H) ? __ldcg(&prm.Y[(size_t)k0 * H + c0 + cc]) : make_double2(0.0, 0.0);
     }
     colbar();
-    // pass 0 reads joint_u (shared by the 4 warps): barrier before uhat is overwritten
-    column_c2c<J0, -1, G::PADC>(work, twc, [&](int q) { return joint_u[jidx(q, cw)]; }, [] { colbar(); });
+    // pass 0 reads joint_u (shared by all column warps): barrier before uhat is overwritten
+    column_c2c<J0, -1, G::PADC>(work, twc, ct2, [&](int q) { return joint_u[jidx(q, cw)]; }, [] { colbar(); }, pb);
+    pb();
     {
       const double inv = 1.0 / ((double)J0 * (double)J1);
-      for (int q = lane; q < J0; q += 32) {
+      for (int q = ct2; q < J0; q += 64) {
         const double2 v = work[padq<G::PADC>(q)];
         uhat[q] = make_double2(v.x * inv, v.y * inv);
       }
-      __syncwarp();
+      pb();
     }
 
     // ---- C(t): inverse columns -> T[t % KRING]
     for (int t = 0; t < ntot; ++t) {
       const int op = t / nterms;
       const int m = prm.m_first + t % nterms;
+      FW_TRACE(t, 0);
       if (t >= KRING) warp_wait(&cR[t - KRING], (unsigned long long)J0);
+      FW_TRACE(t, 1);
       const double* w = prm.w[op] + ((size_t)m * (G::NG * NWC) + c) * J0;  // [m][c][k0]
       column_c2c<J0, +1, G::PADC>(
-          work, twc,
+          work, twc, ct2,
           [&](int q) {
             const double2 v = uhat[q];
             const double wk = valid ? __ldg(&w[q]) : 0.0;
             return make_double2(wk * v.x, wk * v.y);
           },
-          [] {});
+          pb, pb);
       colbar();  // the 4 columns are complete in the 4 work buffers
+      FW_TRACE(t, 2);
       double2* T = prm.T + (size_t)(t % KRING) * J0 * H;
-      for (int e = ct; e < J0 * 4; e += NWC * 32) {  // 64-byte row chunks of the 4 columns
+      for (int e = ct; e < J0 * 4; e += 2 * NWC * 32) {  // 64-byte row chunks of the 4 columns
         const int k0 = e >> 2, cc = e & 3;
         if (cc < ncols) __stcg(&T[(size_t)k0 * H + c0 + cc], works[cc * G::LCOL + padq<G::PADC>(k0)]);
       }
-      colbar();  // stores issued by all 128 threads; work buffers free again
+      colbar();  // stores issued by all column threads; work buffers free again
       if (ct == 0) {
         __threadfence();
         red_release_add(&cC[t], (unsigned long long)ncols);
       }
+      FW_TRACE(t, 3);
     }
     return;
   }
 
   // ============================================ row warps
-  const int rw = warp - NWC;
+  setmaxnreg_inc<160>();
+  const int rw = warp - 2 * NWC;
   const int r0 = (int)(((long long)b * J0) / nblk);
   const int r1 = (int)(((long long)(b + 1) * J0) / nblk);
   if (rw >= r1 - r0) return;
@@ -404,7 +453,9 @@ __global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2
   for (int t = 0; t < ntot; ++t) {
     const int op = t / nterms;
     const int m = prm.m_first + t % nterms;
+    FW_TRACE(t, 0);
     warp_wait(&cC[t], (unsigned long long)H);
+    FW_TRACE(t, 1);
     const double2* X = prm.T + (size_t)(t % KRING) * J0 * H + (size_t)row * H;
     // pass 0 with the pre-processing fused.  Butterfly i needs X[i + r T0] and
     // X[h - i - r T0] = X[(T0 - i) + (R0-1-r) T0]: lane L takes butterflies L and
@@ -448,6 +499,7 @@ __global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2
         for (int r = 0; r < R0; ++r) work[padq<G::PADR>(i2 * R0 + r)] = a[r];
       }
       warp_signal(&cR[t], 1ull);  // this row of T[t] has been consumed: the slot may be reused
+      FW_TRACE(t, 2);
     }
     if constexpr (G::PR == 3) warp_pass<h, 1, +1, G::PADR>(work, twr);
     const double* dv = (m >= 1) ? prm.dev[op] + (size_t)(m - 1) * J0 * J1 + (size_t)row * J1 : nullptr;
@@ -478,6 +530,7 @@ __global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2
       }
     }
     __syncwarp();  // work buffer reads done before the next term's pass 0 writes
+    FW_TRACE(t, 3);
     if (m == M && !(prm.seismic && op == prm.nops - 1)) {  // operator complete: hand over
       double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)row * J1);
 #pragma unroll

@@ -21,6 +21,7 @@ struct Step2DParams {
   double* residue;          // nullable, max-accumulated
   const double2* master;    // twiddle master table
   unsigned long long* counters;  // 2 sets x kStep2dCStride, zero-initialised
+  unsigned long long* trace;     // optional phase timestamps (CTAs 0 and 100), see fw_step2d.cu
   int cset, cstride;
   // seismic update
   int seismic;
