@@ -406,7 +406,7 @@ int launch_persistent(fw_ctx ctx, fw_op const* ops, int nops, int m_first, const
   const int m_last = ops[0]->constant_order ? 0 : ops[0]->M;
   void *Y = nullptr, *T = nullptr;
   FW_TRY(ctx->get_scratch(SLOT_Y2D, g.Nh * sizeof(double2), &Y));
-  FW_TRY(ctx->get_scratch(SLOT_T2D, 3 * g.Nh * sizeof(double2), &T));
+  FW_TRY(ctx->get_scratch(SLOT_T2D, (size_t)fw::kStep2dRing * g.Nh * sizeof(double2), &T));
   fw::Step2DParams p = extra ? *extra : fw::Step2DParams{};
   p.J0 = g.J[0];
   p.J1 = g.J[1];
@@ -424,6 +424,7 @@ int launch_persistent(fw_ctx ctx, fw_op const* ops, int nops, int m_first, const
   }
   p.residue = residue;
   p.master = ctx->master;
+  p.wcols = fw::step2d_wcols(g.J[1]);
   p.counters = ctx->counters;
   p.trace = ctx->trace;
   p.cset = ctx->cset;

@@ -15,7 +15,8 @@ struct Step2DParams {
   const double* u;          // input field (cur)
   double2* Y;               // J0 x (J1/2+1) forward scratch
   double2* T;               // KRING x J0 x (J1/2+1) term ring
-  const double* w[2];       // per op: [M+1][ngroups][J0][CG] weights
+  const double* w[2];       // per op: [M+1][wcols][J0] weights (column-major per term)
+  int wcols;                // columns per term in w (>= J1/2+1)
   const double* dev[2];     // per op: [M][J0][J1] deviation powers m = 1..M
   double* out[2];           // per op result (seismic: out[0] = L1, out[1] = new L2prev)
   double* residue;          // nullable, max-accumulated
@@ -34,7 +35,9 @@ struct Step2DParams {
 
 bool step2d_supported(int J0, int J1, int nsm);
 int step2d_col_groups(int J1);
+int step2d_wcols(int J1);
 constexpr int kStep2dCG = 4;
+constexpr int kStep2dRing = 6;  // term slots of the global ring
 cudaError_t launch_step2d(const Step2DParams& p, cudaStream_t st, int nsm);
 
 // table relayouts for the persistent kernel
