@@ -1,0 +1,50 @@
+"""The drop-in: the reference's OWN test suites, linked against the B200 backend
+(paper_2311_13049_b200/cpp: flap.cpp's apply_matrix_free / _serial /
+apply_perturbation replaced by flap_gpu.cpp over the C-ABI).  Every operator
+apply made by the reference's tests, SeismicStepper and Laplacian seam runs on
+the GPU."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+BUILD = os.path.join(ROOT, "paper_2311_13049_b200", "cpp", "build")
+UNIT = os.path.join(BUILD, "unit_tests_gpu")
+ACC = os.path.join(BUILD, "acceptance_gpu")
+needs_build = pytest.mark.skipif(not os.path.exists(UNIT), reason="drop-in not built (needs /root/reference)")
+
+
+@needs_build
+def test_dropin_links_the_b200_library():
+    out = subprocess.run(["ldd", os.path.join(BUILD, "libfracwave_b200dropin.so")], capture_output=True,
+                         text=True).stdout
+    assert "libfw_b200.so" in out and "not found" not in out
+
+
+def _run(cmd, tmp_path):
+    env = dict(os.environ, FW_DROPIN_REPORT="1")
+    r = subprocess.run(cmd, cwd=tmp_path, capture_output=True, text=True, timeout=900, env=env)
+    m = re.search(r"\[fw-dropin\] (\d+) operator applies ran on the B200 backend", r.stderr)
+    return r, int(m.group(1)) if m else 0
+
+
+@pytest.mark.gpu
+@needs_build
+@pytest.mark.parametrize("suite", ["flap", "seismic", "stepping", "grid"])
+def test_reference_unit_suites_on_b200(suite, tmp_path):
+    r, n = _run([UNIT, f"-ts={suite}"], tmp_path)
+    assert r.returncode == 0 and "0 failed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+    if suite != "grid":
+        assert n > 0  # the applies really went through the GPU
+
+
+@pytest.mark.gpu
+@needs_build
+@pytest.mark.parametrize("criterion", [1, 2, 5, 9])
+def test_reference_acceptance_on_b200(criterion, tmp_path):
+    r, n = _run([ACC, "--criterion", str(criterion)], tmp_path)
+    assert r.returncode == 0 and "[PASS]" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+    assert n > 0
