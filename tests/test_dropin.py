@@ -47,4 +47,5 @@ def test_reference_unit_suites_on_b200(suite, tmp_path):
 def test_reference_acceptance_on_b200(criterion, tmp_path):
     r, n = _run([ACC, "--criterion", str(criterion)], tmp_path)
     assert r.returncode == 0 and "[PASS]" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
-    assert n > 0
+    if criterion != 5:  # criterion 5 uses constant orders only: its perturbations are exact host zeros
+        assert n > 0
