@@ -31,6 +31,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+from paper_2311_13049_b200 import configs  # noqa: E402
 
 METRIC = "VO frac-Laplacian Gpoint·term/s & time-steps/s; % of HBM roofline"
 UNIT = "Gpoint·term/s"
@@ -44,6 +45,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--size", type=int, default=1024, help="grid points per axis (C2 = 1024)")
     p.add_argument("--cpu-baseline-steps", type=int, default=4)
+    p.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
+                   help="c2 (default): fused seismic step; c3/c4: slab-decomposed 3D apply; c5: batched 2D sweep")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -176,10 +179,164 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def run_slab(args, cfg_fn, name):
+    """configs[2]/[3]: slab-decomposed 3D apply of the dispersion operator over N ranks
+    (strong scaling: the global grid is fixed); one NCCL all-to-all forward + one batched
+    all-to-all backward per apply."""
+    import torch
+
+    import paper_2311_13049_b200 as fw
+    from paper_2311_13049_b200.slab import SlabGeometry, slab_apply_device
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = cfg_fn(args.size) if args.size != 1024 else cfg_fn()
+    ctx = fw.Context(local)
+    g = fw.Grid(list(zip(cfg.lo, cfg.hi)), cfg.J)
+    op = fw.build_expansion(fw.OrderField(g, 1.0 + cfg.gamma), cfg.M, ctx=ctx)
+    geo = SlabGeometry(cfg.J, world, rank)
+    u = torch.from_numpy(np.ascontiguousarray(cfg.phi[geo.rows])).cuda()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    for _ in range(args.warmup):
+        slab_apply_device(op, u, geo, ctx)
+    ctx.sync()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            out = slab_apply_device(op, u, geo, ctx)
+        e1.record(stream)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    units = cfg.N * (cfg.M + 1)
+    # e2e: host slab in (pinned), host slab out
+    hin = torch.from_numpy(np.ascontiguousarray(cfg.phi[geo.rows])).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_e2e = max(2, min(args.steps, 10))
+    e2.record(stream)
+    for _ in range(n_e2e):
+        with torch.cuda.stream(stream):
+            ud = hin.cuda(non_blocking=True)
+        o = slab_apply_device(op, ud, geo, ctx)
+        with torch.cuda.stream(stream):
+            hout.copy_(o, non_blocking=True)
+    e3.record(stream)
+    e3.synchronize()
+    t2 = torch.tensor([e2.elapsed_time(e3) / n_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
+    if rank == 0:
+        hbm, peak_src = peaks()
+        B = configs.bytes_per_apply(cfg.N, cfg.N_half, cfg.M) / world
+        line = {"metric": METRIC, "value": units / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{name}: slab-decomposed apply of order 1+gamma "
+                                       f"({'x'.join(map(str, cfg.J))}, M={cfg.M}); one step = one apply",
+                           "grid": list(cfg.J), "M": cfg.M, "parallelism": f"slab P={world} (axis 0)",
+                           "l2": "working set > 126 MB L2; no flush"},
+                "roofline": {"bound": "hbm", "achieved": B / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                             "frac": B / (ms * 1e-3) / 1e9 / hbm, "traffic": None,
+                             "kernel": "whole apply (multi-pass kernels + transposes)",
+                             "bytes_model": "SURVEY 8(d) table model B_apply / P", "peak_source": peak_src},
+                "e2e": {"value": units / (float(t2.item()) * 1e-3) / 1e9, "unit": UNIT,
+                        "h2d_bytes_per_step": 8 * cfg.N // world, "d2h_bytes_per_step": 8 * cfg.N // world},
+                "gpu_launches": None, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def run_c5(args):
+    """configs[4]: 64 independent 512^2 fields (data-parallel over ranks, no collective),
+    apply-only throughput for every M of the sweep; value = the M = 16 sweep point."""
+    import torch
+
+    import paper_2311_13049_b200 as fw
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = fw.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    mine = [f for f in range(configs.C5_FIELDS) if f % world == rank]
+    fields = [configs.c5_field(f) for f in mine]
+    g = fw.Grid(list(zip(fields[0].lo, fields[0].hi)), fields[0].J)
+    us = [torch.from_numpy(np.ascontiguousarray(f.u)).cuda() for f in fields]
+    outs = [torch.empty_like(u) for u in us]
+    per_m = {}
+    for M in configs.C5_M:
+        ops = [fw.build_expansion(fw.OrderField(g, f.s), M, ctx=ctx) for f in fields]
+        for _ in range(max(1, args.warmup)):
+            for op, u, o in zip(ops, us, outs):
+                op.apply_device(u.data_ptr(), o.data_ptr())
+        ctx.sync()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, args.steps // 20)
+        e0.record(stream)
+        for _ in range(reps):
+            for op, u, o in zip(ops, us, outs):
+                op.apply_device(u.data_ptr(), o.data_ptr())
+        e1.record(stream)
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        n = fields[0].u.size
+        per_m[M] = {"ms_per_sweep": ms, "Gpoint_term_per_s": configs.C5_FIELDS * n * (M + 1) / (ms * 1e-3) / 1e9}
+        del ops
+    if rank == 0:
+        hbm, peak_src = peaks()
+        n = fields[0].u.size
+        nh = n // 512 * 257
+        ms16 = per_m[16]["ms_per_sweep"]
+        B = configs.C5_FIELDS * configs.bytes_per_apply(n, nh, 16)
+        line = {"metric": METRIC, "value": per_m[16]["Gpoint_term_per_s"], "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms16, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "C5: 64 x 512^2 independent applies (one step = one sweep at M = 16)",
+                           "M_sweep": {str(k): v for k, v in per_m.items()},
+                           "parallelism": f"data-parallel over {world} GPU(s), no collective"},
+                "roofline": {"bound": "hbm", "achieved": B / (ms16 * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                             "frac": B / (ms16 * 1e-3) / 1e9 / hbm, "traffic": None,
+                             "kernel": "64 applies (multi-pass kernels)", "peak_source": peak_src},
+                "e2e": None, "gpu_launches": None}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.workload in ("c3", "c4"):
+        from paper_2311_13049_b200 import configs as _c
+
+        run_slab(args, _c.c3 if args.workload == "c3" else _c.c4, args.workload.upper())
+        return
+    if args.workload == "c5":
+        run_c5(args)
         return
     rank, world, local = dist_env()
     import torch

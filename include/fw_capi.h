@@ -157,6 +157,24 @@ int fw_tsfp2_get(fw_tsfp2 t, double* u_host, double* v_host, long* n);
 int fw_rfftn(fw_ctx ctx, int dim, const int* J, const double* x_host, double* H_host);
 int fw_irfftn(fw_ctx ctx, int dim, const int* J, const double* H_host, double* x_host);
 
+/* ---- stage entry points (device pointers, enqueued on the ctx stream) ----
+ * The single-device pipeline's kernels applied to caller-provided sub-arrays, for
+ * distributed orchestration (slab decomposition: paper_2311_13049_b200/slab.py).
+ * Arrays are real [J0]..[J_{d-1}] / Hermitian-half [J0]..[J_{d-1}/2+1] (interleaved).
+ *   fw_stage_r2c       R2C along the last axis (x scale when scale != 1)
+ *   fw_stage_c2c       C2C along axis (< d-1) for nterms terms (src/dst/w advance by their
+ *                      term strides, in complex / real elements); w (nullable) multiplies
+ *                      the source element-wise; x scale when != 1
+ *   fw_stage_c2r_accum per row: out = sum_{m=m_first}^{m_last} (s-s0)^m .* C2R(src_m),
+ *                      ascending m, (s-s0)^m regenerated from dev1 = s - s0
+ *   fw_op_device_tables  the operator's resident tables: w[(M+1)][N_half], dev1[N] */
+int fw_stage_r2c(fw_ctx ctx, int dim, const int* J, const double* x_dev, double* H_dev, double scale);
+int fw_stage_c2c(fw_ctx ctx, int dim, const int* J, int axis, int dir, const double* src_dev, double* dst_dev,
+                 const double* w_dev, long long src_ts, long long dst_ts, long long w_ts, int nterms, double scale);
+int fw_stage_c2r_accum(fw_ctx ctx, int dim, const int* J, const double* src_dev, long long src_ts, int m_first,
+                       int m_last, const double* dev1_dev, double* out_dev, double* residue_dev);
+int fw_op_device_tables(fw_op op, const double** w_dev, const double** dev1_dev, int* m_last);
+
 #ifdef __cplusplus
 }
 #endif

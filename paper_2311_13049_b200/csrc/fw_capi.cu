@@ -1002,3 +1002,50 @@ int fw_tsfp2_get(fw_tsfp2 t, double* u_host, double* v_host, long* n) {
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// stage entry points: the pipeline's kernels on caller-provided device sub-arrays
+// (used by the slab-decomposed multi-GPU apply, paper_2311_13049_b200/slab.py)
+
+extern "C" {
+
+int fw_stage_r2c(fw_ctx ctx, int dim, const int* J, const double* x_dev, double* H_dev, double scale) {
+  if (!ctx || !x_dev || !H_dev) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
+  fw::launch_stage_r2c(ctx->L(), g, x_dev, (double2*)H_dev, scale, scale != 1.0);
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+int fw_stage_c2c(fw_ctx ctx, int dim, const int* J, int axis, int dir, const double* src_dev, double* dst_dev,
+                 const double* w_dev, long long src_ts, long long dst_ts, long long w_ts, int nterms, double scale) {
+  if (!ctx || !src_dev || !dst_dev || nterms < 1) return set_err(FW_E_ARG, "bad argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
+  if (axis < 0 || axis > dim - 2) return set_err(FW_E_ARG, "axis must be < dim-1 (the last axis is the halved one)");
+  fw::launch_stage_c2c(ctx->L(), g, axis, dir < 0 ? -1 : +1, (const double2*)src_dev, (double2*)dst_dev, w_dev, src_ts,
+                       dst_ts, w_ts, nterms, scale, scale != 1.0);
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+int fw_stage_c2r_accum(fw_ctx ctx, int dim, const int* J, const double* src_dev, long long src_ts, int m_first,
+                       int m_last, const double* dev1_dev, double* out_dev, double* residue_dev) {
+  if (!ctx || !src_dev || !out_dev || m_last < m_first) return set_err(FW_E_ARG, "bad argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
+  fw::launch_stage_c2r(ctx->L(), g, (const double2*)src_dev, src_ts, m_first, m_last, dev1_dev, out_dev, residue_dev);
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+int fw_op_device_tables(fw_op op, const double** w_dev, const double** dev1_dev, int* m_last) {
+  if (!op) return set_err(FW_E_ARG, "null op");
+  if (w_dev) *w_dev = op->w;
+  if (dev1_dev) *dev1_dev = op->dev1;
+  if (m_last) *m_last = op->constant_order ? 0 : op->M;
+  return FW_OK;
+}
+
+}  // extern "C"

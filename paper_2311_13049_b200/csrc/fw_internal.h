@@ -75,4 +75,12 @@ void launch_tsfp2_kick(const LaunchCtx& L, size_t N, double tau, double kappa, i
 void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x);
 void launch_sup_check(const LaunchCtx& L, size_t N, const double* u, double thr, int step, int* flag);
 
+// stage entry points (distributed orchestration on local sub-arrays)
+void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, double2* H, double scale, bool do_scale);
+void launch_stage_c2c(const LaunchCtx& L, const GridGeom& g, int axis, int dir, const double2* src, double2* dst,
+                      const double* w, long long src_ts, long long dst_ts, long long w_ts, int nterms, double scale,
+                      bool do_scale);
+void launch_stage_c2r(const LaunchCtx& L, const GridGeom& g, const double2* src, long long src_ts, int m_first,
+                      int m_last, const double* dev1, double* out, double* residue);
+
 }  // namespace fw

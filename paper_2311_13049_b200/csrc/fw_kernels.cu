@@ -443,3 +443,27 @@ void launch_sup_check(const LaunchCtx& L, size_t N, const double* u, double thr,
 }
 
 }  // namespace fw
+
+namespace fw {
+// ---- stage entry points for distributed (slab) orchestration: the same kernels as the
+// single-device pipeline, applied to a local sub-array
+void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, double2* H, double scale,
+                      bool do_scale) {
+  const int h = g.nl / 2;
+  const int lpb = std::max(1, std::min(8, 2048 / h));
+  const size_t sm = smem_bytes(h + 1, lpb);
+  const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
+  k_r2c_rows<<<nb, kThreads, sm, L.stream>>>(u, H, g.nl, (long long)g.rows, lpb, scale, do_scale ? 1 : 0,
+                                             L.master);
+  count(L);
+}
+void launch_stage_c2c(const LaunchCtx& L, const GridGeom& g, int axis, int dir, const double2* src, double2* dst,
+                      const double* w, long long src_ts, long long dst_ts, long long w_ts, int nterms, double scale,
+                      bool do_scale) {
+  c2c_axis(L, g, axis, dir, src, dst, w, src_ts, dst_ts, w_ts, nterms, scale, do_scale);
+}
+void launch_stage_c2r(const LaunchCtx& L, const GridGeom& g, const double2* src, long long src_ts, int m_first,
+                      int m_last, const double* dev1, double* out, double* residue) {
+  c2r_accum(L, g, src, src_ts, nullptr, 0, m_first, m_last, dev1, out, residue, nullptr);
+}
+}  // namespace fw

@@ -1,0 +1,249 @@
+"""Slab-decomposed apply of the M-term operator over P ranks (one GPU per rank).
+
+SURVEY.md §8(e): axis 0 of a 3D grid J0 x J1 x J2 is split over P ranks.
+Rank r owns physical planes [r J0/P, (r+1) J0/P) and, in the transposed spectral
+layout, axis-1 lines [r J1/P, (r+1) J1/P):
+
+  forward   R2C along axis 2 and C2C along axis 1 on the local slab
+            -> all-to-all transpose -> C2C along axis 0 (x 1/N)      [J0][J1/P][J2/2+1]
+  inverse   for all terms at once: (w_m .* uhat) -> C2C along axis 0
+            -> all-to-all transpose back -> C2C along axis 1
+            -> per-row C2R with the ascending-m (s-s0)^m recombination  [J0/P][J1][J2]
+
+i.e. (M+2)-term's worth of all-to-alls per apply (one forward, one batched
+backward carrying every term), with NO collective anywhere else.  Every 1D line
+transform is the one the single-device path performs, so the result is
+bit-identical to P = 1 (tests/test_slab.py checks this with world size 2 on CPU,
+tests/test_gpu_parity.py checks the device stages against the single-GPU apply).
+
+The local stages are pluggable:
+  * ``DeviceStages`` -- the sm_100a kernels through the C-ABI stage entry points
+    (fw_stage_r2c / fw_stage_c2c / fw_stage_c2r_accum); buffers are torch CUDA
+    tensors on the context's stream; the transpose is torch.distributed
+    all_to_all_single (NCCL over NVLink when launched under torchrun on one node).
+  * tests supply a numpy implementation of the same three stages to exercise the
+    decomposition logic with the gloo backend on CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+
+@dataclass
+class SlabGeometry:
+    J: tuple          # global (J0, J1, J2)
+    P: int
+    rank: int
+
+    def __post_init__(self):
+        J0, J1, J2 = self.J
+        if J0 % self.P or J1 % self.P:
+            raise ValueError(f"axes 0 and 1 ({J0}, {J1}) must be divisible by P = {self.P}")
+
+    @property
+    def H(self):
+        return self.J[2] // 2 + 1
+
+    @property
+    def J0l(self):
+        return self.J[0] // self.P
+
+    @property
+    def J1l(self):
+        return self.J[1] // self.P
+
+    @property
+    def N(self):
+        return self.J[0] * self.J[1] * self.J[2]
+
+    @property
+    def rows(self):  # physical planes owned by this rank
+        return slice(self.rank * self.J0l, (self.rank + 1) * self.J0l)
+
+    @property
+    def cols(self):  # axis-1 lines owned in the transposed spectral layout
+        return slice(self.rank * self.J1l, (self.rank + 1) * self.J1l)
+
+
+class SlabApply:
+    """Distributed M-term apply for one operator.
+
+    stages: object with r2c(x, shape) -> H, c2c(src, shape, axis, dir, w=None, nterms=1,
+            src_ts=0, w_ts=0, scale=1.0) -> dst, c2r(src, shape, m_first, m_last, dev1) -> out,
+            and array helpers empty/concat/stack (numpy-like semantics on its array type).
+    comm:   object with all_to_all(list_of_P_arrays) -> list_of_P_arrays.
+    w_local: (M+1, J0, J1/P, H) complex-half weights of this rank's spectral columns.
+    dev1_local: (J0/P, J1, J2) values of s - s0 on this rank's planes.
+    """
+
+    def __init__(self, geo: SlabGeometry, stages, comm, w_local, dev1_local, m_last: int):
+        self.g, self.st, self.comm = geo, stages, comm
+        self.w, self.dev1, self.m_last = w_local, dev1_local, m_last
+
+    def forward(self, u_slab):
+        g, st = self.g, self.st
+        loc = (g.J0l, g.J[1], g.J[2])
+        Y = st.r2c(u_slab, loc)                                   # [J0l][J1][H]
+        Y = st.c2c(Y, loc, axis=1, dir=-1)
+        send = [st.contig(Y[:, q * g.J1l:(q + 1) * g.J1l, :]) for q in range(g.P)]
+        recv = self.comm.all_to_all(send)                         # from p: [J0l][J1l][H]
+        T = st.concat(recv, axis=0)                               # [J0][J1l][H]
+        return st.c2c(T, (g.J[0], g.J1l, g.J[2]), axis=0, dir=-1, scale=1.0 / g.N)
+
+    def inverse(self, uhat_t, m_first: int = 0):
+        g, st = self.g, self.st
+        nt = self.m_last - m_first + 1
+        tshape = (g.J[0], g.J1l, g.J[2])
+        T = st.c2c(uhat_t, tshape, axis=0, dir=+1, w=self.w[m_first:], nterms=nt, src_ts=0, w_ts=1)
+        # T: [nt][J0][J1l][H] -> to rank q: its planes of every term
+        send = [st.contig(T[:, q * g.J0l:(q + 1) * g.J0l]) for q in range(g.P)]
+        recv = self.comm.all_to_all(send)                         # from p: [nt][J0l][J1l][H]
+        Ts = st.concat(recv, axis=2)                              # [nt][J0l][J1][H]
+        loc = (g.J0l, g.J[1], g.J[2])
+        Ts = st.c2c(Ts, loc, axis=1, dir=+1, nterms=nt, src_ts=1)
+        return st.c2r(Ts, loc, m_first, self.m_last, self.dev1)
+
+    def apply(self, u_slab, m_first: int = 0):
+        if m_first > self.m_last:  # perturbation of a constant order: exact zeros (flap.cpp:163-166)
+            return u_slab * 0.0
+        return self.inverse(self.forward(u_slab), m_first)
+
+
+# --------------------------------------------------------------------------- device stages
+
+
+class _CAI:
+    """__cuda_array_interface__ view of a raw device pointer (zero copy into torch)."""
+
+    def __init__(self, ptr: int, shape, typestr="<f8"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class DeviceStages:
+    """The sm_100a stage kernels (C-ABI) on torch CUDA tensors.  Complex half-spectrum
+    arrays are torch.complex128 tensors; everything runs on the fw context's stream."""
+
+    def __init__(self, ctx):
+        import torch
+
+        from . import _capi
+
+        self.torch = torch
+        self.ctx = ctx
+        self.lib = _capi.load_library()
+        self.check = _capi.check
+        self.stream = torch.cuda.ExternalStream(ctx.stream)
+        lib = self.lib
+        vp, ll = C.c_void_p, C.c_longlong
+        lib.fw_stage_r2c.argtypes = [vp, C.c_int, C.POINTER(C.c_int), vp, vp, C.c_double]
+        lib.fw_stage_c2c.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, vp, vp, vp, ll, ll, ll,
+                                     C.c_int, C.c_double]
+        lib.fw_stage_c2r_accum.argtypes = [vp, C.c_int, C.POINTER(C.c_int), vp, ll, C.c_int, C.c_int, vp, vp, vp]
+        lib.fw_op_device_tables.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
+
+    @staticmethod
+    def _J(shape):
+        return (C.c_int * 3)(*shape)
+
+    def empty(self, shape, complex_=True):
+        t = self.torch
+        return t.empty(shape, dtype=t.complex128 if complex_ else t.float64, device="cuda")
+
+    def contig(self, x):
+        with self.torch.cuda.stream(self.stream):
+            return x.contiguous()
+
+    def concat(self, xs, axis):
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.cat(xs, dim=axis)
+
+    def r2c(self, x, shape):
+        H = self.empty((shape[0], shape[1], shape[2] // 2 + 1))
+        self.check(self.lib.fw_stage_r2c(self.ctx.handle, 3, self._J(shape), x.data_ptr(), H.data_ptr(), 1.0))
+        return H
+
+    def c2c(self, src, shape, axis, dir, w=None, nterms=1, src_ts=0, w_ts=0, scale=1.0):
+        h = shape[2] // 2 + 1
+        nh = shape[0] * shape[1] * h
+        dst = self.empty(((nterms,) if nterms > 1 else ()) + (shape[0], shape[1], h))
+        self.check(self.lib.fw_stage_c2c(self.ctx.handle, 3, self._J(shape), axis, dir, src.data_ptr(),
+                                         dst.data_ptr(), w.data_ptr() if w is not None else None,
+                                         nh * src_ts, nh, nh * w_ts, nterms, scale))
+        return dst
+
+    def c2r(self, src, shape, m_first, m_last, dev1):
+        out = self.empty(shape, complex_=False)
+        nh = shape[0] * shape[1] * (shape[2] // 2 + 1)
+        self.check(self.lib.fw_stage_c2r_accum(self.ctx.handle, 3, self._J(shape), src.data_ptr(),
+                                               nh if m_last > m_first else 0, m_first, m_last,
+                                               dev1.data_ptr() if dev1 is not None else None, out.data_ptr(),
+                                               None))
+        return out
+
+    def local_tables(self, op, geo: SlabGeometry):
+        """(w_local [M+1][J0][J1/P][H] complex-layout-compatible real weights, dev1 slab, m_last)
+        sliced from the operator's resident device tables (zero-copy views + one gather)."""
+        t = self.torch
+        w, d1, ml = C.c_void_p(), C.c_void_p(), C.c_int()
+        self.check(self.lib.fw_op_device_tables(op.handle, C.byref(w), C.byref(d1), C.byref(ml)))
+        J0, J1, J2 = geo.J
+        H = geo.H
+        wt = t.as_tensor(_CAI(w.value, (op.M + 1, J0, J1, H)), device="cuda")
+        dt = t.as_tensor(_CAI(d1.value, (J0, J1, J2)), device="cuda")
+        with t.cuda.stream(self.stream):
+            wl = wt[:, :, geo.cols, :].contiguous()
+            dl = dt[geo.rows].contiguous()
+        return wl, dl, ml.value
+
+
+class TorchComm:
+    """all-to-all of equal-shape blocks over the default torch.distributed group."""
+
+    def __init__(self, stream=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.stream = torch, dist, stream
+
+    def all_to_all(self, blocks):
+        t = self.torch
+        ctx = t.cuda.stream(self.stream) if self.stream is not None else _null()
+        with ctx:
+            send = t.stack([b.reshape(-1) for b in blocks])
+            recv = t.empty_like(send)
+            if send.is_complex():
+                self.dist.all_to_all_single(t.view_as_real(recv), t.view_as_real(send))
+            else:
+                self.dist.all_to_all_single(recv, send)
+            return [recv[p].reshape(blocks[0].shape) for p in range(len(blocks))]
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def slab_apply_device(op, u_slab, geo: SlabGeometry, ctx, comm: Optional[object] = None, m_first: int = 0):
+    """One distributed apply on the device: u_slab (torch CUDA float64 [J0/P][J1][J2])."""
+    st = DeviceStages(ctx)
+    wl, dl, ml = st.local_tables(op, geo)
+    if comm is None:
+        comm = TorchComm(st.stream) if geo.P > 1 else _SelfComm()
+    return SlabApply(geo, st, comm, wl, dl, ml).apply(u_slab, m_first)
+
+
+class _SelfComm:
+    def all_to_all(self, blocks):
+        return list(blocks)
+
+
+def slab_of(a: np.ndarray, geo: SlabGeometry) -> np.ndarray:
+    return np.ascontiguousarray(a[geo.rows])

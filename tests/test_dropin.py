@@ -49,3 +49,13 @@ def test_reference_acceptance_on_b200(criterion, tmp_path):
     assert r.returncode == 0 and "[PASS]" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
     if criterion != 5:  # criterion 5 uses constant orders only: its perturbations are exact host zeros
         assert n > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(os.path.join(BUILD, "seismic_gpu_check")), reason="drop-in not built")
+def test_cpp_gpu_seismic_stepper(tmp_path):
+    """fwave::gpu::SeismicStepper (reference API, fused device stepper) against the
+    reference's classical-limit LFFP test and against the reference CPU stepper."""
+    r = subprocess.run([os.path.join(BUILD, "seismic_gpu_check")], cwd=tmp_path, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "[PASS]" in r.stdout, r.stdout + r.stderr
