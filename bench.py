@@ -325,6 +325,17 @@ def run_c5(args):
         torch.distributed.destroy_process_group()
 
 
+def _fast_exit():
+    """torch tensors allocated on the fw context's stream must not outlive that stream;
+    skip interpreter teardown once the line is printed and the GPU is idle."""
+    import torch
+
+    torch.cuda.synchronize()
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -334,10 +345,10 @@ def main():
         from paper_2311_13049_b200 import configs as _c
 
         run_slab(args, _c.c3 if args.workload == "c3" else _c.c4, args.workload.upper())
-        return
+        _fast_exit()
     if args.workload == "c5":
         run_c5(args)
-        return
+        _fast_exit()
     rank, world, local = dist_env()
     import torch
 

@@ -68,7 +68,7 @@ void* fw_ctx_stream(fw_ctx ctx);
 /* number of kernels this context has launched so far (diagnostics / bench) */
 long long fw_ctx_launches(fw_ctx ctx);
 /* diagnostics: persistent-kernel phase timestamps (needs FW_TRACE=1 at context creation);
- * out receives 2 x 16 x 136 x 4 unsigned 64-bit globaltimer values */
+ * out receives 2 x 32 x 136 x 8 unsigned 64-bit globaltimer values */
 int fw_ctx_trace(fw_ctx ctx, unsigned long long* out);
 
 /* ---- operator: ExpansionOperator resident on the device ----

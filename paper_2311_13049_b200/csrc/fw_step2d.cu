@@ -38,7 +38,6 @@ namespace fw {
 namespace s2d {
 
 constexpr int KRING = kStep2dRing;
-constexpr int NWC = 4;  // columns per CTA (two mirror pairs)
 
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
 __host__ __device__ constexpr int npass(int n) { return (ilog2c(n) + 3) / 4; }
@@ -59,6 +58,9 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void red_relaxed_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 // whole warp waits until *cnt >= target
 __device__ __forceinline__ void warp_wait(const unsigned long long* cnt, unsigned long long target) {
   if ((threadIdx.x & 31) == 0) {
@@ -74,7 +76,6 @@ __device__ __forceinline__ void warp_signal(unsigned long long* cnt, unsigned lo
   if ((threadIdx.x & 31) == 0) red_release_add(cnt, v);
 }
 // named barriers: 1, 2 = column group g (4 warps), 5 = all 8 column warps
-__device__ __forceinline__ void colbar() { asm volatile("bar.sync 5, 256;" ::: "memory"); }
 __device__ __forceinline__ void groupbar(int g) { asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory"); }
 template <int N>
 __device__ __forceinline__ void setmaxnreg_dec() {
@@ -93,11 +94,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// optional instrumentation: trace[(sel*16 + warp)*136 + t][4] = globaltimer at phase marks
+// optional instrumentation: trace[(sel*32 + warp)*136 + t][8] = globaltimer at phase marks
 #define FW_TRACE(t, slot)                                                                              \
   do {                                                                                                 \
     if (prm.trace && (threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 100))               \
-      prm.trace[(((size_t)(blockIdx.x == 0 ? 0 : 1) * 16 + (threadIdx.x >> 5)) * 136 + (t)) * 4 + (slot)] = \
+      prm.trace[(((size_t)(blockIdx.x == 0 ? 0 : 1) * 32 + (threadIdx.x >> 5)) * 136 + (t)) * 8 + (slot)] = \
           gtimer();                                                                                    \
   } while (0)
 
@@ -151,30 +152,6 @@ __device__ __forceinline__ int padq(int q) {
   return q + (q >> PADSH);
 }
 
-// Middle pass PASS of an N-point C2C held by ONE warp in buf (padded), in place.
-template <int N, int PASS, int DIR, int PADSH>
-__device__ __forceinline__ void warp_pass(double2* buf, const double2* tw) {
-  constexpr int R = radix(N, PASS);
-  constexpr int T = N / R;
-  constexpr int NB = T / 32;
-  static_assert(T % 32 == 0, "warp pass needs >= 32 butterflies");
-  const int lane = threadIdx.x & 31;
-  double2 a[NB][R];
-#pragma unroll
-  for (int j = 0; j < NB; ++j)
-#pragma unroll
-    for (int r = 0; r < R; ++r) a[j][r] = buf[padq<PADSH>(lane + 32 * j + r * T)];
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    const int i = lane + 32 * j;
-    butterfly<N, PASS, DIR>(a[j], i, tw);
-#pragma unroll
-    for (int r = 0; r < R; ++r) buf[padq<PADSH>(out_index<N, PASS>(i, r))] = a[j][r];
-  }
-  __syncwarp();
-}
-
 // R2C post-processing X[k] from Z[k], Z[h-k] (fwcanon fwc_r2c), 1 <= k < h
 __device__ __forceinline__ double2 post_r2c(double2 A, double2 Bz, double2 wk) {
   const double2 B = make_double2(Bz.x, -Bz.y);
@@ -199,103 +176,209 @@ __device__ __forceinline__ double2 pre_c2r(double2 A, double2 Xhk, bool k0, doub
   return make_double2(E.x - O.y, E.y + O.x);
 }
 
-// F2 staging: element (k0, cc) of the CTA's 4 columns, XOR swizzled
-__device__ __forceinline__ int jidx(int k0, int cc) { return k0 * 4 + (cc ^ ((k0 >> 1) & 3)); }
+// ---------------------------------------------------------------- async copies (bulk + mbarrier)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n FW_MBW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra FW_MBW_%=;\n}" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
 
 // --------------------------------------------------------------------------
-// Column slots: slot 0 = {0, h}, slot s in [1, h/2) = {s, h-s}, slot h/2 = {h/2}.
-// CTA b owns slots 2b and 2b+1; column warp pair cw: slot 2b + (cw >> 1), member cw & 1.
+// Geometry.  Column slots: slot 0 = {0, h}, slot s in [1, h/2) = {s, h-s},
+// slot h/2 = {h/2}.  Column group g (warps 4g..4g+3) of CTA b owns slot
+// b + g * gridDim.x and transforms both members of the pair at once.  Row pair
+// p (warps 8+2p, 9+2p: 64 lanes, one radix-8 butterfly per lane and pass) owns
+// row r0 + p of the CTA's rows [r0, r1).
+//
+// Shared-memory layouts are chosen so that every FFT pass is IN PLACE PER
+// BUTTERFLY (a butterfly writes its outputs to the slots its inputs came from):
+// a thread then holds one butterfly at a time, and the padding below makes every
+// pass conflict-free.  Only where data lives changes; the arithmetic is the
+// canonical Stockham plan of fw_fft.cuh.
 template <int J0, int J1, int RMAX>
 struct Geo {
   static constexpr int H = J1 / 2 + 1;
   static constexpr int h = J1 / 2;
   static constexpr int NSLOT = h / 2 + 1;
-  static constexpr int NG = (NSLOT + 1) / 2;  // CTAs with columns
-  static constexpr int NT = 512;               // 8 column warps (2 groups of 4) + 8 row warps
-  static constexpr int PADC = ilog2c(radix(J0, 0));
-  static constexpr int PADR = 4;
-  static constexpr int LCOL = J0 + (J0 >> PADC) + 2;  // per column work buffer
-  static constexpr int LROW = h + (h >> PADR) + 2;    // per row-warp work buffer
-  static constexpr int PC = npass(J0);
-  static constexpr int PR = npass(h);
+  static constexpr int NT = 768;  // 8 column warps (2 groups of 4) + 16 row warps (8 pairs)
+  // column plan (J0 points, 3 passes)
+  static constexpr int CR0 = radix(J0, 0), CR1 = radix(J0, 1), CR2 = radix(J0, 2);
+  static constexpr int CT0 = J0 / CR0, CT1 = J0 / CR1, CT2 = J0 / CR2;
+  static constexpr int CP1 = CR0;  // pprod(J0, 1)
+  static constexpr int CL1 = ilog2c(CR1), CLT = ilog2c(CT1);
+  // row plan (h points, 3 radix-8 passes of 64 butterflies)
+  static constexpr int RR0 = radix(h, 0), RR1 = radix(h, 1), RR2 = radix(h, 2);
+  static constexpr int RT = h / RR0;
+  static constexpr int RP1 = RR0;
+  static constexpr int RLT = ilog2c(RT);
+  static constexpr int LCOL = J0 + (J0 >> CL1) + (J0 >> CLT) + 1;  // per column work buffer
+  static constexpr int LROW = (h + (h >> RLT)) | 1;                // per row work buffer (odd)
   static constexpr int TWC = twtotal(J0);
   static constexpr int TWR = twtotal(h);
   static constexpr int TWP = h + 1;
   static constexpr size_t OFF_TWR = TWC;
   static constexpr size_t OFF_TWP = TWC + TWR;
-  static constexpr size_t OFF_U = TWC + TWR + TWP;              // uhat [4][J0]
-  static constexpr size_t OFF_CW = OFF_U + (size_t)NWC * J0;      // column work [2][LCOL] (one per group)
-  static constexpr size_t OFF_RW = OFF_CW + (size_t)2 * LCOL;    // row work [RMAX][LROW]
-  static constexpr size_t NELEM = OFF_RW + (size_t)RMAX * LROW;
+  static constexpr size_t OFF_CW = TWC + TWR + TWP;                // column work [2 groups][2 members][LCOL]
+  static constexpr size_t OFF_RW = OFF_CW + (size_t)4 * LCOL;      // row work [RMAX][LROW]
+  static constexpr size_t OFF_DEV = OFF_RW + (size_t)RMAX * LROW;  // row (s-s0)^m landing [RMAX][J1 doubles]
+  static constexpr size_t NELEM = OFF_DEV + (size_t)RMAX * (J1 / 2);
   static constexpr size_t SMEM = NELEM * sizeof(double2);
-  static_assert(PC >= 2 && PC <= 3 && PR >= 2 && PR <= 3, "2 or 3 passes per FFT");
+  // tensor memory: [0,128) row accumulators (16 warps x 32 columns), [128, 128 + 8 CR0) uhat
+  static constexpr int TM_U = 128;
+  static constexpr int TM_COLS = 256;
+  static_assert(TM_U + 2 * 4 * CR0 <= TM_COLS, "tensor memory budget");
+  static_assert(2 * CT0 == 128, "column pass 0: one butterfly per group thread");
+  static_assert(npass(J0) == 3 && npass(h) == 3, "3-pass plans");
+  static_assert(RR0 == 8 && RR1 == 8 && RR2 == 8 && RT == 64, "row pair: one radix-8 butterfly per lane");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
-  static_assert(RMAX <= 8, "at most 8 row warps");
-  static_assert(h / radix(h, 0) % 32 == 0, "row pass 0 lane mapping");
+  static_assert(RMAX <= 8, "at most 8 row pairs");
+
+  // column layouts: pass-1 input (i, r) = logical i + CT1 r lives at i CR1 + r
+  __device__ static __forceinline__ int cpad(int pos) { return pos + (pos >> CL1) + (pos >> CLT); }
+  __device__ static __forceinline__ int c_p0out(int e) { return cpad((e % CT1) * CR1 + e / CT1); }
+  __device__ static __forceinline__ int c_p1(int i, int r) { return cpad(i * CR1 + r); }
+  __device__ static __forceinline__ int c_p2in(int e) {
+    const int i = (e / (CP1 * CR1)) * CP1 + e % CP1, r = (e / CP1) % CR1;
+    return cpad(i * CR1 + r);
+  }
+  // row layouts: pass-0 input natural; passes 0 and 1 in place
+  __device__ static __forceinline__ int rpad(int pos) { return pos + (pos >> RLT); }
+  __device__ static __forceinline__ int r_p1raw(int e) { return e / RR0 + RT * (e % RR0); }
+  __device__ static __forceinline__ int r_p1in(int e) { return rpad(r_p1raw(e)); }
+  __device__ static __forceinline__ int r_p2in(int e) {
+    const int i1 = (e / (RP1 * RR1)) * RP1 + e % RP1, r1 = (e / RP1) % RR1;
+    return rpad(r_p1raw(i1 + RT * r1));
+  }
 };
 
-// ---------------------------------------------------------------- column group: J0-point C2C
-// Four warps (128 threads, cg = 0..127, group barrier `gbar`) transform one column.
-// Pass 0 reads src(q) (q = i + r*T0); the last pass writes each butterfly's
-// outputs back to the slots it read, so `work` ends holding the column in
-// natural order (padded).
-template <int J0, int DIR, int PADSH, class Src, class GBar>
-__device__ __forceinline__ void column_c2c(double2* work, const double2* tw, int cg, Src src, GBar gbar) {
-  constexpr int P = npass(J0);
+__device__ __forceinline__ void tmem_ld32_nw(unsigned taddr, unsigned* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16_nw(unsigned taddr, unsigned* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16_nw(unsigned taddr, const unsigned* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+               :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(unsigned taddr, unsigned* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ double tm_d(const unsigned* v, int k) { return __hiloint2double((int)v[2 * k + 1], (int)v[2 * k]); }
+__device__ __forceinline__ void tm_put(unsigned* v, int k, double x) {
+  v[2 * k] = (unsigned)__double2loint(x);
+  v[2 * k + 1] = (unsigned)__double2hiint(x);
+}
+__device__ __forceinline__ void pairbar(int p) { asm volatile("bar.sync %0, 64;" ::"r"(4 + p) : "memory"); }
+__device__ __forceinline__ void rowsbar() { asm volatile("bar.sync 3, 512;" ::: "memory"); }
+
+// ---------------------------------------------------------------- column group: 2 x J0-point C2C
+// 128 threads (cg), both members of a mirror pair.  Pass 0 takes each thread's CR0
+// inputs in registers (member cg / CT0, butterfly cg % CT0, element q = cg % CT0 + r CT0);
+// passes 1 and 2 run one butterfly at a time in place; pass 2 hands the natural-order
+// outputs q = i + r CT2 of both members to epilogue(i, X0[], X1[]).
+template <class G, int DIR, class GBar, class Hook, class Epi, class Mark>
+__device__ __forceinline__ void column_pair(double2* work, const double2* tw, int cg, double2 (&a)[G::CR0], GBar gbar,
+                                            Hook after_pass0, Epi epilogue, Mark mark) {
+  constexpr int J0 = G::CT0 * G::CR0;
   {
-    constexpr int R = radix(J0, 0);
-    constexpr int T = J0 / R;
-    static_assert(T <= 128, "column pass 0");
-    if (cg < T) {
-      const int i = cg;
-      double2 a[R];
+    const int mbr = cg / G::CT0, I = cg % G::CT0;
+    Dft<G::CR0, DIR>::run(a);
+    double2* wb = work + mbr * G::LCOL;
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[r] = src(i + r * T);
-      Dft<R, DIR>::run(a);
-#pragma unroll
-      for (int r = 0; r < R; ++r) work[padq<PADSH>(i * R + r)] = a[r];
-    }
-    gbar();
+    for (int r = 0; r < G::CR0; ++r) wb[G::c_p0out(I * G::CR0 + r)] = a[r];
   }
-  if constexpr (P == 3) {  // middle pass, in place across the group
-    constexpr int R = radix(J0, 1);
-    constexpr int T = J0 / R;
-    static_assert(T <= 128, "column middle pass: at most one butterfly per thread");
-    double2 a[R];
-    if (cg < T) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) a[r] = work[padq<PADSH>(cg + r * T)];
-    }
-    gbar();
-    if (cg < T) {
-      butterfly<J0, 1, DIR>(a, cg, tw);
-#pragma unroll
-      for (int r = 0; r < R; ++r) work[padq<PADSH>(out_index<J0, 1>(cg, r))] = a[r];
-    }
-    gbar();
-  }
-  {
-    constexpr int PL = P - 1;
-    constexpr int R = radix(J0, PL);
-    constexpr int T = J0 / R;
+  gbar();
+  mark(3);
+  after_pass0();
 #pragma unroll 1
-    for (int i = cg; i < T; i += 128) {
-      double2 a[R];
+  for (int bi = cg; bi < 2 * G::CT1; bi += 128) {
+    const int mbr = bi / G::CT1, i = bi % G::CT1;
+    double2* wb = work + mbr * G::LCOL;
+    double2 c[G::CR1];
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[r] = work[padq<PADSH>(i + r * T)];
-      butterfly<J0, PL, DIR>(a, i, tw);
+    for (int r = 0; r < G::CR1; ++r) c[r] = wb[G::c_p1(i, r)];
+    butterfly<J0, 1, DIR>(c, i, tw);
 #pragma unroll
-      for (int r = 0; r < R; ++r) work[padq<PADSH>(i + r * T)] = a[r];
-    }
+    for (int r = 0; r < G::CR1; ++r) wb[G::c_p1(i, r)] = c[r];
   }
+  gbar();
+  mark(4);
+#pragma unroll 1
+  for (int i = cg; i < G::CT2; i += 128) {
+    double2 c0[G::CR2], c1[G::CR2];
+#pragma unroll
+    for (int r = 0; r < G::CR2; ++r) {
+      const int p = G::c_p2in(i + r * G::CT2);
+      c0[r] = work[p];
+      c1[r] = work[G::LCOL + p];
+    }
+    butterfly<J0, 2, DIR>(c0, i, tw);
+    butterfly<J0, 2, DIR>(c1, i, tw);
+    epilogue(i, c0, c1);
+  }
+}
+
+// ---------------------------------------------------------------- row pair: h-point C2C
+// passes 0 and 1 in place (pass-0 input in natural order, padded); returns after the
+// pair barrier that follows pass 1.  Lane l (0..63) owns butterfly l of every pass.
+template <class G, int DIR>
+__device__ __forceinline__ void row_passes01(double2* work, const double2* tw, int l, int pair) {
+  constexpr int h = G::h;
+  {
+    double2 a[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = work[G::rpad(l + r * G::RT)];
+    Dft<8, DIR>::run(a);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = a[r];
+  }
+  pairbar(pair);
+  {
+    double2 a[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = work[G::r_p1in(l + r * G::RT)];
+    butterfly<h, 1, DIR>(a, l, tw);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) work[G::r_p1in(l + r * G::RT)] = a[r];
+  }
+  pairbar(pair);
 }
 
 // --------------------------------------------------------------------------
 template <int J0, int J1, int RMAX>
-__global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2DParams prm) {
+__global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
   using G = Geo<J0, J1, RMAX>;
   constexpr int H = G::H, h = G::h, NT = G::NT;
+  constexpr int CR0 = G::CR0, CT0 = G::CT0;
   extern __shared__ __align__(16) double2 sm[];
+  __shared__ __align__(8) unsigned long long dbar[RMAX];  // row dev-landing mbarriers
+  __shared__ unsigned tmem_base_sh;
   double2* twc = sm;
   double2* twr = sm + G::OFF_TWR;
   double2* twp = sm + G::OFF_TWP;
@@ -323,18 +406,20 @@ __global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2
       }
     };
     fill(twc, twoff(J0, 1), pprod(J0, 1), radix(J0, 1));
-    if constexpr (G::PC >= 3) fill(twc, twoff(J0, 2), pprod(J0, 2), radix(J0, 2));
+    fill(twc, twoff(J0, 2), pprod(J0, 2), radix(J0, 2));
     fill(twr, twoff(h, 1), pprod(h, 1), radix(h, 1));
-    if constexpr (G::PR >= 3) fill(twr, twoff(h, 2), pprod(h, 2), radix(h, 2));
+    fill(twr, twoff(h, 2), pprod(h, 2), radix(h, 2));
     for (int e = tid; e <= h; e += NT) twp[e] = prm.master[e * (kTwMaster / J1)];
   }
-  __shared__ unsigned tmem_base_sh;
-  if (warp == 0) {  // 128 TMEM columns: row accumulators (2 row warps per lane quadrant x 64 columns)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(&tmem_base_sh))
+  if (tid < RMAX) mbar_init(&dbar[tid], 1);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tmem_base_sh)),
+                 "n"(G::TM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -344,284 +429,302 @@ __global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2
   const int nterms = M + 1 - prm.m_first;
   const int ntot = prm.nops * nterms;
 
-  if (warp < 2 * NWC) {
+  if (warp < 8) {
     // ============================================ column warps (2 groups of 4)
-    if (b >= G::NG) return;
-    const int g = warp >> 2;       // group: member g of each mirror slot (0: k = s, 1: k = h - s)
-    const int cg = tid & 127;      // thread within the group
-    const int ct = tid;            // 0..255 within the column warps
-    // column q = 2*sl + member of this CTA: slot s -> {s, h-s}; slot 0 -> {0, h}; slot h/2 -> {h/2, -}
-    auto colno = [&](int q) {
-      const int s = 2 * b + (q >> 1);
-      if (s >= G::NSLOT) return -1;
-      if (s == 0) return (q & 1) ? h : 0;
-      if (s == h / 2) return (q & 1) ? -1 : h / 2;
-      return (q & 1) ? h - s : s;
+    setmaxnreg_inc<112>();
+    const int g = warp >> 2;   // group
+    const int cg = tid & 127;  // thread within the group
+    const int slot = b + g * nblk;
+    const int mbr = cg / CT0, i0 = cg % CT0;
+    auto colno = [&](int m_) {
+      if (slot >= G::NSLOT) return -1;
+      if (slot == 0) return m_ ? h : 0;
+      if (slot == h / 2) return m_ ? -1 : h / 2;
+      return m_ ? h - slot : slot;
     };
-    double2* works = sm + G::OFF_CW;  // the 2 group work buffers (line stride LCOL)
-    double2* work = works + (size_t)g * G::LCOL;
-    auto gb = [g] { groupbar(g); };
-    int nz = 0;
-    for (int q = 0; q < 4; ++q) {
-      const int col = colno(q);
-      if (col >= 0 && col < h) ++nz;  // column h feeds Z_0 and produces no Z of its own
-    }
+    if (slot < G::NSLOT) {
+      double2* work = sm + G::OFF_CW + (size_t)g * 2 * G::LCOL;  // members at +0, +LCOL
+      auto gb = [g] { groupbar(g); };
+      const int mycol = colno(mbr);
+      const int kA = colno(0), kB = colno(1);
+      int nz = 0;
+      if (kA >= 0 && kA < h) ++nz;
+      if (kB >= 0 && kB < h) ++nz;  // column h feeds Z_0 and produces no Z of its own
+      // this thread's uhat values: TMEM lane (32 (warp & 3) + lane), columns TM_U + g 4 CR0 + [0, 4 CR0)
+      const unsigned tu = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_U + g * 4 * CR0);
 
-    // ---- F2: forward columns -> uhat (pass 0 straight from Y)
-    warp_wait(cY, (unsigned long long)J0);
-    colbar();  // every column thread has seen all rows
-    const double inv = 1.0 / ((double)J0 * (double)J1);
-    for (int sl = 0; sl < 2; ++sl) {
-      const int q = 2 * sl + g;
-      const int col = colno(q);
-      double2* uh = sm + G::OFF_U + (size_t)q * J0;
-      column_c2c<J0, -1, G::PADC>(
-          work, twc, cg,
-          [&](int k0) { return col >= 0 ? __ldcg(&prm.Y[(size_t)k0 * H + col]) : make_double2(0.0, 0.0); }, gb);
-      gb();
-      for (int k0 = cg; k0 < J0; k0 += 128) {
-        const double2 v = work[padq<G::PADC>(k0)];
-        uh[k0] = make_double2(v.x * inv, v.y * inv);
+      // ---- F2: forward columns -> uhat (pass 0 straight from Y) -> tensor memory
+      warp_wait(cY, (unsigned long long)J0);
+      gb();  // every thread of the group has seen all rows
+      {
+        double2 a[CR0];
+#pragma unroll
+        for (int r = 0; r < CR0; ++r)
+          a[r] = mycol >= 0 ? __ldcg(&prm.Y[(size_t)(i0 + r * CT0) * H + mycol]) : make_double2(0.0, 0.0);
+        double2 x0[G::CR2], x1[G::CR2];
+        int ix = 0;
+        column_pair<G, -1>(
+            work, twc, cg, a, gb, [] {},
+            [&](int i, const double2* c0, const double2* c1) {
+              ix = i;
+#pragma unroll
+              for (int r = 0; r < G::CR2; ++r) {
+                x0[r] = c0[r];
+                x1[r] = c1[r];
+              }
+            },
+            [](int) {});
+        gb();  // pass-2 reads done: the buffers may take the natural-order result
+        if (cg < G::CT2) {
+#pragma unroll
+          for (int r = 0; r < G::CR2; ++r) {
+            work[ix + r * G::CT2] = x0[r];
+            work[G::LCOL + ix + r * G::CT2] = x1[r];
+          }
+        }
+        gb();
+        const double inv = 1.0 / ((double)J0 * (double)J1);
+#pragma unroll
+        for (int c = 0; c < 4 * CR0; c += 32) {
+          unsigned v[32];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const double2 x = work[mbr * G::LCOL + i0 + (c / 4 + k) * CT0];
+            tm_put(v, 2 * k, x.x * inv);
+            tm_put(v, 2 * k + 1, x.y * inv);
+          }
+          tmem_st32(tu + c, v);
+        }
+        gb();
       }
-      gb();
+
+      double rmax = 0.0;
+      // ---- C(t): inverse columns -> pre-processed Z[t % KRING], column-major Z[k][k0]
+      for (int t = 0; t < ntot; ++t) {
+        FW_TRACE(t, 0);
+        const int op = t / nterms, m = prm.m_first + t % nterms;
+        const double* w = prm.w[op] + ((size_t)m * prm.wcols + (mycol >= 0 ? mycol : 0)) * J0 + i0;
+        if (cg == 0 && t + 1 < ntot) {  // the next term's weights of both columns -> L2
+          const int op1 = (t + 1) / nterms, m1 = prm.m_first + (t + 1) % nterms;
+          if (kA >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kA) * J0, J0 * sizeof(double));
+          if (kB >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kB) * J0, J0 * sizeof(double));
+        }
+        double2 a[CR0];
+#pragma unroll
+        for (int c = 0; c < 4 * CR0; c += 32) {
+          double wk[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) wk[k] = mycol >= 0 ? __ldg(&w[(c / 4 + k) * CT0]) : 0.0;
+          unsigned v[32];
+          tmem_ld32_nw(tu + c, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) a[c / 4 + k] = make_double2(wk[k] * tm_d(v, 2 * k), wk[k] * tm_d(v, 2 * k + 1));
+        }
+        FW_TRACE(t, 1);
+        if (t >= KRING) warp_wait(&cR[t - KRING], (unsigned long long)J0);
+        FW_TRACE(t, 2);
+        double2* Z = prm.T + (size_t)(t % KRING) * J0 * h;
+        // the previous term's Z columns are published once this term's pass 0 is done:
+        // by then its stores have drained and the release fence is cheap
+        column_pair<G, +1>(work, twc, cg, a, gb, [&] {
+          if (cg == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz);
+        }, [&](int i, const double2* xa, const double2* xb) {
+#pragma unroll
+          for (int r = 0; r < G::CR2; ++r) {
+            const int k0 = i + r * G::CT2;
+            if (kA == 0) {  // Z_0 from X_0 and X_h (member 1 = column h has no Z of its own)
+              if (prm.residue) rmax = fmax(rmax, fabs(xa[r].y) + fabs(xb[r].y));
+              __stcg(&Z[k0], pre_c2r(xa[r], xb[r], true, twp[0]));
+            } else if (kA == h / 2) {
+              __stcg(&Z[(size_t)kA * J0 + k0], pre_c2r(xa[r], xa[r], false, twp[kA]));
+            } else {
+              __stcg(&Z[(size_t)kA * J0 + k0], pre_c2r(xa[r], xb[r], false, twp[kA]));
+              __stcg(&Z[(size_t)kB * J0 + k0], pre_c2r(xb[r], xa[r], false, twp[kB]));
+            }
+          }
+        }, [&](int sl) { FW_TRACE(t, sl); });
+        FW_TRACE(t, 5);
+        gb();  // work buffers free again; all Z stores of the group issued
+        FW_TRACE(t, 6);
+      }
+      if (cg == 0 && ntot > 0) red_release_add(&cC[ntot - 1], (unsigned long long)nz);
+      if (prm.residue && rmax > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(prm.residue),
+                  (unsigned long long)__double_as_longlong(rmax));
+    }
+  } else {
+    // ============================================ row warps (8 pairs)
+    setmaxnreg_dec<64>();
+    const int rw = warp - 8;
+    const int pair = rw >> 1;
+    const int l = (rw & 1) * 32 + lane;  // lane within the pair = butterfly index
+    const int r0 = (int)(((long long)b * J0) / nblk);
+    const int r1 = (int)(((long long)(b + 1) * J0) / nblk);
+    const int nr = r1 - r0;
+    const bool active = pair < nr;
+    const int row = r0 + (active ? pair : 0);
+    // this warp's 32 TMEM columns in its lane quadrant: (s-s0)^m-weighted sums of outputs l + 64 r
+    const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 32u * (unsigned)(rw >> 2);
+    double2* work = sm + G::OFF_RW + (size_t)(active ? pair : 0) * G::LROW;
+    const double2* dl = sm + G::OFF_DEV + (size_t)(active ? pair : 0) * (J1 / 2);  // (s-s0)^m row landing
+    unsigned long long* bar = &dbar[active ? pair : 0];
+    unsigned dphase = 0;
+    // bulk-load the (s-s0)^m row of term t into the landing buffer (pair's first lane)
+    auto issue_dev = [&](int t) {
+      if (t >= ntot) return;
+      const int op1 = t / nterms, m1 = prm.m_first + t % nterms;
+      if (m1 < 1) return;
+      if (l == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, J1 * sizeof(double));
+        bulk_g2s((void*)dl, prm.dev[op1] + (size_t)(m1 - 1) * J0 * J1 + (size_t)row * J1, J1 * sizeof(double), bar);
+      }
+    };
+
+    if (active) {
+      issue_dev(0);
+      // ---- F1: R2C of the row -> Y
+      const double2* u2 = reinterpret_cast<const double2*>(prm.u) + (size_t)row * h;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = u2[l + r * G::RT];
+      pairbar(pair);
+      row_passes01<G, -1>(work, twr, l, pair);
+      double2 a[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l + r * G::RT)];
+      butterfly<h, 2, -1>(a, l, twr);
+      pairbar(pair);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = a[r];
+      pairbar(pair);
+      double2* Yr = prm.Y + (size_t)row * H;
+      for (int jj = l; jj <= h / 2; jj += 64) {
+        if (jj == 0) {
+          const double2 z0 = work[0];
+          __stcg(&Yr[0], make_double2(z0.x + z0.y, 0.0));
+          __stcg(&Yr[h], make_double2(z0.x - z0.y, 0.0));
+        } else {
+          const double2 A = work[G::rpad(jj)];
+          const double2 B = work[G::rpad(h - jj)];
+          __stcg(&Yr[jj], post_r2c(A, B, twp[jj]));
+          if (jj != h - jj) __stcg(&Yr[h - jj], post_r2c(B, A, twp[h - jj]));
+        }
+      }
+      pairbar(pair);  // both warps' Y stores precede the signal
+      if (!(rw & 1)) warp_signal(cY, 1ull);
+      unsigned z[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) z[e] = 0u;
+      tmem_st32(tacc, z);
     }
 
-    double rmax = 0.0;
-    // ---- C(t): inverse columns -> pre-processed Z[t % KRING]
+    // ---- R(t): h-point C2C of the pre-processed row + recombination
+    const int f = tid - 256, rs = f & 7, kq = f >> 3;
+    double2* wr = sm + G::OFF_RW + (size_t)rs * G::LROW;
     for (int t = 0; t < ntot; ++t) {
       const int op = t / nterms;
       const int m = prm.m_first + t % nterms;
       FW_TRACE(t, 0);
-      if (t >= KRING) warp_wait(&cR[t - KRING], (unsigned long long)J0);
+      rowsbar();  // every row warp is done with its work buffer (F1 or term t - 1)
       FW_TRACE(t, 1);
-      double2* Z = prm.T + (size_t)(t % KRING) * J0 * h;
-      for (int sl = 0; sl < 2; ++sl) {
-        const int q = 2 * sl + g;
-        const int col = colno(q);
-        const bool valid = col >= 0;
-        const double2* uh = sm + G::OFF_U + (size_t)q * J0;
-        const double* w = prm.w[op] + ((size_t)m * prm.wcols + (valid ? col : 0)) * J0;  // [m][c][k0]
-        if (cg == 0 && valid) {  // the next use of this column's weights -> L2
-          const int t1 = sl == 0 ? t : t + 1;
-          if (t1 < ntot) {
-            const int op1 = t1 / nterms, m1 = prm.m_first + t1 % nterms;
-            const int q1 = sl == 0 ? q + 2 : q - 2;
-            const int col1 = colno(q1);
-            if (col1 >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + col1) * J0, J0 * sizeof(double));
-          }
+      warp_wait(&cC[t], (unsigned long long)h);
+      FW_TRACE(t, 2);
+      {  // the CTA's rows of Z[t] (column-major [k][k0]): 8 row slots x 4 k per warp load,
+         // each k a contiguous run of nr elements -> row work buffers, natural order
+        const double2* Zt = prm.T + (size_t)(t % KRING) * J0 * h + r0 + rs;
+        if (rs < nr) {
+          double2 v[h / 64];
+#pragma unroll
+          for (int it = 0; it < h / 64; ++it) v[it] = __ldcg(&Zt[(size_t)(it * 64 + kq) * J0]);
+#pragma unroll
+          for (int it = 0; it < h / 64; ++it) wr[G::rpad(it * 64 + kq)] = v[it];
         }
-        column_c2c<J0, +1, G::PADC>(
-            work, twc, cg,
-            [&](int k0) {
-              const double2 v = uh[k0];
-              const double wk = valid ? __ldg(&w[k0]) : 0.0;
-              return make_double2(wk * v.x, wk * v.y);
-            },
-            gb);
-        colbar();  // both members of slot 2b + sl are complete in the 2 work buffers
-        FW_TRACE(t, 2);
-        // C2R pre-processing of the mirror pair -> Z rows (k = s and k = h - s)
-        const int kA = colno(2 * sl), kB = colno(2 * sl + 1);
-        for (int e = ct; e < J0 * 2; e += 256) {
-          const int k0 = e >> 1, mbr = e & 1;
-          const int k = mbr ? kB : kA;
-          if (k < 0 || k == h) continue;
-          const double2 X = works[mbr * G::LCOL + padq<G::PADC>(k0)];
-          double2 z;
-          if (k == 0) {  // Z_0 from X_0 and X_h
-            const double2 B = works[G::LCOL + padq<G::PADC>(k0)];
-            if (prm.residue) rmax = fmax(rmax, fabs(X.y) + fabs(B.y));
-            z = pre_c2r(X, B, true, twp[0]);
-          } else if (k == h / 2) {
-            z = pre_c2r(X, X, false, twp[k]);
-          } else {
-            z = pre_c2r(X, works[(mbr ^ 1) * G::LCOL + padq<G::PADC>(k0)], false, twp[k]);
-          }
-          __stcg(&Z[(size_t)k0 * h + k], z);
-        }
-        colbar();  // work buffers free again
       }
-      if (ct == 0) red_release_add(&cC[t], (unsigned long long)nz);
       FW_TRACE(t, 3);
-    }
-    if (prm.residue && rmax > 0.0)
-      atomicMax(reinterpret_cast<unsigned long long*>(prm.residue), (unsigned long long)__double_as_longlong(rmax));
-    return;
-  }
-
-  // ============================================ row warps
-  const int rw = warp - 2 * NWC;
-  const int r0 = (int)(((long long)b * J0) / nblk);
-  const int r1 = (int)(((long long)(b + 1) * J0) / nblk);
-  if (rw < r1 - r0) {
-  const int row = r0 + rw;
-  // this warp's 64 TMEM columns in its lane quadrant: butterfly j uses columns [32 j, 32 j + 32)
-  const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 64u * (unsigned)((warp - 2 * NWC) >> 2);
-  double2* work = sm + G::OFF_RW + (size_t)rw * G::LROW;
-  constexpr int R0 = radix(h, 0);
-  constexpr int T0 = h / R0;
-  constexpr int RL = radix(h, G::PR - 1);
-  constexpr int TL = h / RL;
-  constexpr int NBL = TL / 32;
-  static_assert(TL % 32 == 0, "row last pass");
-
-  // ---- F1: R2C of the row -> Y
-  {
-    const double2* u2 = reinterpret_cast<const double2*>(prm.u) + (size_t)row * h;
-#pragma unroll
-    for (int j = 0; j < T0 / 32; ++j) {
-      const int i = lane + 32 * j;
-      double2 a[R0];
-#pragma unroll
-      for (int r = 0; r < R0; ++r) a[r] = u2[i + r * T0];
-      Dft<R0, -1>::run(a);
-#pragma unroll
-      for (int r = 0; r < R0; ++r) work[padq<G::PADR>(i * R0 + r)] = a[r];
-    }
-    __syncwarp();
-    if constexpr (G::PR == 3) warp_pass<h, 1, -1, G::PADR>(work, twr);
-#pragma unroll
-    for (int j = 0; j < NBL; ++j) {
-      const int i = lane + 32 * j;
-      double2 a[RL];
-#pragma unroll
-      for (int r = 0; r < RL; ++r) a[r] = work[padq<G::PADR>(i + r * TL)];
-      butterfly<h, G::PR - 1, -1>(a, i, twr);
-#pragma unroll
-      for (int r = 0; r < RL; ++r) work[padq<G::PADR>(i + r * TL)] = a[r];
-    }
-    __syncwarp();
-    double2* Yr = prm.Y + (size_t)row * H;
-    for (int jj = lane; jj <= h / 2; jj += 32) {
-      if (jj == 0) {
-        const double2 z0 = work[0];
-        __stcg(&Yr[0], make_double2(z0.x + z0.y, 0.0));
-        __stcg(&Yr[h], make_double2(z0.x - z0.y, 0.0));
-      } else {
-        const double2 A = work[padq<G::PADR>(jj)];
-        const double2 B = work[padq<G::PADR>(h - jj)];
-        __stcg(&Yr[jj], post_r2c(A, B, twp[jj]));
-        if (jj != h - jj) __stcg(&Yr[h - jj], post_r2c(B, A, twp[h - jj]));
+      rowsbar();  // the tile is complete
+      // the CTA's rows of Z[t] are consumed (their values are in shared memory):
+      // the ring slot may be reused.  No release fence needed.
+      if (tid == 256) red_relaxed_add(&cR[t], (unsigned long long)nr);
+      FW_TRACE(t, 4);
+      if (!active) continue;
+      row_passes01<G, +1>(work, twr, l, pair);
+      FW_TRACE(t, 5);
+      const bool hasdev = m >= 1;
+      if (hasdev) {
+        mbar_wait(bar, dphase);
+        dphase ^= 1u;
       }
-    }
-    warp_signal(cY, 1ull);
-  }
-
-  // ---- R(t): h-point C2C of the pre-processed row + recombination
-  static_assert(NBL * RL * 2 * 2 == 64, "row accumulator = 64 TMEM columns per lane");
-  {
-    unsigned z[32];
+      {
+        double2 a[8];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) z[e] = 0u;
+        for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l + r * G::RT)];
+        butterfly<h, 2, +1>(a, l, twr);
 #pragma unroll
-    for (int j = 0; j < NBL; ++j) tmem_st32(tacc + 32u * j, z);
-  }
-
-  for (int t = 0; t < ntot; ++t) {
-    const int op = t / nterms;
-    const int m = prm.m_first + t % nterms;
-    if (lane == 0 && t + 1 < ntot) {  // next term's (s-s0)^m row -> L2
-      const int op1 = (t + 1) / nterms, m1 = prm.m_first + (t + 1) % nterms;
-      if (m1 >= 1) prefetch_l2(prm.dev[op1] + (size_t)(m1 - 1) * J0 * J1 + (size_t)row * J1, J1 * sizeof(double));
-    }
-    FW_TRACE(t, 0);
-    warp_wait(&cC[t], (unsigned long long)h);
-    FW_TRACE(t, 1);
-    const double2* Zr = prm.T + (size_t)(t % KRING) * J0 * h + (size_t)row * h;
-#pragma unroll
-    for (int j = 0; j < T0 / 32; ++j) {  // pass 0 (p = 1) straight from global
-      const int i = lane + 32 * j;
-      double2 a[R0];
-#pragma unroll
-      for (int r = 0; r < R0; ++r) a[r] = __ldcg(&Zr[i + r * T0]);
-      Dft<R0, +1>::run(a);
-#pragma unroll
-      for (int r = 0; r < R0; ++r) work[padq<G::PADR>(i * R0 + r)] = a[r];
-    }
-    warp_signal(&cR[t], 1ull);  // this row of Z[t] has been consumed: the slot may be reused
-    FW_TRACE(t, 2);
-    if constexpr (G::PR == 3) warp_pass<h, 1, +1, G::PADR>(work, twr);
-    const double* dv = (m >= 1) ? prm.dev[op] + (size_t)(m - 1) * J0 * J1 + (size_t)row * J1 : nullptr;
-#pragma unroll
-    for (int j = 0; j < NBL; ++j) {
-      const int i = lane + 32 * j;
-      asm volatile("" ::: "memory");  // keep the butterflies sequential (register pressure)
-      double2 a[RL];
-#pragma unroll
-      for (int r = 0; r < RL; ++r) a[r] = work[padq<G::PADR>(i + r * TL)];
-      double2 d[RL];
-      if (dv) {
-#pragma unroll
-        for (int r = 0; r < RL; ++r) d[r] = __ldg(reinterpret_cast<const double2*>(dv) + i + r * TL);
-      }
-      butterfly<h, G::PR - 1, +1>(a, i, twr);
-      unsigned v[32];
-      tmem_ld32(tacc + 32u * j, v);
-#pragma unroll
-      for (int r = 0; r < RL; ++r) {
-        double v0 = a[r].x, v1 = a[r].y;
-        if (dv) {
-          v0 = d[r].x * v0;
-          v1 = d[r].y * v1;
+        for (int r = 0; r < 8; ++r) {
+          double v0 = a[r].x, v1 = a[r].y;
+          if (hasdev) {
+            const double2 d = dl[l + r * G::RT];
+            v0 = d.x * v0;
+            v1 = d.y * v1;
+          }
+          double p0 = 0.0, p1 = 0.0;  // the reference's per-term partial: 0 + dev * x
+          p0 += v0;
+          p1 += v1;
+          a[r] = make_double2(p0, p1);
         }
-        double p0 = 0.0, p1 = 0.0;
-        p0 += v0;
-        p1 += v1;
-        double a0 = __hiloint2double((int)v[4 * r + 1], (int)v[4 * r]);
-        double a1 = __hiloint2double((int)v[4 * r + 3], (int)v[4 * r + 2]);
-        a0 += p0;
-        a1 += p1;
-        v[4 * r] = (unsigned)__double2loint(a0);
-        v[4 * r + 1] = (unsigned)__double2hiint(a0);
-        v[4 * r + 2] = (unsigned)__double2loint(a1);
-        v[4 * r + 3] = (unsigned)__double2hiint(a1);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          unsigned v[16];
+          tmem_ld16_nw(tacc + 16u * hf, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            tm_put(v, 2 * r, tm_d(v, 2 * r) + a[4 * hf + r].x);
+            tm_put(v, 2 * r + 1, tm_d(v, 2 * r + 1) + a[4 * hf + r].y);
+          }
+          tmem_st16_nw(tacc + 16u * hf, v);
+        }
+        tmem_wait_st();
       }
-      tmem_st32(tacc + 32u * j, v);
-    }
-    __syncwarp();  // work buffer reads done before the next term's pass 0 writes
-    FW_TRACE(t, 3);
-    if (m == M && !(prm.seismic && op == prm.nops - 1)) {  // operator complete: hand over
-      double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)row * J1);
-#pragma unroll
-      for (int j = 0; j < NBL; ++j) {
+      FW_TRACE(t, 6);
+      pairbar(pair);  // both warps are done with the landing buffer
+      issue_dev(t + 1);
+      FW_TRACE(t, 7);
+      if (m == M && !(prm.seismic && op == prm.nops - 1)) {  // operator complete: hand over
+        double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)row * J1);
         unsigned v[32];
-        tmem_ld32(tacc + 32u * j, v);
+        tmem_ld32(tacc, v);
 #pragma unroll
-        for (int r = 0; r < RL; ++r)
-          o[lane + 32 * j + r * TL] = make_double2(__hiloint2double((int)v[4 * r + 1], (int)v[4 * r]),
-                                                   __hiloint2double((int)v[4 * r + 3], (int)v[4 * r + 2]));
+        for (int r = 0; r < 8; ++r) o[l + r * G::RT] = make_double2(tm_d(v, 2 * r), tm_d(v, 2 * r + 1));
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = 0u;
-        tmem_st32(tacc + 32u * j, v);
+        tmem_st32(tacc, v);
       }
     }
-  }
 
-  // ---- seismic update (seismic.cpp:116-129)
-  if (prm.seismic) {
-    bool bad = false;
-    const double tau = prm.tau;
-    const double t2 = tau * tau;
-    const size_t rowoff = (size_t)row * J1;
-    const double2* cur = reinterpret_cast<const double2*>(prm.u + rowoff);
-    const double2* prev = reinterpret_cast<const double2*>(prm.prev + rowoff);
-    const double2* ap = reinterpret_cast<const double2*>(prm.ap + rowoff);
-    const double2* l1 = reinterpret_cast<const double2*>(prm.out[0] + rowoff);
-    const double2* c = reinterpret_cast<const double2*>(prm.c + rowoff);
-    const double2* eta = reinterpret_cast<const double2*>(prm.eta + rowoff);
-    const double2* tc = reinterpret_cast<const double2*>(prm.tc + rowoff);
-    double2* nx = reinterpret_cast<double2*>(prm.next + rowoff);
-    double2* l2o = reinterpret_cast<double2*>(prm.out[1] + rowoff);
-#pragma unroll
-    for (int j = 0; j < NBL; ++j) {
-      unsigned v[32];
-      tmem_ld32(tacc + 32u * j, v);
-#pragma unroll
-      for (int r = 0; r < RL; ++r) {
-        const int q = lane + 32 * j + r * TL;
+    // ---- seismic update (seismic.cpp:116-129)
+    if (active && prm.seismic) {
+      bool bad = false;
+      const double tau = prm.tau;
+      const double t2 = tau * tau;
+      const size_t rowoff = (size_t)row * J1;
+      const double2* cur = reinterpret_cast<const double2*>(prm.u + rowoff);
+      const double2* prev = reinterpret_cast<const double2*>(prm.prev + rowoff);
+      const double2* ap = reinterpret_cast<const double2*>(prm.ap + rowoff);
+      const double2* l1 = reinterpret_cast<const double2*>(prm.out[0] + rowoff);
+      const double2* c = reinterpret_cast<const double2*>(prm.c + rowoff);
+      const double2* eta = reinterpret_cast<const double2*>(prm.eta + rowoff);
+      const double2* tc = reinterpret_cast<const double2*>(prm.tc + rowoff);
+      double2* nx = reinterpret_cast<double2*>(prm.next + rowoff);
+      double2* l2o = reinterpret_cast<double2*>(prm.out[1] + rowoff);
+#pragma unroll 1
+      for (int r = 0; r < 8; ++r) {
+        unsigned v[4];
+        tmem_ld4(tacc + 4u * r, v);
+        const int q = l + r * G::RT;
         const double2 vc = cur[q], vp = prev[q], va = ap[q], v1 = l1[q], cc = c[q], ve = eta[q], vt = tc[q];
-        const double l2x = __hiloint2double((int)v[4 * r + 1], (int)v[4 * r]);
-        const double l2y = __hiloint2double((int)v[4 * r + 3], (int)v[4 * r + 2]);
+        const double l2x = tm_d(v, 0), l2y = tm_d(v, 1);
         const double c2x = cc.x * cc.x, c2y = cc.y * cc.y;
         const double nx0 = 2.0 * vc.x - vp.x + t2 * c2x * (ve.x * v1.x + vt.x * (l2x - va.x) / tau);
         const double nx1 = 2.0 * vc.y - vp.y + t2 * c2y * (ve.y * v1.y + vt.y * (l2y - va.y) / tau);
@@ -629,22 +732,21 @@ __global__ void __launch_bounds__(Geo<J0, J1, RMAX>::NT, 1) k_step2d(const Step2
         l2o[q] = make_double2(l2x, l2y);
         bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
       }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(prm.flag, prm.step);
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(prm.flag, prm.step);
   }
-  }  // active row warp
-  // all row warps are done with tensor memory: release it
+  // everyone is done with tensor memory: release it
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  asm volatile("bar.sync 7, 256;" ::: "memory");
+  __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 2 * NWC)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem_base) : "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(G::TM_COLS) : "memory");
 }
 
 template <int J0, int J1, int RMAX>
 cudaError_t launch_t(const Step2DParams& p, cudaStream_t st, int nblk) {
   using G = Geo<J0, J1, RMAX>;
-  if ((J0 + nblk - 1) / nblk > RMAX || G::NG > nblk) return cudaErrorInvalidConfiguration;
+  if ((J0 + nblk - 1) / nblk > RMAX || 2 * nblk < G::NSLOT) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_step2d<J0, J1, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
@@ -659,7 +761,7 @@ cudaError_t launch_t(const Step2DParams& p, cudaStream_t st, int nblk) {
 bool step2d_supported(int J0, int J1, int nsm) {
   if (!((J0 == 1024 && J1 == 1024) || (J0 == 512 && J1 == 1024))) return false;
   const int nslot = J1 / 4 + 1;
-  return nsm >= 148 && (nslot + 1) / 2 <= nsm;
+  return nsm >= 148 && nslot <= 2 * nsm;
 }
 
 int step2d_col_groups(int J1) { return (J1 / 2 + 1 + kStep2dCG - 1) / kStep2dCG; }

@@ -1,4 +1,11 @@
-"""Run a few C2 steps with FW_TRACE=1 and print the per-warp phase timeline of CTA 0 / CTA 100."""
+"""Run a few C2 steps with FW_TRACE=1 and print the per-warp phase timeline of CTA 0 / CTA 100
+of the persistent step kernel (fw_step2d.cu, FW_TRACE marks; 8 marks per warp and term).
+
+column warps: 0 term start | 1 weights + uhat loaded | 2 ring slot free | 3 pass 0 | 4 pass 1
+              | 5 pass 2 + pre-processing + Z stores | 6 group barrier
+row warps:    0 term start | 1 row barrier | 2 Z[t] complete | 3 tile loaded | 4 row barrier
+              | 5 passes 0-1 | 6 pass 2 + recombination | 7 pair barrier + next (s-s0)^m issued
+"""
 import ctypes as C
 import os
 import sys
@@ -17,26 +24,31 @@ st = fw.SeismicStepper(fw.build_medium(g, cfg.gamma, cfg.c0, 1.0, cfg.M), cfg.ph
 st.advance(3)
 lib = fw.load_library()
 lib.fw_ctx_trace.argtypes = [C.c_void_p, C.c_void_p]
-buf = np.zeros(2 * 16 * 136 * 4, dtype=np.uint64)
+buf = np.zeros(2 * 32 * 136 * 8, dtype=np.uint64)
 fw._capi.check(lib.fw_ctx_trace(ctx.handle, buf.ctypes.data))
-tr = buf.reshape(2, 16, 136, 4).astype(np.int64)
+tr = buf.reshape(2, 32, 136, 8).astype(np.int64)
 ntot = 34
 t0 = tr[tr > 0].min()
+COL = ["w+uhat", "ring", "pass0", "pass1", "pass2+Z", "gbar"]
+ROW = ["rowbar", "cC wait", "tile", "rowbar", "pass01", "pass2+acc", "pairbar"]
 for sel in range(2):
-    print(f"=== CTA {0 if sel == 0 else 100} (times in us from first mark)")
-    for w in range(16):
+    print(f"=== CTA {0 if sel == 0 else 100} (us; mean per term over terms 2..{ntot - 1})")
+    for w in range(24):
         d = tr[sel, w, :ntot]
         if d.max() == 0:
             continue
+        names = COL if w < 8 else ROW
+        nm = len(names) + 1
+        d = d[:, :nm].astype(np.float64)
+        ok = (d > 0).all(axis=1)
         d = (d - t0) / 1000.0
-        role = "col" if w < 8 else "row"
-        waits = d[:, 1] - d[:, 0]
-        work1 = d[:, 2] - d[:, 1]
-        work2 = d[:, 3] - d[:, 2]
-        print(f"w{w:2d} {role} start {d[0,0]:8.1f} end {d[ntot-1,3]:8.1f} | wait mean {waits.mean():6.2f} max {waits.max():6.2f}"
-              f" | phaseA mean {work1.mean():6.2f} | phaseB mean {work2.mean():6.2f}")
-    w = 0 if sel == 0 else 0
-    d = (tr[sel, 0, :8] - t0) / 1000.0
-    print("col w0 first terms:", np.round(d, 1).tolist())
-    d = (tr[sel, 8, :8] - t0) / 1000.0
-    print("row w8 first terms:", np.round(d, 1).tolist())
+        rng = [i for i in range(2, ntot) if ok[i]]
+        if not rng:
+            print(f"w{w:2d} (inactive)")
+            continue
+        dd = d[rng]
+        per = np.diff(dd, axis=1).mean(axis=0)
+        nxt = [d[i + 1, 0] - d[i, 0] for i in rng if i + 1 < ntot and ok[i + 1]]
+        print(f"w{w:2d} {'col' if w < 8 else 'row'} term {np.mean(nxt) if nxt else float('nan'):5.2f} | "
+              + " ".join(f"{n} {x:5.2f}" for n, x in zip(names, per))
+              + f" | start {d[0, 0]:6.1f} end {d[ntot - 1, nm - 1]:6.1f}")
