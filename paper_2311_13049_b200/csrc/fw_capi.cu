@@ -201,6 +201,7 @@ struct fw_ctx_s {
   double* residue = nullptr;  // device scalar
   int nsm = 148;
   bool force_generic = false;                 // FW_FORCE_GENERIC=1: multi-pass kernels only
+  int dbg = 0;                                // FW_STEP2D_DBG: timing experiments only (wrong results)
   unsigned long long* counters = nullptr;     // persistent-kernel counters (2 sets)
   unsigned long long* trace = nullptr;        // FW_TRACE=1: persistent-kernel phase timestamps
   int cset = 0;
@@ -270,6 +271,8 @@ int fw_ctx_create(int device, fw_ctx* out) {
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
   const char* fg = getenv("FW_FORCE_GENERIC");
   c->force_generic = fg && fg[0] == '1';
+  const char* dg = getenv("FW_STEP2D_DBG");
+  c->dbg = dg ? atoi(dg) : 0;
   if (dalloc(&c->counters, 2 * (size_t)fw::kStep2dCStride)) {
     fw_ctx_destroy(c);
     return FW_E_OOM;
@@ -427,6 +430,7 @@ int launch_persistent(fw_ctx ctx, fw_op const* ops, int nops, int m_first, const
   p.wcols = fw::step2d_wcols(g.J[1]);
   p.counters = ctx->counters;
   p.trace = ctx->trace;
+  p.dbg = ctx->dbg;
   p.cset = ctx->cset;
   p.cstride = fw::kStep2dCStride;
   ctx->cset ^= 1;

@@ -235,8 +235,8 @@ struct Geo {
   static constexpr size_t OFF_TWP = TWC + TWR;
   static constexpr size_t OFF_CW = TWC + TWR + TWP;                // column work [2 groups][2 members][LCOL]
   static constexpr size_t OFF_RW = OFF_CW + (size_t)4 * LCOL;      // row work [RMAX][LROW]
-  static constexpr size_t OFF_DEV = OFF_RW + (size_t)RMAX * LROW;  // row (s-s0)^m landing [RMAX][J1 doubles]
-  static constexpr size_t NELEM = OFF_DEV + (size_t)RMAX * (J1 / 2);
+  static constexpr size_t OFF_TILE = OFF_RW + (size_t)RMAX * LROW;  // next term's rows of Z [RMAX][LROW]
+  static constexpr size_t NELEM = OFF_TILE + (size_t)RMAX * LROW;
   static constexpr size_t SMEM = NELEM * sizeof(double2);
   // tensor memory: [0,128) row accumulators (16 warps x 32 columns), [128, 128 + 8 CR0) uhat
   static constexpr int TM_U = 128;
@@ -286,6 +286,16 @@ __device__ __forceinline__ void tmem_ld4(unsigned taddr, unsigned* v) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld8_nw(unsigned taddr, unsigned* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8_nw(unsigned taddr, const unsigned* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -377,7 +387,6 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
   constexpr int H = G::H, h = G::h, NT = G::NT;
   constexpr int CR0 = G::CR0, CT0 = G::CT0;
   extern __shared__ __align__(16) double2 sm[];
-  __shared__ __align__(8) unsigned long long dbar[RMAX];  // row dev-landing mbarriers
   __shared__ unsigned tmem_base_sh;
   double2* twc = sm;
   double2* twr = sm + G::OFF_TWR;
@@ -387,6 +396,12 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
   const int b = blockIdx.x;
   const int nblk = gridDim.x;
 
+  // launch marks (tracing only): warp slot 31 of the trace, [step % 64][entry, exit]
+  auto launch_mark = [&](int which) {
+    if (prm.trace && tid == 0 && (b == 0 || b == 100))
+      prm.trace[((size_t)(b == 0 ? 0 : 1) * 32 + 31) * 136 * 8 + (size_t)(prm.step & 63) * 2 + which] = gtimer();
+  };
+  launch_mark(0);
   unsigned long long* cnt = prm.counters + (size_t)prm.cset * prm.cstride;
   if (b == 0) {
     unsigned long long* other = prm.counters + (size_t)(prm.cset ^ 1) * prm.cstride;
@@ -411,7 +426,6 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
     fill(twr, twoff(h, 2), pprod(h, 2), radix(h, 2));
     for (int e = tid; e <= h; e += NT) twp[e] = prm.master[e * (kTwMaster / J1)];
   }
-  if (tid < RMAX) mbar_init(&dbar[tid], 1);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (unsigned)__cvta_generic_to_shared(&tmem_base_sh)),
@@ -419,7 +433,6 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -514,7 +527,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
         for (int c = 0; c < 4 * CR0; c += 32) {
           double wk[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) wk[k] = mycol >= 0 ? __ldg(&w[(c / 4 + k) * CT0]) : 0.0;
+          for (int k = 0; k < 8; ++k) wk[k] = (mycol >= 0 && !(prm.dbg & 2)) ? __ldg(&w[(c / 4 + k) * CT0]) : 0.5;
           unsigned v[32];
           tmem_ld32_nw(tu + c, v);
           tmem_wait_ld();
@@ -527,6 +540,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
         double2* Z = prm.T + (size_t)(t % KRING) * J0 * h;
         // the previous term's Z columns are published once this term's pass 0 is done:
         // by then its stores have drained and the release fence is cheap
+        if (prm.dbg & 8) Z = prm.T + (size_t)(KRING - 1) * J0 * h;  // all terms into one slot
         column_pair<G, +1>(work, twc, cg, a, gb, [&] {
           if (cg == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz);
         }, [&](int i, const double2* xa, const double2* xb) {
@@ -567,23 +581,36 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
     // this warp's 32 TMEM columns in its lane quadrant: (s-s0)^m-weighted sums of outputs l + 64 r
     const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 32u * (unsigned)(rw >> 2);
     double2* work = sm + G::OFF_RW + (size_t)(active ? pair : 0) * G::LROW;
-    const double2* dl = sm + G::OFF_DEV + (size_t)(active ? pair : 0) * (J1 / 2);  // (s-s0)^m row landing
-    unsigned long long* bar = &dbar[active ? pair : 0];
-    unsigned dphase = 0;
-    // bulk-load the (s-s0)^m row of term t into the landing buffer (pair's first lane)
-    auto issue_dev = [&](int t) {
-      if (t >= ntot) return;
+    const double2* tile = sm + G::OFF_TILE + (size_t)(active ? pair : 0) * G::LROW;
+    // (s-s0)^m row of term t: global (streamed once), L2-prefetched one term ahead
+    auto dev_row = [&](int t) -> const double2* {
       const int op1 = t / nterms, m1 = prm.m_first + t % nterms;
-      if (m1 < 1) return;
-      if (l == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, J1 * sizeof(double));
-        bulk_g2s((void*)dl, prm.dev[op1] + (size_t)(m1 - 1) * J0 * J1 + (size_t)row * J1, J1 * sizeof(double), bar);
+      return m1 < 1 ? nullptr
+                    : reinterpret_cast<const double2*>(prm.dev[op1] + (size_t)(m1 - 1) * J0 * J1 + (size_t)row * J1);
+    };
+    // the CTA's rows of Z[t] (column-major [k][k0]) -> tile buffers (natural order, padded):
+    // 8 row slots x 4 k per warp instruction, each k a contiguous run of nr elements.
+    // cp.async: no registers, the copies land while the warps run passes 1 and 2.
+    const int f = tid - 256, rs = f & 7, kq = f >> 3;
+    const unsigned tdst = smem_u32(sm + G::OFF_TILE + (size_t)rs * G::LROW);
+    auto issue_tile = [&](int t) {
+      warp_wait(&cC[t], (unsigned long long)h);
+      if (rs < nr && !(prm.dbg & 4)) {
+        const double2* Zt = prm.T + (size_t)(t % KRING) * J0 * h + r0 + rs;
+#pragma unroll
+        for (int it = 0; it < h / 64; ++it)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tdst + 16u * G::rpad(it * 64 + kq)),
+                       "l"(Zt + (size_t)(it * 64 + kq) * J0)
+                       : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (active && l == 0) {
+        const double2* d = dev_row(t);
+        if (d) prefetch_l2(d, J1 * sizeof(double));
       }
     };
 
     if (active) {
-      issue_dev(0);
       // ---- F1: R2C of the row -> Y
       const double2* u2 = reinterpret_cast<const double2*>(prm.u) + (size_t)row * h;
 #pragma unroll
@@ -618,78 +645,79 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
       for (int e = 0; e < 32; ++e) z[e] = 0u;
       tmem_st32(tacc, z);
     }
+    if (ntot > 0) issue_tile(0);
 
     // ---- R(t): h-point C2C of the pre-processed row + recombination
-    const int f = tid - 256, rs = f & 7, kq = f >> 3;
-    double2* wr = sm + G::OFF_RW + (size_t)rs * G::LROW;
     for (int t = 0; t < ntot; ++t) {
       const int op = t / nterms;
       const int m = prm.m_first + t % nterms;
       FW_TRACE(t, 0);
-      rowsbar();  // every row warp is done with its work buffer (F1 or term t - 1)
+      asm volatile("cp.async.wait_all;" ::: "memory");
       FW_TRACE(t, 1);
-      warp_wait(&cC[t], (unsigned long long)h);
-      FW_TRACE(t, 2);
-      {  // the CTA's rows of Z[t] (column-major [k][k0]): 8 row slots x 4 k per warp load,
-         // each k a contiguous run of nr elements -> row work buffers, natural order
-        const double2* Zt = prm.T + (size_t)(t % KRING) * J0 * h + r0 + rs;
-        if (rs < nr) {
-          double2 v[h / 64];
-#pragma unroll
-          for (int it = 0; it < h / 64; ++it) v[it] = __ldcg(&Zt[(size_t)(it * 64 + kq) * J0]);
-#pragma unroll
-          for (int it = 0; it < h / 64; ++it) wr[G::rpad(it * 64 + kq)] = v[it];
-        }
-      }
-      FW_TRACE(t, 3);
-      rowsbar();  // the tile is complete
+      rowsbar();  // the tile of Z[t] is complete
       // the CTA's rows of Z[t] are consumed (their values are in shared memory):
       // the ring slot may be reused.  No release fence needed.
       if (tid == 256) red_relaxed_add(&cR[t], (unsigned long long)nr);
+      FW_TRACE(t, 2);
+      if (active) {  // pass 0 (p = 1): tile -> work, same (natural) positions
+        double2 a[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a[r] = tile[G::rpad(l + r * G::RT)];
+        Dft<8, +1>::run(a);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = a[r];
+      }
+      FW_TRACE(t, 3);
+      rowsbar();  // tile buffers free: the next tile may land
+      if (t + 1 < ntot) issue_tile(t + 1);
       FW_TRACE(t, 4);
       if (!active) continue;
-      row_passes01<G, +1>(work, twr, l, pair);
-      FW_TRACE(t, 5);
-      const bool hasdev = m >= 1;
-      if (hasdev) {
-        mbar_wait(bar, dphase);
-        dphase ^= 1u;
+      pairbar(pair);
+      {
+        double2 a[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a[r] = work[G::r_p1in(l + r * G::RT)];
+        butterfly<h, 1, +1>(a, l, twr);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) work[G::r_p1in(l + r * G::RT)] = a[r];
       }
+      pairbar(pair);
+      FW_TRACE(t, 5);
+      const double2* dv = (prm.dbg & 1) ? nullptr : dev_row(t);
       {
         double2 a[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l + r * G::RT)];
         butterfly<h, 2, +1>(a, l, twr);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          double v0 = a[r].x, v1 = a[r].y;
-          if (hasdev) {
-            const double2 d = dl[l + r * G::RT];
-            v0 = d.x * v0;
-            v1 = d.y * v1;
-          }
-          double p0 = 0.0, p1 = 0.0;  // the reference's per-term partial: 0 + dev * x
-          p0 += v0;
-          p1 += v1;
-          a[r] = make_double2(p0, p1);
-        }
+        for (int qt = 0; qt < 4; ++qt) {
+          double2 d[2];
+          if (dv) {
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          unsigned v[16];
-          tmem_ld16_nw(tacc + 16u * hf, v);
+            for (int r = 0; r < 2; ++r) d[r] = __ldcg(&dv[l + (2 * qt + r) * G::RT]);
+          }
+          unsigned v[8];
+          tmem_ld8_nw(tacc + 8u * qt, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            tm_put(v, 2 * r, tm_d(v, 2 * r) + a[4 * hf + r].x);
-            tm_put(v, 2 * r + 1, tm_d(v, 2 * r + 1) + a[4 * hf + r].y);
+          for (int r = 0; r < 2; ++r) {
+            double v0 = a[2 * qt + r].x, v1 = a[2 * qt + r].y;
+            if (dv) {
+              v0 = d[r].x * v0;
+              v1 = d[r].y * v1;
+            }
+            double p0 = 0.0, p1 = 0.0;  // the reference's per-term partial: 0 + dev * x
+            p0 += v0;
+            p1 += v1;
+            tm_put(v, 2 * r, tm_d(v, 2 * r) + p0);
+            tm_put(v, 2 * r + 1, tm_d(v, 2 * r + 1) + p1);
           }
-          tmem_st16_nw(tacc + 16u * hf, v);
+          tmem_st8_nw(tacc + 8u * qt, v);
         }
         tmem_wait_st();
       }
       FW_TRACE(t, 6);
-      pairbar(pair);  // both warps are done with the landing buffer
-      issue_dev(t + 1);
+      pairbar(pair);  // pass-2 reads of the work buffer are done
       FW_TRACE(t, 7);
       if (m == M && !(prm.seismic && op == prm.nops - 1)) {  // operator complete: hand over
         double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)row * J1);
@@ -732,7 +760,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
         l2o[q] = make_double2(l2x, l2y);
         bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
       }
-      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(prm.flag, prm.step);
+      if (__any_sync(0xffffffffu, bad) && lane == 0 && !prm.dbg) atomicMin(prm.flag, prm.step);
     }
   }
   // everyone is done with tensor memory: release it
@@ -741,6 +769,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(G::TM_COLS) : "memory");
+  launch_mark(1);
 }
 
 template <int J0, int J1, int RMAX>

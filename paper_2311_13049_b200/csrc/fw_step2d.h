@@ -31,6 +31,7 @@ struct Step2DParams {
   double tau, thr;
   int step;
   int* flag;
+  int dbg;  // timing experiments (FW_STEP2D_DBG), 0 in production
 };
 
 bool step2d_supported(int J0, int J1, int nsm);

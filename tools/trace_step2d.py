@@ -21,14 +21,14 @@ cfg = configs.c2()
 ctx = fw.Context(0)
 g = fw.Grid(list(zip(cfg.lo, cfg.hi)), cfg.J)
 st = fw.SeismicStepper(fw.build_medium(g, cfg.gamma, cfg.c0, 1.0, cfg.M), cfg.phi, cfg.psi, cfg.tau, ctx=ctx)
-st.advance(3)
+st.advance(6)
 lib = fw.load_library()
 lib.fw_ctx_trace.argtypes = [C.c_void_p, C.c_void_p]
 buf = np.zeros(2 * 32 * 136 * 8, dtype=np.uint64)
 fw._capi.check(lib.fw_ctx_trace(ctx.handle, buf.ctypes.data))
 tr = buf.reshape(2, 32, 136, 8).astype(np.int64)
 ntot = 34
-t0 = tr[tr > 0].min()
+t0 = tr[:, :24][tr[:, :24] > 0].min()
 COL = ["w+uhat", "ring", "pass0", "pass1", "pass2+Z", "gbar"]
 ROW = ["rowbar", "cC wait", "tile", "rowbar", "pass01", "pass2+acc", "pairbar"]
 for sel in range(2):
@@ -52,3 +52,16 @@ for sel in range(2):
         print(f"w{w:2d} {'col' if w < 8 else 'row'} term {np.mean(nxt) if nxt else float('nan'):5.2f} | "
               + " ".join(f"{n} {x:5.2f}" for n, x in zip(names, per))
               + f" | start {d[0, 0]:6.1f} end {d[ntot - 1, nm - 1]:6.1f}")
+
+# launch marks: warp slot 31, [step % 64][entry, exit] (CTA 0)
+lm = buf.reshape(2, 32, 136 * 8)[0, 31, :128].reshape(64, 2).astype(np.int64)
+ok = np.nonzero(lm[:, 0] > 0)[0]
+if len(ok):
+    print("launch marks (CTA 0, us): step: entry -> exit (duration), gap from previous exit")
+    prev = None
+    for k in sorted(ok, key=lambda i: lm[i, 0]):
+        e0, e1 = lm[k]
+        gap = (e0 - prev) / 1000.0 if prev is not None else float("nan")
+        print(f"  slot {k:2d}: {(e1 - e0) / 1000.0:8.1f} us, gap {gap:6.1f} us; first term mark at "
+              f"{(tr[0, :24][tr[0, :24] > 0].min() - e0) / 1000.0 if k == ok[-1] else float('nan'):6.1f}")
+        prev = e1
