@@ -27,7 +27,9 @@
 // plan, twiddle values, fma placement, pre-processing formula): results are
 // bit-identical to the multi-pass path and to the CPU oracle.  Per-pass twiddle
 // tables live in shared memory in a [k][r-1] layout (odd stride, conflict-free).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 
 #include "fw_fft.cuh"
@@ -190,6 +192,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(b))
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(b))
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n FW_MBW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra FW_MBW_%=;\n}" ::"r"(
@@ -235,8 +248,10 @@ struct Geo {
   static constexpr size_t OFF_TWP = TWC + TWR;
   static constexpr size_t OFF_CW = TWC + TWR + TWP;                // column work [2 groups][2 members][LCOL]
   static constexpr size_t OFF_RW = OFF_CW + (size_t)4 * LCOL;      // row work [RMAX][LROW]
-  static constexpr size_t OFF_TILE = OFF_RW + (size_t)RMAX * LROW;  // next term's rows of Z [RMAX][LROW]
-  static constexpr size_t NELEM = OFF_TILE + (size_t)RMAX * LROW;
+  // next term's 8 rows of Z: two TMA boxes [256 k][8 rows] (128-B swizzled), 1 KB aligned at run time
+  static constexpr size_t OFF_TILE = OFF_RW + (size_t)RMAX * LROW;
+  static constexpr size_t TILE_ELEMS = (size_t)h * 8;
+  static constexpr size_t NELEM = OFF_TILE + 64 + TILE_ELEMS;
   static constexpr size_t SMEM = NELEM * sizeof(double2);
   // tensor memory: [0,128) row accumulators (16 warps x 32 columns), [128, 128 + 8 CR0) uhat
   static constexpr int TM_U = 128;
@@ -246,7 +261,8 @@ struct Geo {
   static_assert(npass(J0) == 3 && npass(h) == 3, "3-pass plans");
   static_assert(RR0 == 8 && RR1 == 8 && RR2 == 8 && RT == 64, "row pair: one radix-8 butterfly per lane");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
-  static_assert(RMAX <= 8, "at most 8 row pairs");
+  static_assert(RMAX < 8, "one row pair is the tile producer");
+  static_assert(h % 256 == 0, "whole TMA boxes");
 
   // column layouts: pass-1 input (i, r) = logical i + CT1 r lives at i CR1 + r
   __device__ static __forceinline__ int cpad(int pos) { return pos + (pos >> CL1) + (pos >> CLT); }
@@ -305,7 +321,6 @@ __device__ __forceinline__ void tm_put(unsigned* v, int k, double x) {
   v[2 * k + 1] = (unsigned)__double2hiint(x);
 }
 __device__ __forceinline__ void pairbar(int p) { asm volatile("bar.sync %0, 64;" ::"r"(4 + p) : "memory"); }
-__device__ __forceinline__ void rowsbar() { asm volatile("bar.sync 3, 512;" ::: "memory"); }
 
 // ---------------------------------------------------------------- column group: 2 x J0-point C2C
 // 128 threads (cg), both members of a mirror pair.  Pass 0 takes each thread's CR0
@@ -327,15 +342,20 @@ __device__ __forceinline__ void column_pair(double2* work, const double2* tw, in
   mark(3);
   after_pass0();
 #pragma unroll 1
-  for (int bi = cg; bi < 2 * G::CT1; bi += 128) {
-    const int mbr = bi / G::CT1, i = bi % G::CT1;
-    double2* wb = work + mbr * G::LCOL;
-    double2 c[G::CR1];
+  for (int i = cg; i < G::CT1; i += 128) {  // butterfly i of both members (same twiddles)
+    double2 c0[G::CR1], c1[G::CR1];
 #pragma unroll
-    for (int r = 0; r < G::CR1; ++r) c[r] = wb[G::c_p1(i, r)];
-    butterfly<J0, 1, DIR>(c, i, tw);
+    for (int r = 0; r < G::CR1; ++r) {
+      c0[r] = work[G::c_p1(i, r)];
+      c1[r] = work[G::LCOL + G::c_p1(i, r)];
+    }
+    butterfly<J0, 1, DIR>(c0, i, tw);
+    butterfly<J0, 1, DIR>(c1, i, tw);
 #pragma unroll
-    for (int r = 0; r < G::CR1; ++r) wb[G::c_p1(i, r)] = c[r];
+    for (int r = 0; r < G::CR1; ++r) {
+      work[G::c_p1(i, r)] = c0[r];
+      work[G::LCOL + G::c_p1(i, r)] = c1[r];
+    }
   }
   gbar();
   mark(4);
@@ -382,12 +402,13 @@ __device__ __forceinline__ void row_passes01(double2* work, const double2* tw, i
 
 // --------------------------------------------------------------------------
 template <int J0, int J1, int RMAX>
-__global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
+__global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const __grid_constant__ CUtensorMap zmap) {
   using G = Geo<J0, J1, RMAX>;
   constexpr int H = G::H, h = G::h, NT = G::NT;
   constexpr int CR0 = G::CR0, CT0 = G::CT0;
   extern __shared__ __align__(16) double2 sm[];
   __shared__ unsigned tmem_base_sh;
+  __shared__ __align__(8) unsigned long long tile_full, tile_empty;  // row tile pipeline (TMA producer)
   double2* twc = sm;
   double2* twr = sm + G::OFF_TWR;
   double2* twp = sm + G::OFF_TWP;
@@ -425,6 +446,12 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
     fill(twr, twoff(h, 1), pprod(h, 1), radix(h, 1));
     fill(twr, twoff(h, 2), pprod(h, 2), radix(h, 2));
     for (int e = tid; e <= h; e += NT) twp[e] = prm.master[e * (kTwMaster / J1)];
+  }
+  if (tid == 0) {
+    const int nr0 = (int)(((long long)(b + 1) * J0) / nblk) - (int)(((long long)b * J0) / nblk);
+    mbar_init(&tile_full, 1);
+    mbar_init(&tile_empty, 2 * nr0);  // one arrive per consumer warp
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -581,34 +608,50 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
     // this warp's 32 TMEM columns in its lane quadrant: (s-s0)^m-weighted sums of outputs l + 64 r
     const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 32u * (unsigned)(rw >> 2);
     double2* work = sm + G::OFF_RW + (size_t)(active ? pair : 0) * G::LROW;
-    const double2* tile = sm + G::OFF_TILE + (size_t)(active ? pair : 0) * G::LROW;
+    // the tile: rows r0..r0+7 of Z[t] as two [256 k][8 rows] TMA boxes, 128-B swizzled
+    double2* tile;
+    {
+      const unsigned base = smem_u32(sm + G::OFF_TILE);
+      tile = sm + G::OFF_TILE + (((base + 1023u) & ~1023u) - base) / 16u;
+    }
+    auto tile_at = [&](int k, int rs) -> const double2& {
+      return tile[(size_t)k * 8 + (unsigned)(rs ^ (k & 7))];
+    };
     // (s-s0)^m row of term t: global (streamed once), L2-prefetched one term ahead
     auto dev_row = [&](int t) -> const double2* {
       const int op1 = t / nterms, m1 = prm.m_first + t % nterms;
       return m1 < 1 ? nullptr
                     : reinterpret_cast<const double2*>(prm.dev[op1] + (size_t)(m1 - 1) * J0 * J1 + (size_t)row * J1);
     };
-    // the CTA's rows of Z[t] (column-major [k][k0]) -> tile buffers (natural order, padded):
-    // 8 row slots x 4 k per warp instruction, each k a contiguous run of nr elements.
-    // cp.async: no registers, the copies land while the warps run passes 1 and 2.
-    const int f = tid - 256, rs = f & 7, kq = f >> 3;
-    const unsigned tdst = smem_u32(sm + G::OFF_TILE + (size_t)rs * G::LROW);
-    auto issue_tile = [&](int t) {
-      warp_wait(&cC[t], (unsigned long long)h);
-      if (rs < nr && !(prm.dbg & 4)) {
-        const double2* Zt = prm.T + (size_t)(t % KRING) * J0 * h + r0 + rs;
-#pragma unroll
-        for (int it = 0; it < h / 64; ++it)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tdst + 16u * G::rpad(it * 64 + kq)),
-                       "l"(Zt + (size_t)(it * 64 + kq) * J0)
-                       : "memory");
+
+    if (rw == 2 * RMAX) {
+      // ---- tile producer (one lane of an otherwise idle warp): Z[t] -> tile by TMA as soon as
+      // the columns of term t are published and the consumers are done with tile t-1
+      if (lane == 0) {
+        for (int t = 0; t < ntot; ++t) {
+          if (t > 0) {
+            mbar_wait(&tile_empty, (unsigned)(t - 1) & 1u);
+            // the CTA's rows of Z[t-1] are consumed (in shared memory / registers): the ring
+            // slot may be reused.  No release fence needed.
+            red_relaxed_add(&cR[t - 1], (unsigned long long)nr);
+          }
+          while (ld_acquire(&cC[t]) < (unsigned long long)h) {
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy Z stores -> TMA reads
+          if (!(prm.dbg & 4)) {
+            mbar_expect_tx(&tile_full, (unsigned)(G::TILE_ELEMS * sizeof(double2)));
+            for (int bx = 0; bx < h / 256; ++bx)
+              tma_load_3d(tile + (size_t)bx * 256 * 8, &zmap, 2 * r0, bx * 256, t % KRING, &tile_full);
+          } else {
+            mbar_arrive(&tile_full);
+          }
+        }
+        if (ntot > 0) {
+          mbar_wait(&tile_empty, (unsigned)(ntot - 1) & 1u);
+          red_relaxed_add(&cR[ntot - 1], (unsigned long long)nr);
+        }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (active && l == 0) {
-        const double2* d = dev_row(t);
-        if (d) prefetch_l2(d, J1 * sizeof(double));
-      }
-    };
+    }
 
     if (active) {
       // ---- F1: R2C of the row -> Y
@@ -645,33 +688,29 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm) {
       for (int e = 0; e < 32; ++e) z[e] = 0u;
       tmem_st32(tacc, z);
     }
-    if (ntot > 0) issue_tile(0);
 
     // ---- R(t): h-point C2C of the pre-processed row + recombination
-    for (int t = 0; t < ntot; ++t) {
+    for (int t = 0; active && t < ntot; ++t) {
       const int op = t / nterms;
       const int m = prm.m_first + t % nterms;
       FW_TRACE(t, 0);
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      FW_TRACE(t, 1);
-      rowsbar();  // the tile of Z[t] is complete
-      // the CTA's rows of Z[t] are consumed (their values are in shared memory):
-      // the ring slot may be reused.  No release fence needed.
-      if (tid == 256) red_relaxed_add(&cR[t], (unsigned long long)nr);
+      if (l == 0 && t + 1 < ntot) {  // the next term's (s-s0)^m row -> L2
+        const double2* d = dev_row(t + 1);
+        if (d) prefetch_l2(d, J1 * sizeof(double));
+      }
+      mbar_wait(&tile_full, (unsigned)t & 1u);
       FW_TRACE(t, 2);
-      if (active) {  // pass 0 (p = 1): tile -> work, same (natural) positions
+      {  // pass 0 (p = 1): tile -> work (natural positions)
         double2 a[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r] = tile[G::rpad(l + r * G::RT)];
+        for (int r = 0; r < 8; ++r) a[r] = tile_at(l + r * G::RT, pair);
         Dft<8, +1>::run(a);
 #pragma unroll
         for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = a[r];
       }
-      FW_TRACE(t, 3);
-      rowsbar();  // tile buffers free: the next tile may land
-      if (t + 1 < ntot) issue_tile(t + 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty);  // this warp is done with tile t
       FW_TRACE(t, 4);
-      if (!active) continue;
       pairbar(pair);
       {
         double2 a[8];
@@ -781,7 +820,25 @@ cudaError_t launch_t(const Step2DParams& p, cudaStream_t st, int nblk) {
     cudaFuncSetAttribute(k_step2d<J0, J1, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     attr = true;
   }
-  void* args[] = {(void*)&p};
+  // the term ring as a 3D tensor of doubles [KRING][h][2 J0]; box = 8 rows (128 B) x 256 k
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode)
+      return cudaErrorNotSupported;
+  }
+  constexpr int h = J1 / 2;
+  CUtensorMap zmap;
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * J0, (cuuint64_t)h, (cuuint64_t)KRING};
+  const cuuint64_t strides[2] = {(cuuint64_t)2 * J0 * sizeof(double), (cuuint64_t)2 * J0 * h * sizeof(double)};
+  const cuuint32_t box[3] = {16, 256, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (encode(&zmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)p.T, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  void* args[] = {(void*)&p, (void*)&zmap};
   return cudaLaunchCooperativeKernel((void*)k_step2d<J0, J1, RMAX>, dim3(nblk), dim3(G::NT), args, G::SMEM, st);
 }
 
