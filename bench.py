@@ -282,9 +282,9 @@ def run_c5(args):
     per_m = {}
     for M in configs.C5_M:
         ops = [fw.build_expansion(fw.OrderField(g, f.s), M, ctx=ctx) for f in fields]
+        uptr, optr = [u.data_ptr() for u in us], [o.data_ptr() for o in outs]
         for _ in range(max(1, args.warmup)):
-            for op, u, o in zip(ops, us, outs):
-                op.apply_device(u.data_ptr(), o.data_ptr())
+            fw.apply_batch_device(ops, uptr, optr)
         ctx.sync()
         if world > 1:
             torch.distributed.barrier()
@@ -292,8 +292,7 @@ def run_c5(args):
         reps = max(1, args.steps // 20)
         e0.record(stream)
         for _ in range(reps):
-            for op, u, o in zip(ops, us, outs):
-                op.apply_device(u.data_ptr(), o.data_ptr())
+            fw.apply_batch_device(ops, uptr, optr)
         e1.record(stream)
         e1.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device="cuda")

@@ -40,6 +40,8 @@ from .api import (  # noqa: F401
     SeismicMedium,
     SeismicStepper,
     TSFP2Stepper,
+    apply_batch,
+    apply_batch_device,
     apply_matrix_free,
     apply_matrix_free_serial,
     apply_perturbation,

@@ -234,6 +234,31 @@ def apply_perturbation(op: ExpansionOperator, u, residue: bool = False):
     return op.apply(_check_field(op, u), 1, residue)
 
 
+
+def apply_batch_device(ops, u_ptrs, out_ptrs):
+    """``apply_matrix_free`` of many independent fields at once (configs[4]: 64 fields
+    of one grid, each with its own order field).  Device pointers; enqueued on the
+    operators' (common) context stream.  Fields sharing grid and M run as ONE batched
+    pipeline (one launch per stage for all fields, fw_apply_batch_device)."""
+    n = len(ops)
+    if len(u_ptrs) != n or len(out_ptrs) != n:
+        raise ValueError("ops, u_ptrs and out_ptrs must have the same length")
+    H = C.c_void_p * max(n, 1)
+    check(load_library().fw_apply_batch_device(H(*[o._h for o in ops]), n, H(*[C.c_void_p(p) for p in u_ptrs]),
+                                               H(*[C.c_void_p(p) for p in out_ptrs])))
+
+
+def apply_batch(ops, fields):
+    """Host-buffer variant of :func:`apply_batch_device`: returns the list of results."""
+    import torch
+
+    us = [torch.from_numpy(np.ascontiguousarray(f, dtype=np.float64)).cuda() for f in fields]
+    outs = [torch.empty_like(u) for u in us]
+    apply_batch_device(ops, [u.data_ptr() for u in us], [o.data_ptr() for o in outs])
+    if ops:
+        ops[0].ctx.sync()
+    return [o.cpu().numpy() for o in outs]
+
 class SeismicMedium:
     """Inputs of derive_medium (seismic.cpp:11-44); the coefficient fields and the
     two operators are built on the device by SeismicStepper."""

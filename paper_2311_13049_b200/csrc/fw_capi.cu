@@ -196,8 +196,8 @@ struct fw_ctx_s {
   double2* master = nullptr;
   long long launches = 0;
   // grow-only scratch slots (single stream: ops on one ctx run in order)
-  void* scratch[8] = {};
-  size_t scratch_bytes[8] = {};
+  void* scratch[12] = {};
+  size_t scratch_bytes[12] = {};
   double* residue = nullptr;  // device scalar
   int nsm = 148;
   bool force_generic = false;                 // FW_FORCE_GENERIC=1: multi-pass kernels only
@@ -223,7 +223,10 @@ struct fw_ctx_s {
   }
 };
 
-enum { SLOT_UH = 0, SLOT_T = 1, SLOT_U = 2, SLOT_OUT = 3, SLOT_TMP = 4, SLOT_UH2 = 5, SLOT_Y2D = 6, SLOT_T2D = 7 };
+enum {
+  SLOT_UH = 0, SLOT_T = 1, SLOT_U = 2, SLOT_OUT = 3, SLOT_TMP = 4, SLOT_UH2 = 5, SLOT_Y2D = 6, SLOT_T2D = 7,
+  SLOT_BUH = 8, SLOT_BT = 9, SLOT_BTAB = 10  // batched multi-field pipeline
+};
 
 struct fw_op_s {
   fw_ctx ctx = nullptr;
@@ -598,9 +601,51 @@ int fw_apply_device(fw_op op, const double* u_dev, double* out_dev, int m_first,
 
 int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_dev, double* const* out_dev) {
   if (!ops || !u_dev || !out_dev || nfields < 0) return set_err(FW_E_ARG, "null argument");
-  for (int f = 0; f < nfields; ++f) {
+  for (int f = 0; f < nfields; ++f)
     if (!ops[f]) return set_err(FW_E_ARG, "null op in batch");
-    FW_TRY(apply_device(ops[f], u_dev[f], out_dev[f], 0, nullptr, nullptr));
+  if (nfields == 0) return FW_OK;
+  // one batched pipeline (grid.z = field) when every field shares grid, context and term range and
+  // the grid is not served by the persistent single-launch kernel; else one apply per field
+  const fw_op o0 = ops[0];
+  bool batch = nfields > 1 && o0->g.d >= 2 && !use_persistent(o0);
+  for (int f = 1; f < nfields && batch; ++f) {
+    const fw_op o = ops[f];
+    batch = o->ctx == o0->ctx && o->g.d == o0->g.d && o->g.N == o0->g.N && o->M == o0->M &&
+            o->constant_order == o0->constant_order && !use_persistent(o);
+    for (int a = 0; a < o0->g.d && batch; ++a) batch = o->g.J[a] == o0->g.J[a];
+  }
+  if (!batch) {
+    for (int f = 0; f < nfields; ++f) FW_TRY(apply_device(ops[f], u_dev[f], out_dev[f], 0, nullptr, nullptr));
+    FW_CUDA(cudaGetLastError());
+    return FW_OK;
+  }
+  fw_ctx ctx = o0->ctx;
+  const fw::GridGeom& g = o0->g;
+  const int m_last = o0->constant_order ? 0 : o0->M;
+  const size_t per_field = (size_t)(m_last + 1) * g.Nh * sizeof(double2);
+  const int Fc = (int)std::max<size_t>(1, std::min<size_t>((size_t)nfields, ((size_t)2 << 30) / per_field));
+  void *uh = nullptr, *T = nullptr, *tab = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_BUH, (size_t)Fc * g.Nh * sizeof(double2), &uh));
+  FW_TRY(ctx->get_scratch(SLOT_BT, (size_t)Fc * per_field, &T));
+  FW_TRY(ctx->get_scratch(SLOT_BTAB, (size_t)5 * Fc * sizeof(fw::BatchLine), &tab));
+  fw::BatchLine* dt = static_cast<fw::BatchLine*>(tab);
+  for (int f0 = 0; f0 < nfields; f0 += Fc) {
+    const int F = std::min(Fc, nfields - f0);
+    std::vector<fw::BatchLine> h((size_t)5 * Fc);
+    for (int i = 0; i < F; ++i) {
+      const fw_op o = ops[f0 + i];
+      double2* Uh = static_cast<double2*>(uh) + (size_t)i * g.Nh;
+      double2* Ti = reinterpret_cast<double2*>(static_cast<char*>(T) + (size_t)i * per_field);
+      h[0 * Fc + i] = {u_dev[f0 + i], Uh, nullptr, nullptr, nullptr};             // R2C
+      h[1 * Fc + i] = {Uh, Uh, nullptr, nullptr, nullptr};                        // forward C2C
+      h[2 * Fc + i] = {Uh, Ti, o->w, nullptr, nullptr};                           // inverse axis 0 (x w_m)
+      h[3 * Fc + i] = {Ti, Ti, nullptr, nullptr, nullptr};                        // inverse axes 1..d-2
+      h[4 * Fc + i] = {Ti, nullptr, nullptr, o->dev1, out_dev[f0 + i]};          // C2R + recombination
+    }
+    FW_CUDA(cudaMemcpyAsync(dt, h.data(), h.size() * sizeof(fw::BatchLine), cudaMemcpyHostToDevice, ctx->stream));
+    auto L = ctx->L();
+    fw::launch_forward_batch(L, g, F, dt, dt + Fc, true);
+    fw::launch_inverse_batch(L, g, F, 0, m_last, dt + 2 * Fc, dt + 3 * Fc, dt + 4 * Fc);
   }
   FW_CUDA(cudaGetLastError());
   return FW_OK;

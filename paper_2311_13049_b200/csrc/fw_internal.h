@@ -75,6 +75,23 @@ void launch_tsfp2_kick(const LaunchCtx& L, size_t N, double tau, double kappa, i
 void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x);
 void launch_sup_check(const LaunchCtx& L, size_t N, const double* u, double thr, int step, int* flag);
 
+// batched multi-field pipeline (many independent fields of one grid, e.g. configs[4]):
+// per-field pointers of one kernel launch, indexed by blockIdx.z
+struct BatchLine {
+  const void* src;
+  void* dst;
+  const double* w;    // weights (already offset to the launch's first term)
+  const double* aux;  // dev1 for the C2R recombination
+  double* out;
+};
+// forward for F fields: tab[f] = {u_f, Uh_f}; tab is a DEVICE array of F entries
+void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const BatchLine* tab_r2c,
+                          const BatchLine* tab_c2c, bool scale);
+// inverse + recombination for F fields of one grid and term range:
+// tab0[f] = {Uh_f, T_f, w_f + m_first Nh}, tab1[f] = {T_f, T_f} (axes 1..d-2), tab2[f] = {T_f, -, -, dev1_f, out_f}
+void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_first, int m_last,
+                          const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2);
+
 // stage entry points (distributed orchestration on local sub-arrays)
 void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, double2* H, double scale, bool do_scale);
 void launch_stage_c2c(const LaunchCtx& L, const GridGeom& g, int axis, int dir, const double2* src, double2* dst,

@@ -46,7 +46,12 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 // forward, last axis: rows of nl reals -> nl/2+1 bins
 __global__ void __launch_bounds__(kThreads) k_r2c_rows(const double* __restrict__ u, double2* __restrict__ Uh, int nl,
                                                       long long rows, int lpb, double sc, int do_scale,
-                                                      const double2* __restrict__ master) {
+                                                      const double2* __restrict__ master,
+                                                      const BatchLine* __restrict__ bl) {
+  if (bl) {  // batched: this field's pointers
+    u = static_cast<const double*>(bl[blockIdx.z].src);
+    Uh = static_cast<double2*>(bl[blockIdx.z].dst);
+  }
   extern __shared__ double2 sm[];
   const int h = nl / 2;
   const int ls = line_stride(h + 1, lpb);
@@ -80,7 +85,13 @@ __global__ void __launch_bounds__(kThreads) k_c2c_axis(const double2* __restrict
                                                       const double* __restrict__ w, int n, long long S,
                                                       long long inner, long long src_ts, long long dst_ts,
                                                       long long w_ts, int lpb, double sc, int do_scale,
-                                                      const double2* __restrict__ master) {
+                                                      const double2* __restrict__ master,
+                                                      const BatchLine* __restrict__ bl) {
+  if (bl) {  // batched: this field's pointers
+    src = static_cast<const double2*>(bl[blockIdx.z].src);
+    dst = static_cast<double2*>(bl[blockIdx.z].dst);
+    w = bl[blockIdx.z].w;
+  }
   extern __shared__ double2 sm[];
   const int ls = line_stride(n, lpb);
   double2* buf0 = sm;
@@ -127,8 +138,14 @@ __global__ void __launch_bounds__(kThreads) k_c2r_accum(const double2* __restric
                                                        int m_last, const double* __restrict__ dev1,
                                                        double* __restrict__ out, int nl, long long rows, int lpb,
                                                        double* residue, const int* guard,
-                                                       const double2* __restrict__ master) {
+                                                       const double2* __restrict__ master,
+                                                       const BatchLine* __restrict__ bl) {
   if (guard && *guard != kNoBlowup) return;
+  if (bl) {  // batched: this field's pointers
+    src = static_cast<const double2*>(bl[blockIdx.z].src);
+    dev1 = bl[blockIdx.z].aux;
+    out = bl[blockIdx.z].out;
+  }
   extern __shared__ double2 sm[];
   const int h = nl / 2;
   const int ls = line_stride(h + 1, lpb);
@@ -327,11 +344,11 @@ void c2c_axis(const LaunchCtx& L, const GridGeom& g, int a, int dir, const doubl
   if (dir < 0) {
     allow_smem(k_c2c_axis<-1>, sm);
     k_c2c_axis<-1><<<grid, kThreads, sm, L.stream>>>(src, dst, w, n, S, inner, src_ts, dst_ts, w_ts, lpb, sc,
-                                                      scale ? 1 : 0, L.master);
+                                                      scale ? 1 : 0, L.master, nullptr);
   } else {
     allow_smem(k_c2c_axis<+1>, sm);
     k_c2c_axis<+1><<<grid, kThreads, sm, L.stream>>>(src, dst, w, n, S, inner, src_ts, dst_ts, w_ts, lpb, sc,
-                                                      scale ? 1 : 0, L.master);
+                                                      scale ? 1 : 0, L.master, nullptr);
   }
   count(L);
 }
@@ -354,7 +371,7 @@ void launch_forward(const LaunchCtx& L, const GridGeom& g, const double* u, doub
   allow_smem(k_r2c_rows, sm);
   const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
   k_r2c_rows<<<nb, kThreads, sm, L.stream>>>(u, Uh, g.nl, (long long)g.rows, lpb, inv,
-                                             (scale && g.d == 1) ? 1 : 0, L.master);
+                                             (scale && g.d == 1) ? 1 : 0, L.master, nullptr);
   count(L);
   for (int a = g.d - 2; a >= 0; --a)
     c2c_axis(L, g, a, -1, Uh, Uh, nullptr, 0, 0, 0, 1, inv, scale && a == 0);
@@ -369,7 +386,7 @@ static void c2r_accum(const LaunchCtx& L, const GridGeom& g, const double2* src,
   allow_smem(k_c2r_accum, sm);
   const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
   k_c2r_accum<<<nb, kThreads, sm, L.stream>>>(src, src_ts, w, w_ts, m_first, m_last, dev1, out, g.nl,
-                                              (long long)g.rows, lpb, residue, guard, L.master);
+                                              (long long)g.rows, lpb, residue, guard, L.master, nullptr);
   count(L);
 }
 
@@ -454,7 +471,7 @@ void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, do
   const size_t sm = smem_bytes(h + 1, lpb);
   const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
   k_r2c_rows<<<nb, kThreads, sm, L.stream>>>(u, H, g.nl, (long long)g.rows, lpb, scale, do_scale ? 1 : 0,
-                                             L.master);
+                                             L.master, nullptr);
   count(L);
 }
 void launch_stage_c2c(const LaunchCtx& L, const GridGeom& g, int axis, int dir, const double2* src, double2* dst,
@@ -466,4 +483,55 @@ void launch_stage_c2r(const LaunchCtx& L, const GridGeom& g, const double2* src,
                       int m_last, const double* dev1, double* out, double* residue) {
   c2r_accum(L, g, src, src_ts, nullptr, 0, m_first, m_last, dev1, out, residue, nullptr);
 }
+// ---- batched multi-field pipeline (grid.z = field)
+void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const BatchLine* tab_r2c,
+                          const BatchLine* tab_c2c, bool scale) {
+  const double inv = 1.0 / (double)g.N;
+  const int h = g.nl / 2;
+  const int lpb = std::max(1, std::min(8, 2048 / h));
+  const size_t sm = smem_bytes(h + 1, lpb);
+  const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
+  k_r2c_rows<<<dim3(nb, 1, F), kThreads, sm, L.stream>>>(nullptr, nullptr, g.nl, (long long)g.rows, lpb, inv,
+                                                         (scale && g.d == 1) ? 1 : 0, L.master, tab_r2c);
+  count(L);
+  for (int a = g.d - 2; a >= 0; --a) {
+    const int n = g.J[a];
+    long long S = g.hp1;
+    for (int b = a + 1; b <= g.d - 2; ++b) S *= g.J[b];
+    long long outer = 1;
+    for (int b = 0; b < a; ++b) outer *= g.J[b];
+    const int lp = std::max(1, std::min(8, 4096 / n));
+    const long long bpo = (S + lp - 1) / lp;
+    k_c2c_axis<-1><<<dim3((unsigned)(outer * bpo), 1, F), kThreads, smem_bytes(n, lp), L.stream>>>(
+        nullptr, nullptr, nullptr, n, S, S, 0, 0, 0, lp, inv, (scale && a == 0) ? 1 : 0, L.master, tab_c2c);
+    count(L);
+  }
+}
+
+void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_first, int m_last,
+                          const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2) {
+  const int nterms = m_last - m_first + 1;
+  for (int a = 0; a <= g.d - 2; ++a) {
+    const int n = g.J[a];
+    long long S = g.hp1;
+    for (int b = a + 1; b <= g.d - 2; ++b) S *= g.J[b];
+    long long outer = 1;
+    for (int b = 0; b < a; ++b) outer *= g.J[b];
+    const int lp = std::max(1, std::min(8, 4096 / n));
+    const long long bpo = (S + lp - 1) / lp;
+    const long long ts = (long long)g.Nh;
+    k_c2c_axis<+1><<<dim3((unsigned)(outer * bpo), (unsigned)nterms, F), kThreads, smem_bytes(n, lp), L.stream>>>(
+        nullptr, nullptr, nullptr, n, S, S, a == 0 ? 0 : ts, ts, a == 0 ? ts : 0, lp, 1.0, 0, L.master,
+        a == 0 ? tab0 : tab1);
+    count(L);
+  }
+  const int h = g.nl / 2;
+  const int lpb = std::max(1, std::min(8, 4096 / g.nl));
+  const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
+  k_c2r_accum<<<dim3(nb, 1, F), kThreads, smem_bytes(h + 1, lpb), L.stream>>>(
+      nullptr, (long long)g.Nh, nullptr, 0, m_first, m_last, nullptr, nullptr, g.nl, (long long)g.rows, lpb, nullptr,
+      nullptr, L.master, tab2);
+  count(L);
+}
+
 }  // namespace fw

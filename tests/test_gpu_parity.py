@@ -391,3 +391,21 @@ def test_slab_device_stages_equal_single_gpu_apply():
         op.ctx.sync()
         want = ref if m_first == 0 else op.apply(cfg.phi, 1)
         assert np.array_equal(got.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("J,nf", [((512, 512), 6), ((64, 128), 3), ((32, 32, 16), 2)])
+def test_batched_apply_equals_per_field(J, nf):
+    """fw_apply_batch_device (one batched pipeline for all fields, configs[4]) gives the
+    bits of one apply per field, and of the oracle for a small case."""
+    m = fw()
+    lo, hi = tuple(-4.0 for _ in J), tuple(4.0 for _ in J)
+    g = grid_of(J, lo, hi)
+    rng = np.random.default_rng(17 + len(J))
+    ops, us = [], []
+    for f in range(nf):
+        s = 0.9 + 0.2 * rng.random(J)
+        ops.append(m.build_expansion(m.OrderField(g, s), 8))
+        us.append(rng.standard_normal(J))
+    got = m.apply_batch(ops, us)
+    for op, u, x in zip(ops, us, got):
+        assert np.array_equal(x, op.apply(u))
