@@ -272,6 +272,10 @@ struct Geo {
     const int i = (e / (CP1 * CR1)) * CP1 + e % CP1, r = (e / CP1) % CR1;
     return cpad(i * CR1 + r);
   }
+  // the padded positions of a butterfly's R elements are base + r * stride (checked exhaustively
+  // for the instantiated sizes): pass-0 outputs, pass-1 and pass-2 inputs / rows
+  static constexpr int CS0 = CR1 + 1, CS2 = CT2 + CT2 / CR1 + 1;
+  static constexpr int RS0 = RT + 1, RS1 = 8, RS2 = 1;
   // row layouts: pass-0 input natural; passes 0 and 1 in place
   __device__ static __forceinline__ int rpad(int pos) { return pos + (pos >> RLT); }
   __device__ static __forceinline__ int r_p1raw(int e) { return e / RR0 + RT * (e % RR0); }
@@ -336,7 +340,7 @@ __device__ __forceinline__ void column_pair(double2* work, const double2* tw, in
     Dft<G::CR0, DIR>::run(a);
     double2* wb = work + mbr * G::LCOL;
 #pragma unroll
-    for (int r = 0; r < G::CR0; ++r) wb[G::c_p0out(I * G::CR0 + r)] = a[r];
+    for (int r = 0; r < G::CR0; ++r) wb[G::c_p0out(I * G::CR0) + r * G::CS0] = a[r];
   }
   gbar();
   mark(3);
@@ -346,15 +350,15 @@ __device__ __forceinline__ void column_pair(double2* work, const double2* tw, in
     double2 c0[G::CR1], c1[G::CR1];
 #pragma unroll
     for (int r = 0; r < G::CR1; ++r) {
-      c0[r] = work[G::c_p1(i, r)];
-      c1[r] = work[G::LCOL + G::c_p1(i, r)];
+      c0[r] = work[G::c_p1(i, 0) + r];
+      c1[r] = work[G::LCOL + G::c_p1(i, 0) + r];
     }
     butterfly<J0, 1, DIR>(c0, i, tw);
     butterfly<J0, 1, DIR>(c1, i, tw);
 #pragma unroll
     for (int r = 0; r < G::CR1; ++r) {
-      work[G::c_p1(i, r)] = c0[r];
-      work[G::LCOL + G::c_p1(i, r)] = c1[r];
+      work[G::c_p1(i, 0) + r] = c0[r];
+      work[G::LCOL + G::c_p1(i, 0) + r] = c1[r];
     }
   }
   gbar();
@@ -364,7 +368,7 @@ __device__ __forceinline__ void column_pair(double2* work, const double2* tw, in
     double2 c0[G::CR2], c1[G::CR2];
 #pragma unroll
     for (int r = 0; r < G::CR2; ++r) {
-      const int p = G::c_p2in(i + r * G::CT2);
+      const int p = G::c_p2in(i) + r * G::CS2;
       c0[r] = work[p];
       c1[r] = work[G::LCOL + p];
     }
@@ -383,19 +387,19 @@ __device__ __forceinline__ void row_passes01(double2* work, const double2* tw, i
   {
     double2 a[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) a[r] = work[G::rpad(l + r * G::RT)];
+    for (int r = 0; r < 8; ++r) a[r] = work[G::rpad(l) + r * G::RS0];
     Dft<8, DIR>::run(a);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = a[r];
+    for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = a[r];
   }
   pairbar(pair);
   {
     double2 a[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) a[r] = work[G::r_p1in(l + r * G::RT)];
+    for (int r = 0; r < 8; ++r) a[r] = work[G::r_p1in(l) + r * G::RS1];
     butterfly<h, 1, DIR>(a, l, tw);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) work[G::r_p1in(l + r * G::RT)] = a[r];
+    for (int r = 0; r < 8; ++r) work[G::r_p1in(l) + r * G::RS1] = a[r];
   }
   pairbar(pair);
 }
@@ -494,7 +498,9 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       const unsigned tu = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_U + g * 4 * CR0);
 
       // ---- F2: forward columns -> uhat (pass 0 straight from Y) -> tensor memory
+      FW_TRACE(135, 0);
       warp_wait(cY, (unsigned long long)J0);
+      FW_TRACE(135, 1);
       gb();  // every thread of the group has seen all rows
       {
         double2 a[CR0];
@@ -537,6 +543,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         }
         gb();
       }
+      FW_TRACE(135, 2);
 
       double rmax = 0.0;
       // ---- C(t): inverse columns -> pre-processed Z[t % KRING], column-major Z[k][k0]
@@ -568,6 +575,11 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         // the previous term's Z columns are published once this term's pass 0 is done:
         // by then its stores have drained and the release fence is cheap
         if (prm.dbg & 8) Z = prm.T + (size_t)(KRING - 1) * J0 * h;  // all terms into one slot
+        if (prm.dbg & 32) {  // timing experiment: columns skip the FFT
+          gb();
+          if (cg == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz);
+          continue;
+        }
         column_pair<G, +1>(work, twc, cg, a, gb, [&] {
           if (cg == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz);
         }, [&](int i, const double2* xa, const double2* xb) {
@@ -614,8 +626,9 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       const unsigned base = smem_u32(sm + G::OFF_TILE);
       tile = sm + G::OFF_TILE + (((base + 1023u) & ~1023u) - base) / 16u;
     }
-    auto tile_at = [&](int k, int rs) -> const double2& {
-      return tile[(size_t)k * 8 + (unsigned)(rs ^ (k & 7))];
+    // element k = l + 64 r of row slot rs: chunk (rs ^ (k & 7)) of the 128-B line of k
+    auto tile_at = [&](int l_, int rs, int r) -> const double2& {
+      return tile[l_ * 8 + (rs ^ (l_ & 7)) + r * 64 * 8];
     };
     // (s-s0)^m row of term t: global (streamed once), L2-prefetched one term ahead
     auto dev_row = [&](int t) -> const double2* {
@@ -654,19 +667,20 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
     }
 
     if (active) {
+      FW_TRACE(135, 0);
       // ---- F1: R2C of the row -> Y
       const double2* u2 = reinterpret_cast<const double2*>(prm.u) + (size_t)row * h;
 #pragma unroll
-      for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = u2[l + r * G::RT];
+      for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = u2[l + r * G::RT];
       pairbar(pair);
       row_passes01<G, -1>(work, twr, l, pair);
       double2 a[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l + r * G::RT)];
+      for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l) + r * G::RS2];
       butterfly<h, 2, -1>(a, l, twr);
       pairbar(pair);
 #pragma unroll
-      for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = a[r];
+      for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = a[r];
       pairbar(pair);
       double2* Yr = prm.Y + (size_t)row * H;
       for (int jj = l; jj <= h / 2; jj += 64) {
@@ -683,6 +697,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       }
       pairbar(pair);  // both warps' Y stores precede the signal
       if (!(rw & 1)) warp_signal(cY, 1ull);
+      FW_TRACE(135, 1);
       unsigned z[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) z[e] = 0u;
@@ -703,22 +718,23 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       {  // pass 0 (p = 1): tile -> work (natural positions)
         double2 a[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r] = tile_at(l + r * G::RT, pair);
+        for (int r = 0; r < 8; ++r) a[r] = tile_at(l, pair, r);
         Dft<8, +1>::run(a);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) work[G::rpad(l + r * G::RT)] = a[r];
+        for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = a[r];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty);  // this warp is done with tile t
       FW_TRACE(t, 4);
+      if (prm.dbg & 16) continue;  // timing experiment: rows do pass 0 only
       pairbar(pair);
       {
         double2 a[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r] = work[G::r_p1in(l + r * G::RT)];
+        for (int r = 0; r < 8; ++r) a[r] = work[G::r_p1in(l) + r * G::RS1];
         butterfly<h, 1, +1>(a, l, twr);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) work[G::r_p1in(l + r * G::RT)] = a[r];
+        for (int r = 0; r < 8; ++r) work[G::r_p1in(l) + r * G::RS1] = a[r];
       }
       pairbar(pair);
       FW_TRACE(t, 5);
@@ -726,7 +742,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       {
         double2 a[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l + r * G::RT)];
+        for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l) + r * G::RS2];
         butterfly<h, 2, +1>(a, l, twr);
 #pragma unroll
         for (int qt = 0; qt < 4; ++qt) {

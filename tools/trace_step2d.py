@@ -3,8 +3,8 @@ of the persistent step kernel (fw_step2d.cu, FW_TRACE marks; 8 marks per warp an
 
 column warps: 0 term start | 1 weights + uhat loaded | 2 ring slot free | 3 pass 0 | 4 pass 1
               | 5 pass 2 + pre-processing + Z stores | 6 group barrier
-row warps:    0 term start | 1 row barrier | 2 Z[t] complete | 3 tile loaded | 4 row barrier
-              | 5 passes 0-1 | 6 pass 2 + recombination | 7 pair barrier + next (s-s0)^m issued
+row warps:    0 term start | 2 tile of Z[t] landed (TMA) | 4 pass 0 + tile released | 5 pass 1
+              | 6 pass 2 + recombination | 7 pair barrier
 """
 import ctypes as C
 import os
@@ -30,7 +30,8 @@ tr = buf.reshape(2, 32, 136, 8).astype(np.int64)
 ntot = 34
 t0 = tr[:, :24][tr[:, :24] > 0].min()
 COL = ["w+uhat", "ring", "pass0", "pass1", "pass2+Z", "gbar"]
-ROW = ["rowbar", "cC wait", "tile", "rowbar", "pass01", "pass2+acc", "pairbar"]
+ROW = ["tile wait", "pass0", "pass1", "pass2+acc", "pairbar"]
+ROWMARKS = [0, 2, 4, 5, 6, 7]
 for sel in range(2):
     print(f"=== CTA {0 if sel == 0 else 100} (us; mean per term over terms 2..{ntot - 1})")
     for w in range(24):
@@ -39,7 +40,7 @@ for sel in range(2):
             continue
         names = COL if w < 8 else ROW
         nm = len(names) + 1
-        d = d[:, :nm].astype(np.float64)
+        d = (d[:, :nm] if w < 8 else d[:, ROWMARKS]).astype(np.float64)
         ok = (d > 0).all(axis=1)
         d = (d - t0) / 1000.0
         rng = [i for i in range(2, ntot) if ok[i]]
@@ -65,3 +66,12 @@ if len(ok):
         print(f"  slot {k:2d}: {(e1 - e0) / 1000.0:8.1f} us, gap {gap:6.1f} us; first term mark at "
               f"{(tr[0, :24][tr[0, :24] > 0].min() - e0) / 1000.0 if k == ok[-1] else float('nan'):6.1f}")
         prev = e1
+
+# step start marks (term slot 135): columns [0] before the F1 wait, [1] F1 complete, [2] F2 complete;
+# rows [0] F1 start, [1] F1 signalled
+for sel in range(2):
+    c = (tr[sel, 0, 135, :3] - t0) / 1000.0
+    r = (tr[sel, 8, 135, :2] - t0) / 1000.0
+    f = (tr[sel, 0, 0, 0] - t0) / 1000.0
+    print(f"CTA {0 if sel == 0 else 100}: rows F1 {r[0]:.1f} -> {r[1]:.1f} us; columns wait F1 {c[0]:.1f} -> {c[1]:.1f},"
+          f" F2 done {c[2]:.1f}, first term starts {f:.1f} us (t0 = earliest mark)")
