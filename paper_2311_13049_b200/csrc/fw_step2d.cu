@@ -1,32 +1,33 @@
 // fw_step2d.cu — persistent, warp-specialised single-launch 2D apply / seismic step (sm_100a).
 //
-// One cooperative launch of one CTA per SM does the whole seismic step (or one
-// operator apply) on a J0 x J1 grid (half spectrum H = J1/2 + 1 columns,
-// h = J1/2).  CTA b owns two mirror column pairs {k, h-k} of the half spectrum
-// (4 columns) and up to RMAX rows.  Its 16 warps are specialised and progress
-// independently (no CTA-wide barrier after setup):
+// One cooperative launch (one CTA per SM, 768 threads) does a whole seismic step
+// (seismic.cpp:111-133: two M-term applies sharing one forward transform, plus
+// the update) or one operator apply (flap.cpp:38-92) on a J0 x J1 grid
+// (half spectrum H = J1/2 + 1 columns, h = J1/2).  Warp roles:
 //
-//   column warps (8: a warp pair per column)       row warps (up to 8: one per row)
-//   F2: wait all rows -> C2C of its column of      F1: R2C of its row of u -> Y row
-//       Y, x 1/N -> uhat column (SHARED MEMORY,     R(t), t = (op, m) in order:
-//       kept for the whole step)                      wait all of Z[t%3]; h-point
-//   C(t), t = (op, m) in order:                       C2C of its row of Z; acc +=
-//       wait slot free (rows of t-3 done);            (s-s0)^m .* x in registers
-//       IFFT(w_m .* uhat) of the 4 columns; the    update (seismic.cpp:116-129) from
-//       C2R pre-processing of each mirror pair        the registers
-//       (k, h-k) -> Z[t%3] (global)
+//   column warps 0-7 (2 groups of 4)            row warps 8-23 (8 pairs; RMAX active)
+//   group g owns mirror slot b + g*gridDim:      pair p owns row r0 + p
+//   columns {s, h-s} of the half spectrum        F1: R2C of its row of u -> Y (global)
+//   F2: wait all rows, C2C of its 2 columns      R(t), t = (op, m) in ascending order:
+//       of Y, x 1/N -> uhat in TENSOR MEMORY         wait for the TMA tile of Z[t] (mbarrier),
+//   C(t), t = (op, m):                               pass 0 tile -> work, release the tile,
+//       a = w_m .* uhat (TMEM), IFFT of both         passes 1-2 in place, x (s-s0)^m, accumulate
+//       columns, C2R pre-processing of the pair      in TENSOR MEMORY (ascending m); operator
+//       in registers -> Z[t % 6] (column-major,      done: write L1 / fused seismic update
+//       global), publish (red.release)           pair RMAX: tile producer (one lane): wait for
+//                                                    the columns of term t, TMA the CTA's 8 rows
+//                                                    of Z[t] into the 128-B-swizzled tile
 //
-// Because a CTA owns both columns k and h-k, the C2R pre-processing
-// Z_k = f(X_k, X_{h-k}) happens in the column phase, so rows only run a plain
-// h-point C2C.  Producer/consumer ordering between warps of all CTAs uses
-// monotone counters counted in rows / Z columns (red.release.gpu /
-// ld.acquire.gpu), two counter sets alternating between launches.  Only the
-// term intermediate Z round-trips through global memory (a 2D FFT is an
-// all-to-all across SMs).  Registers are split with setmaxnreg (column warps
-// 96, row warps 160).  Arithmetic is the canonical FFT of fw_fft.cuh (radix
-// plan, twiddle values, fma placement, pre-processing formula): results are
-// bit-identical to the multi-pass path and to the CPU oracle.  Per-pass twiddle
-// tables live in shared memory in a [k][r-1] layout (odd stride, conflict-free).
+// Producer/consumer ordering between CTAs uses monotone counters (rows
+// transformed, Z columns stored per term, rows consumed per term;
+// red.release.gpu / red.relaxed.gpu / ld.acquire.gpu), two counter sets
+// alternating between launches; inside a CTA named barriers (column groups,
+// row pairs) and the full/empty mbarriers of the tile.  Every FFT pass is in
+// place per butterfly with padded, bank-conflict-free positions.  Registers are
+// split with setmaxnreg (column warps 112, row warps 64).  Arithmetic is the
+// canonical FFT of fw_fft.cuh (radix plan, twiddle values, fma placement,
+// pre-processing formula): results are bit-identical to the multi-pass path
+// and to the CPU oracle (tests/test_gpu_parity.py).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -557,16 +558,19 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           if (kB >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kB) * J0, J0 * sizeof(double));
         }
         double2 a[CR0];
+        {
+          double wk[CR0];  // all weight loads in flight before the first use (one L2 latency)
 #pragma unroll
-        for (int c = 0; c < 4 * CR0; c += 32) {
-          double wk[8];
+          for (int r = 0; r < CR0; ++r) wk[r] = (mycol >= 0 && !(prm.dbg & 2)) ? __ldg(&w[r * CT0]) : 0.5;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) wk[k] = (mycol >= 0 && !(prm.dbg & 2)) ? __ldg(&w[(c / 4 + k) * CT0]) : 0.5;
-          unsigned v[32];
-          tmem_ld32_nw(tu + c, v);
-          tmem_wait_ld();
+          for (int c = 0; c < 4 * CR0; c += 32) {
+            unsigned v[32];
+            tmem_ld32_nw(tu + c, v);
+            tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 8; ++k) a[c / 4 + k] = make_double2(wk[k] * tm_d(v, 2 * k), wk[k] * tm_d(v, 2 * k + 1));
+            for (int k = 0; k < 8; ++k)
+              a[c / 4 + k] = make_double2(wk[c / 4 + k] * tm_d(v, 2 * k), wk[c / 4 + k] * tm_d(v, 2 * k + 1));
+          }
         }
         FW_TRACE(t, 1);
         if (t >= KRING) warp_wait(&cR[t - KRING], (unsigned long long)J0);
@@ -642,13 +646,14 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       // the columns of term t are published and the consumers are done with tile t-1
       if (lane == 0) {
         for (int t = 0; t < ntot; ++t) {
+          // term t's columns first (its latency overlaps the consumers' pass 0 of term t-1)
+          while (ld_acquire(&cC[t]) < (unsigned long long)h) {
+          }
           if (t > 0) {
             mbar_wait(&tile_empty, (unsigned)(t - 1) & 1u);
             // the CTA's rows of Z[t-1] are consumed (in shared memory / registers): the ring
             // slot may be reused.  No release fence needed.
             red_relaxed_add(&cR[t - 1], (unsigned long long)nr);
-          }
-          while (ld_acquire(&cC[t]) < (unsigned long long)h) {
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy Z stores -> TMA reads
           if (!(prm.dbg & 4)) {
