@@ -315,7 +315,6 @@ __global__ void k_sup_check(long long N, const double* __restrict__ u, double th
 }
 
 // ---------------------------------------------------------------------------
-int lines_per_block(int n) { return std::max(1, std::min(8, 4096 / n)); }
 
 size_t smem_bytes(int n, int lpb) { return (size_t)2 * lpb * line_stride(n, lpb) * sizeof(double2); }
 
