@@ -205,7 +205,8 @@ struct fw_ctx_s {
   unsigned long long* counters = nullptr;     // persistent-kernel counters (2 sets)
   unsigned long long* trace = nullptr;        // FW_TRACE=1: persistent-kernel phase timestamps
   int cset = 0;
-  fw::LaunchCtx L() { return fw::LaunchCtx{stream, master, &launches}; }
+  bool generic_lines = false;                 // FW_GENERIC_LINES=1: shared-memory line FFTs only (tests)
+  fw::LaunchCtx L() { return fw::LaunchCtx{stream, master, &launches, generic_lines}; }
   int get_scratch(int slot, size_t bytes, void** out) {
     if (scratch_bytes[slot] < bytes) {
       if (scratch[slot]) cudaFree(scratch[slot]);
@@ -274,6 +275,8 @@ int fw_ctx_create(int device, fw_ctx* out) {
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
   const char* fg = getenv("FW_FORCE_GENERIC");
   c->force_generic = fg && fg[0] == '1';
+  const char* gl = getenv("FW_GENERIC_LINES");
+  c->generic_lines = gl && gl[0] == '1';
   const char* dg = getenv("FW_STEP2D_DBG");
   c->dbg = dg ? atoi(dg) : 0;
   if (dalloc(&c->counters, 2 * (size_t)fw::kStep2dCStride)) {

@@ -21,6 +21,7 @@ struct LaunchCtx {
   cudaStream_t stream = nullptr;
   const double2* master = nullptr;  // master twiddle table (kTwMaster entries)
   long long* launches = nullptr;    // host-side launch counter
+  bool generic_lines = false;       // FW_GENERIC_LINES=1: shared-memory line FFTs only (tests)
 };
 
 // u (N reals) -> Uh (Nh bins), scaled by 1/N (flap.cpp:46-50)
@@ -91,6 +92,11 @@ void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const Ba
 // tab0[f] = {Uh_f, T_f, w_f + m_first Nh}, tab1[f] = {T_f, T_f} (axes 1..d-2), tab2[f] = {T_f, -, -, dev1_f, out_f}
 void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_first, int m_last,
                           const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2);
+
+// register-resident line FFTs (fw_lines.cu) for n in {256, 512, 1024}; false = not served
+bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double2* dst, const double* w,
+                  long long S, long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts,
+                  int nterms, int nfields, double sc, bool scale, const BatchLine* bl);
 
 // stage entry points (distributed orchestration on local sub-arrays)
 void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, double2* H, double scale, bool do_scale);

@@ -336,6 +336,9 @@ void c2c_axis(const LaunchCtx& L, const GridGeom& g, int a, int dir, const doubl
   long long outer = 1;
   for (int b = 0; b < a; ++b) outer *= g.J[b];
   const long long inner = S;
+  if (!L.generic_lines &&
+      launch_lines(L, n, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, 1, sc, scale, nullptr))
+    return;
   const int lpb = std::max(1, std::min(8, 4096 / n));
   const long long bpo = (inner + lpb - 1) / lpb;
   dim3 grid((unsigned)(outer * bpo), (unsigned)nterms);
@@ -499,6 +502,9 @@ void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const Ba
     for (int b = a + 1; b <= g.d - 2; ++b) S *= g.J[b];
     long long outer = 1;
     for (int b = 0; b < a; ++b) outer *= g.J[b];
+    if (!L.generic_lines && launch_lines(L, n, -1, nullptr, nullptr, nullptr, S, outer, S, 0, 0, 0, 1, F, inv,
+                                         scale && a == 0, tab_c2c))
+      continue;
     const int lp = std::max(1, std::min(8, 4096 / n));
     const long long bpo = (S + lp - 1) / lp;
     k_c2c_axis<-1><<<dim3((unsigned)(outer * bpo), 1, F), kThreads, smem_bytes(n, lp), L.stream>>>(
@@ -516,9 +522,12 @@ void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_fi
     for (int b = a + 1; b <= g.d - 2; ++b) S *= g.J[b];
     long long outer = 1;
     for (int b = 0; b < a; ++b) outer *= g.J[b];
+    const long long ts = (long long)g.Nh;
+    if (!L.generic_lines && launch_lines(L, n, +1, nullptr, nullptr, nullptr, S, outer, S, a == 0 ? 0 : ts, ts,
+                                         a == 0 ? ts : 0, nterms, F, 1.0, false, a == 0 ? tab0 : tab1))
+      continue;
     const int lp = std::max(1, std::min(8, 4096 / n));
     const long long bpo = (S + lp - 1) / lp;
-    const long long ts = (long long)g.Nh;
     k_c2c_axis<+1><<<dim3((unsigned)(outer * bpo), (unsigned)nterms, F), kThreads, smem_bytes(n, lp), L.stream>>>(
         nullptr, nullptr, nullptr, n, S, S, a == 0 ? 0 : ts, ts, a == 0 ? ts : 0, lp, 1.0, 0, L.master,
         a == 0 ? tab0 : tab1);

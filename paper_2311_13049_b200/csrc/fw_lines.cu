@@ -1,0 +1,197 @@
+// fw_lines.cu — register-resident line FFTs along a strided axis (generic multi-pass path).
+//
+// One kernel family for the C2C passes of the multi-pass pipeline (3D grids, 2D
+// grids the persistent kernel does not serve, the slab stages): a block owns L
+// consecutive lines of one axis (line-fastest thread mapping, so every global
+// access of a warp is a contiguous run over L lines), thread (l, i) owns
+// butterfly i of line l in every pass.  Pass 0 reads its inputs straight from
+// global memory (optionally x w_m), the last pass writes straight to global
+// memory (optionally x scale); in between the line lives once in shared memory
+// in an in-place-per-butterfly layout (the canonical Stockham plan of
+// fw_fft.cuh, only the storage order differs), one barrier per pass boundary.
+// Bit-identical to k_c2c_axis / the CPU oracle (same radix plan, twiddles,
+// fma placement).
+#include <cuda_runtime.h>
+
+#include "fw_fft.cuh"
+#include "fw_internal.h"
+
+namespace fw {
+namespace lines {
+
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
+__host__ __device__ constexpr int npass(int n) { return (ilog2c(n) + 3) / 4; }
+__host__ __device__ constexpr int radix(int n, int i) {
+  return 1 << (ilog2c(n) / npass(n) + (i < ilog2c(n) % npass(n) ? 1 : 0));
+}
+__host__ __device__ constexpr int pprod(int n, int i) { return i == 0 ? 1 : pprod(n, i - 1) * radix(n, i - 1); }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+template <int N>
+struct Plan {
+  static constexpr int P = npass(N);
+  static constexpr int R0 = radix(N, 0), R1 = radix(N, 1), R2 = P > 2 ? radix(N, 2) : 1;
+  static constexpr int T0 = N / R0, T1 = N / R1, T2 = N / R2;
+  static constexpr int TMAX = cmax(T0, cmax(T1, P > 2 ? T2 : 0));
+  static constexpr int L = 256 / TMAX;  // lines per block (256 threads)
+  static constexpr int S1 = ilog2c(R1), ST = ilog2c(T1);
+  // padded position; the line stride is odd so the L lines of a quarter warp hit distinct banks
+  __device__ static __forceinline__ int pad(int p) { return p + (p >> S1) + (p >> ST); }
+  static constexpr int LS = ((N - 1) + ((N - 1) >> S1) + ((N - 1) >> ST) + 1) | 1;
+  // pass-0 output logical e -> position of pass-1 input (e % T1, e / T1) = (e % T1) R1 + e / T1
+  __device__ static __forceinline__ int p0out(int e) { return pad((e % T1) * R1 + e / T1); }
+  __device__ static __forceinline__ int p1(int i, int r) { return pad(i * R1 + r); }
+  // pass-2 input logical e: the pass-1 slot (i1, r1) that produced it
+  __device__ static __forceinline__ int p2in(int e) {
+    const int i1 = (e / (R0 * R1)) * R0 + e % R0, r1 = (e / R0) % R1;
+    return pad(i1 * R1 + r1);
+  }
+  static_assert(P == 2 || P == 3, "2- or 3-pass plans");
+  static_assert(L >= 1 && L * TMAX == 256, "256 threads");
+};
+
+// twiddled radix-R butterfly of pass PASS (p = pprod > 1): twiddles = master entries
+template <int N, int PASS, int DIR>
+__device__ __forceinline__ void bfly(double2* a, int i, const double2* __restrict__ master) {
+  constexpr int R = radix(N, PASS);
+  constexpr int p = pprod(N, PASS);
+  if constexpr (p > 1) {
+    const int k = i & (p - 1);
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double2 w = __ldg(&master[(r * k) * (kTwMaster / (p * R))]);
+      a[r] = cmulw(a[r], w.x, DIR < 0 ? -w.y : w.y);
+    }
+  }
+  Dft<R, DIR>::run(a);
+}
+
+// C2C of lines of length N along an axis of stride S (line (o, in): o*N*S + in + j*S).
+// blockIdx.y = term (src/dst/w advance by their term strides), blockIdx.z = field (bl).
+template <int N, int DIR>
+__global__ void __launch_bounds__(256) k_lines(const double2* __restrict__ src, double2* __restrict__ dst,
+                                               const double* __restrict__ w, long long S, long long inner,
+                                               long long src_ts, long long dst_ts, long long w_ts, double sc,
+                                               int do_scale, const double2* __restrict__ master,
+                                               const BatchLine* __restrict__ bl) {
+  using PL = Plan<N>;
+  constexpr int L = PL::L;
+  extern __shared__ double2 sm[];  // L lines x LS
+  if (bl) {
+    src = static_cast<const double2*>(bl[blockIdx.z].src);
+    dst = static_cast<double2*>(bl[blockIdx.z].dst);
+    w = bl[blockIdx.z].w;
+  }
+  const long long term = blockIdx.y;
+  src += term * src_ts;
+  dst += term * dst_ts;
+  if (w) w += term * w_ts;
+  const long long bpo = (inner + L - 1) / L;
+  const long long o = blockIdx.x / bpo;
+  const long long in0 = (blockIdx.x - o * bpo) * L;
+  const int l = threadIdx.x % L, i = threadIdx.x / L;
+  const bool live = in0 + l < inner;
+  const long long base = o * (long long)N * S + in0 + l;
+  double2* line = sm + l * PL::LS;
+
+  {  // pass 0 (no twiddles): global -> registers -> shared
+    constexpr int R = PL::R0, T = PL::T0;
+    if (i < T) {
+      double2 a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long idx = base + (long long)(i + r * T) * S;
+        double2 v = live ? src[idx] : make_double2(0.0, 0.0);
+        if (w && live) {
+          const double wk = __ldg(&w[idx]);
+          v.x = wk * v.x;
+          v.y = wk * v.y;
+        }
+        a[r] = v;
+      }
+      Dft<R, DIR>::run(a);
+#pragma unroll
+      for (int r = 0; r < R; ++r) line[PL::p0out(i * R + r)] = a[r];
+    }
+  }
+  __syncthreads();
+  if constexpr (PL::P == 3) {  // middle pass, in place
+    constexpr int R = PL::R1, T = PL::T1;
+    if (i < T) {
+      double2 a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = line[PL::p1(i, r)];
+      bfly<N, 1, DIR>(a, i, master);
+#pragma unroll
+      for (int r = 0; r < R; ++r) line[PL::p1(i, r)] = a[r];
+    }
+    __syncthreads();
+  }
+  {  // last pass: shared -> registers -> global (natural order q = i + r T)
+    constexpr int LAST = PL::P - 1;
+    constexpr int R = radix(N, LAST), T = N / R;
+    if (i < T) {
+      double2 a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = line[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * T)];
+      bfly<N, LAST, DIR>(a, i, master);
+      if (live) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          double2 v = a[r];
+          if (do_scale) {
+            v.x *= sc;
+            v.y *= sc;
+          }
+          dst[base + (long long)(i + r * T) * S] = v;
+        }
+      }
+    }
+  }
+}
+
+template <int N>
+bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
+              long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
+              int nfields, double sc, bool scale, const BatchLine* bl) {
+  constexpr int LPB = Plan<N>::L;
+  constexpr size_t SMEM = (size_t)LPB * Plan<N>::LS * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lines<N, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, +1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    attr = true;
+  }
+  const long long bpo = (inner + LPB - 1) / LPB;
+  const dim3 grid((unsigned)(outer * bpo), (unsigned)nterms, (unsigned)nfields);
+  if (dir < 0)
+    k_lines<N, -1><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, scale ? 1 : 0,
+                                                   L.master, bl);
+  else
+    k_lines<N, +1><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, scale ? 1 : 0,
+                                                   L.master, bl);
+  if (L.launches) *L.launches += 1;
+  return true;
+}
+
+}  // namespace lines
+
+bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double2* dst, const double* w,
+                  long long S, long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts,
+                  int nterms, int nfields, double sc, bool scale, const BatchLine* bl) {
+  switch (n) {
+    case 256:
+      return lines::launch_n<256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
+                                  scale, bl);
+    case 512:
+      return lines::launch_n<512>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
+                                  scale, bl);
+    case 1024:
+      return lines::launch_n<1024>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
+                                   scale, bl);
+    default:
+      return false;
+  }
+}
+
+}  // namespace fw

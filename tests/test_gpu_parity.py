@@ -409,3 +409,33 @@ def test_batched_apply_equals_per_field(J, nf):
     got = m.apply_batch(ops, us)
     for op, u, x in zip(ops, us, got):
         assert np.array_equal(x, op.apply(u))
+
+
+def lines_context():
+    import os
+
+    m = fw()
+    os.environ["FW_GENERIC_LINES"] = "1"
+    try:
+        return m.Context(0)
+    finally:
+        del os.environ["FW_GENERIC_LINES"]
+
+
+@pytest.mark.parametrize("J", [(256, 16, 8), (512, 8, 8), (1024, 4, 8), (16, 256, 8), (8, 512, 4), (256, 64),
+                               (1024, 32), (512, 512)])
+def test_register_line_ffts_equal_shared_memory_path(J):
+    """fw_lines.cu (register-resident line FFTs for n in {256, 512, 1024}) against the
+    shared-memory line kernels: identical bits, both directions (forward + inverse)."""
+    m = fw()
+    lo, hi = tuple(-3.0 for _ in J), tuple(3.0 for _ in J)
+    g = grid_of(J, lo, hi)
+    rng = np.random.default_rng(sum(J))
+    s = 0.8 + 0.4 * rng.random(J)
+    u = rng.standard_normal(J)
+    op_a = m.build_expansion(m.OrderField(g, s), 5)
+    op_b = m.build_expansion(m.OrderField(g, s), 5, ctx=lines_context())
+    for m_first in (0, 1):
+        a, ra = op_a.apply(u, m_first, residue=True)
+        b, rb = op_b.apply(u, m_first, residue=True)
+        assert np.array_equal(a, b) and ra == rb
