@@ -257,6 +257,7 @@ def run_slab(args, cfg_fn, name):
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+    _fast_exit()  # while the context and its tensors are still alive
 
 
 def run_c5(args):
@@ -322,6 +323,7 @@ def run_c5(args):
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+    _fast_exit()  # while the context and its tensors are still alive
 
 
 def _fast_exit():

@@ -98,6 +98,11 @@ bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double
                   long long S, long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts,
                   int nterms, int nfields, double sc, bool scale, const BatchLine* bl);
 
+// register-resident row C2R + ascending-m recombination (fw_lines.cu) for nl in {256, 512, 1024}
+bool launch_rows_c2r(const LaunchCtx& L, int nl, const double2* src, long long src_ts, int m_first, int m_last,
+                     const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
+                     const BatchLine* bl);
+
 // stage entry points (distributed orchestration on local sub-arrays)
 void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, double2* H, double scale, bool do_scale);
 void launch_stage_c2c(const LaunchCtx& L, const GridGeom& g, int axis, int dir, const double2* src, double2* dst,

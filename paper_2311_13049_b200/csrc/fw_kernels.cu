@@ -382,6 +382,10 @@ void launch_forward(const LaunchCtx& L, const GridGeom& g, const double* u, doub
 static void c2r_accum(const LaunchCtx& L, const GridGeom& g, const double2* src, long long src_ts, const double* w,
                       long long w_ts, int m_first, int m_last, const double* dev1, double* out, double* residue,
                       const int* guard) {
+  if (!w && !L.generic_lines &&
+      launch_rows_c2r(L, g.nl, src, src_ts, m_first, m_last, dev1, out, (long long)g.rows, 1, residue, guard,
+                      nullptr))
+    return;
   const int h = g.nl / 2;
   const int lpb = std::max(1, std::min(8, 4096 / g.nl));
   const size_t sm = smem_bytes(h + 1, lpb);
@@ -533,6 +537,9 @@ void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_fi
         a == 0 ? tab0 : tab1);
     count(L);
   }
+  if (!L.generic_lines && launch_rows_c2r(L, g.nl, nullptr, (long long)g.Nh, m_first, m_last, nullptr, nullptr,
+                                         (long long)g.rows, F, nullptr, nullptr, tab2))
+    return;
   const int h = g.nl / 2;
   const int lpb = std::max(1, std::min(8, 4096 / g.nl));
   const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);

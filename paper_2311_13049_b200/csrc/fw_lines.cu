@@ -174,6 +174,147 @@ bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, con
   return true;
 }
 
+// Per row of the last axis (NL reals, h = NL/2 complex, rows contiguous): for every
+// term m = m_first..m_last in ascending order, C2R of the half-spectrum row src_m
+// (flap.cpp:21-36: pre-processing Z_q = f(X_q, X_{h-q}), h-point C2C, real parts
+// interleaved) and acc += 0 + (s-s0)^m .* x with (s-s0)^m = (s-s0)^{m-1} (s-s0) carried
+// per element (flap.cpp:61-91, 124-133).  Thread (row, i) owns butterfly i of every
+// pass; its outputs q = i + r T_last and their accumulators stay in registers across
+// the terms, the running powers in shared memory.
+template <int H>
+struct RowPlan {
+  using P = Plan<H>;
+  static constexpr int TM = P::TMAX;                 // threads per row
+  static constexpr int RL = radix(H, P::P - 1);      // last-pass radix
+  static constexpr int TL = H / RL;
+  static constexpr int XS = (H + 1) | 1;             // X row stride (natural order, odd)
+  static constexpr size_t ROWB = (size_t)(XS + P::LS) * sizeof(double2) + (size_t)2 * H * sizeof(double);
+  // rows per block: up to 256 threads, at most ~110 KB of shared memory (two blocks per SM)
+  static constexpr int RPB = (256 / TM) * ROWB <= 112640 ? 256 / TM : (int)(112640 / ROWB);
+  static constexpr int NT = RPB * TM;
+  static constexpr size_t SMEM = (size_t)RPB * ROWB;
+  static_assert(RPB >= 1, "row fits");
+};
+
+template <int H>
+__global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ src, long long src_ts, int m_first,
+                                                  int m_last, const double* __restrict__ dev1,
+                                                  double* __restrict__ out, long long rows, double* residue,
+                                                  const int* guard, const double2* __restrict__ master,
+                                                  const BatchLine* __restrict__ bl) {
+  using RP = RowPlan<H>;
+  using PL = Plan<H>;
+  constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL, NL = 2 * H;
+  if (guard && *guard != kNoBlowup) return;
+  if (bl) {
+    src = static_cast<const double2*>(bl[blockIdx.z].src);
+    dev1 = bl[blockIdx.z].aux;
+    out = bl[blockIdx.z].out;
+  }
+  extern __shared__ double2 sm[];
+  const int rl = threadIdx.x / TM, i = threadIdx.x % TM;
+  const long long row = (long long)blockIdx.x * RPB + rl;
+  const bool live = row < rows;
+  double2* X = sm + rl * RP::XS;                            // natural-order X of this row
+  double2* Wk = sm + RPB * RP::XS + rl * PL::LS;           // FFT work (in-place layout)
+  double* devm = reinterpret_cast<double*>(sm + RPB * (RP::XS + PL::LS)) + (size_t)rl * NL;
+  double acc[2 * RL];
+#pragma unroll
+  for (int e = 0; e < 2 * RL; ++e) acc[e] = 0.0;
+  double rmax = 0.0;
+  const double* d1row = dev1 ? dev1 + row * NL : nullptr;
+  for (int m = m_first; m <= m_last; ++m) {
+    const double2* S = src + (long long)(m - m_first) * src_ts + row * (H + 1);
+    if (live)
+      for (int k = i; k <= H; k += TM) X[k] = S[k];
+    __syncthreads();
+    if (residue && live && i == 0) rmax = fmax(rmax, fabs(X[0].y) + fabs(X[H].y));
+    {  // C2R pre-processing + pass 0 (no twiddles) -> work
+      constexpr int R = PL::R0, T = PL::T0;
+      if (i < T) {
+        double2 a[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int q = i + r * T;
+          a[r] = c2r_pre(X[q], X[H - q], q, H, master);
+        }
+        Dft<R, +1>::run(a);
+#pragma unroll
+        for (int r = 0; r < R; ++r) Wk[PL::p0out(i * R + r)] = a[r];
+      }
+    }
+    __syncthreads();
+    if constexpr (PL::P == 3) {
+      constexpr int R = PL::R1, T = PL::T1;
+      if (i < T) {
+        double2 a[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) a[r] = Wk[PL::p1(i, r)];
+        bfly<H, 1, +1>(a, i, master);
+#pragma unroll
+        for (int r = 0; r < R; ++r) Wk[PL::p1(i, r)] = a[r];
+      }
+      __syncthreads();
+    }
+    {  // last pass -> outputs z_q, q = i + r TL: reals x[2q], x[2q+1]
+      constexpr int LAST = PL::P - 1;
+      if (i < TL) {
+        double2 a[RL];
+#pragma unroll
+        for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * TL)];
+        bfly<H, LAST, +1>(a, i, master);
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int q = i + r * TL;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const double x = c ? a[r].y : a[r].x;
+            double v;
+            if (m == 0 || !d1row) {
+              v = x;
+            } else {
+              const int j = 2 * q + c;
+              const double d = (m == 1) ? __ldg(&d1row[j]) : devm[j] * __ldg(&d1row[j]);
+              devm[j] = d;
+              v = d * x;
+            }
+            double p = 0.0;
+            p += v;
+            acc[2 * r + c] += p;
+          }
+        }
+      }
+    }
+    __syncthreads();  // X / work buffers are rewritten by the next term
+  }
+  if (live && i < TL) {
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const int q = i + r * TL;
+      reinterpret_cast<double2*>(out + row * NL)[q] = make_double2(acc[2 * r], acc[2 * r + 1]);
+    }
+  }
+  if (residue && live && i == 0 && rmax > 0.0)
+    atomicMax(reinterpret_cast<unsigned long long*>(residue), (unsigned long long)__double_as_longlong(rmax));
+}
+
+template <int H>
+bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m_first, int m_last,
+                 const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
+                 const BatchLine* bl) {
+  using RP = RowPlan<H>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rows_c2r<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RP::SMEM);
+    attr = true;
+  }
+  const dim3 grid((unsigned)((rows + RP::RPB - 1) / RP::RPB), 1, (unsigned)nfields);
+  k_rows_c2r<H><<<grid, RP::NT, RP::SMEM, L.stream>>>(src, src_ts, m_first, m_last, dev1, out, rows, residue, guard,
+                                                    L.master, bl);
+  if (L.launches) *L.launches += 1;
+  return true;
+}
+
 }  // namespace lines
 
 bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double2* dst, const double* w,
@@ -189,6 +330,21 @@ bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double
     case 1024:
       return lines::launch_n<1024>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
                                    scale, bl);
+    default:
+      return false;
+  }
+}
+
+bool launch_rows_c2r(const LaunchCtx& L, int nl, const double2* src, long long src_ts, int m_first, int m_last,
+                     const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
+                     const BatchLine* bl) {
+  switch (nl / 2) {
+    case 128:
+      return lines::launch_rows<128>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl);
+    case 256:
+      return lines::launch_rows<256>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl);
+    case 512:
+      return lines::launch_rows<512>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl);
     default:
       return false;
   }

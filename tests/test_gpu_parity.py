@@ -439,3 +439,21 @@ def test_register_line_ffts_equal_shared_memory_path(J):
         a, ra = op_a.apply(u, m_first, residue=True)
         b, rb = op_b.apply(u, m_first, residue=True)
         assert np.array_equal(a, b) and ra == rb
+
+
+@pytest.mark.parametrize("J", [(64, 256), (32, 512), (16, 1024), (8, 8, 256), (4, 16, 512), (300 // 75 * 2, 256)])
+def test_register_row_c2r_equal_shared_memory_path(J):
+    """fw_lines.cu k_rows_c2r (row C2R + ascending-m recombination with registers) against
+    the shared-memory k_c2r_accum: identical bits incl. the imaginary residue."""
+    m = fw()
+    lo, hi = tuple(-3.0 for _ in J), tuple(3.0 for _ in J)
+    g = grid_of(J, lo, hi)
+    rng = np.random.default_rng(7 * sum(J))
+    s = 0.8 + 0.4 * rng.random(J)
+    u = rng.standard_normal(J)
+    op_a = m.build_expansion(m.OrderField(g, s), 6)
+    op_b = m.build_expansion(m.OrderField(g, s), 6, ctx=lines_context())
+    for m_first in (0, 1):
+        a, ra = op_a.apply(u, m_first, residue=True)
+        b, rb = op_b.apply(u, m_first, residue=True)
+        assert np.array_equal(a, b) and ra == rb
