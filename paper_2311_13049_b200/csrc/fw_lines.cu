@@ -223,11 +223,22 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
   for (int e = 0; e < 2 * RL; ++e) acc[e] = 0.0;
   double rmax = 0.0;
   const double* d1row = dev1 ? dev1 + row * NL : nullptr;
+  // X rows arrive by cp.async one term ahead: the next term's copy is issued as soon as
+  // pass 0 of this term has read the buffer, and lands during the remaining passes
+  auto fetch = [&](int m) {
+    if (live && m <= m_last) {
+      const double2* S = src + (long long)(m - m_first) * src_ts + row * (H + 1);
+      for (int k = i; k <= H; k += TM)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(&X[k])),
+                     "l"(S + k)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  fetch(m_first);
   for (int m = m_first; m <= m_last; ++m) {
-    const double2* S = src + (long long)(m - m_first) * src_ts + row * (H + 1);
-    if (live)
-      for (int k = i; k <= H; k += TM) X[k] = S[k];
-    __syncthreads();
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();  // X of term m complete; every thread is done with the previous term's work buffer
     if (residue && live && i == 0) rmax = fmax(rmax, fabs(X[0].y) + fabs(X[H].y));
     {  // C2R pre-processing + pass 0 (no twiddles) -> work
       constexpr int R = PL::R0, T = PL::T0;
@@ -244,6 +255,7 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
       }
     }
     __syncthreads();
+    fetch(m + 1);  // X is free again
     if constexpr (PL::P == 3) {
       constexpr int R = PL::R1, T = PL::T1;
       if (i < T) {
@@ -285,7 +297,6 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
         }
       }
     }
-    __syncthreads();  // X / work buffers are rewritten by the next term
   }
   if (live && i < TL) {
 #pragma unroll
