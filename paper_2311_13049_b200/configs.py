@@ -183,6 +183,14 @@ def bytes_per_apply(N: int, N_half: int, M: int, table_model: bool = True) -> in
     return 8 * N + 8 * N + dev + 8 * (M + 1) * N_half
 
 
+def bytes_per_apply_pass_model(N: int, N_half: int, M: int, table_model: bool = True) -> int:
+    """SURVEY.md §8(d) 3D pass model (one plane pass + transpose + one pencil pass per
+    transform, intermediates in HBM): 8N + 3*16 N_h + (M+1)(16+8+16+16) N_h + 8MN + 8N;
+    the 8MN deviation-table term becomes 8N when the powers are regenerated on chip."""
+    dev = 8 * M * N if table_model else 8 * N
+    return 8 * N + 3 * 16 * N_half + (M + 1) * (16 + 8 + 16 + 16) * N_half + dev + 8 * N
+
+
 def bytes_per_seismic_step(N: int, N_half: int, M: int, table_model: bool = True) -> int:
     """B_step = 2 B_apply - 8N + 72N (shared forward transform, update
     reading cur, prev, L1, L2, L2prev, c, eta, tau_c and writing next)."""
