@@ -89,9 +89,12 @@ class SlabApply:
         loc = (g.J0l, g.J[1], g.J[2])
         Y = st.r2c(u_slab, loc)                                   # [J0l][J1][H]
         Y = st.c2c(Y, loc, axis=1, dir=-1)
-        send = [st.contig(Y[:, q * g.J1l:(q + 1) * g.J1l, :]) for q in range(g.P)]
-        recv = self.comm.all_to_all(send)                         # from p: [J0l][J1l][H]
-        T = st.concat(recv, axis=0)                               # [J0][J1l][H]
+        if g.P == 1:  # no transpose: the local array is the whole spectrum
+            T = Y
+        else:
+            send = [st.contig(Y[:, q * g.J1l:(q + 1) * g.J1l, :]) for q in range(g.P)]
+            recv = self.comm.all_to_all(send)                     # from p: [J0l][J1l][H]
+            T = st.concat(recv, axis=0)                           # [J0][J1l][H]
         return st.c2c(T, (g.J[0], g.J1l, g.J[2]), axis=0, dir=-1, scale=1.0 / g.N)
 
     def inverse(self, uhat_t, m_first: int = 0):
@@ -99,10 +102,15 @@ class SlabApply:
         nt = self.m_last - m_first + 1
         tshape = (g.J[0], g.J1l, g.J[2])
         T = st.c2c(uhat_t, tshape, axis=0, dir=+1, w=self.w[m_first:], nterms=nt, src_ts=0, w_ts=1)
-        # T: [nt][J0][J1l][H] -> to rank q: its planes of every term
-        send = [st.contig(T[:, q * g.J0l:(q + 1) * g.J0l]) for q in range(g.P)]
-        recv = self.comm.all_to_all(send)                         # from p: [nt][J0l][J1l][H]
-        Ts = st.concat(recv, axis=2)                              # [nt][J0l][J1][H]
+        if nt == 1 and len(T.shape) == 3:  # single term: keep the term axis for the transpose
+            T = T.reshape((1,) + tuple(T.shape))
+        if g.P == 1:
+            Ts = T
+        else:
+            # T: [nt][J0][J1l][H] -> to rank q: its planes of every term
+            send = [st.contig(T[:, q * g.J0l:(q + 1) * g.J0l]) for q in range(g.P)]
+            recv = self.comm.all_to_all(send)                     # from p: [nt][J0l][J1l][H]
+            Ts = st.concat(recv, axis=2)                          # [nt][J0l][J1][H]
         loc = (g.J0l, g.J[1], g.J[2])
         Ts = st.c2c(Ts, loc, axis=1, dir=+1, nterms=nt, src_ts=1)
         return st.c2r(Ts, loc, m_first, self.m_last, self.dev1)

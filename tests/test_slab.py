@@ -148,3 +148,14 @@ def test_slab_geometry_validation():
     g = SlabGeometry((256, 256, 256), 8, 3)
     assert (g.J0l, g.J1l, g.H) == (32, 32, 129)
     assert g.rows == slice(96, 128) and g.cols == slice(96, 128)
+
+
+def test_slab_world2_single_term():
+    """One term in the inverse (M = 1, m_first = 1): the batched transpose keeps its term axis."""
+    J, lo, hi, M = (8, 16, 16), (-2.0, -2.0, -2.0), (2.0, 2.0, 2.0), 1
+    two = run_distributed(2, J, lo, hi, M, 1)
+    rng = np.random.default_rng(5)
+    s = 1.0 + 0.3 * np.sin(np.pi * cfgs._mesh(lo, hi, J)[0] / 2.0)
+    u = rng.standard_normal(J)
+    ref, _ = O.port_apply(J, lo, hi, s, u, M, m_first=1)
+    assert np.linalg.norm(two - ref) / np.linalg.norm(ref) < 1e-13
