@@ -202,6 +202,7 @@ struct fw_ctx_s {
   int nsm = 148;
   bool force_generic = false;                 // FW_FORCE_GENERIC=1: multi-pass kernels only
   int dbg = 0;                                // FW_STEP2D_DBG: timing experiments only (wrong results)
+  int steps_per_launch = 0;                   // FW_STEPS_PER_LAUNCH: seismic steps per persistent launch (0 = all)
   unsigned long long* counters = nullptr;     // persistent-kernel counters (2 sets)
   unsigned long long* trace = nullptr;        // FW_TRACE=1: persistent-kernel phase timestamps
   int cset = 0;
@@ -279,6 +280,8 @@ int fw_ctx_create(int device, fw_ctx* out) {
   c->generic_lines = gl && gl[0] == '1';
   const char* dg = getenv("FW_STEP2D_DBG");
   c->dbg = dg ? atoi(dg) : 0;
+  const char* spl = getenv("FW_STEPS_PER_LAUNCH");
+  c->steps_per_launch = spl ? std::max(0, atoi(spl)) : 0;
   if (dalloc(&c->counters, 2 * (size_t)fw::kStep2dCStride)) {
     fw_ctx_destroy(c);
     return FW_E_OOM;
@@ -417,6 +420,7 @@ int launch_persistent(fw_ctx ctx, fw_op const* ops, int nops, int m_first, const
   FW_TRY(ctx->get_scratch(SLOT_Y2D, g.Nh * sizeof(double2), &Y));
   FW_TRY(ctx->get_scratch(SLOT_T2D, (size_t)fw::kStep2dRing * g.Nh * sizeof(double2), &T));
   fw::Step2DParams p = extra ? *extra : fw::Step2DParams{};
+  if (p.nsteps < 1) p.nsteps = 1;
   p.J0 = g.J[0];
   p.J1 = g.J[1];
   p.M = m_last;
@@ -717,6 +721,36 @@ void seis_free(fw_seis s) {
 }
 
 // one SeismicStepper::step (seismic.cpp:111-133), enqueued
+bool seis_persistent(fw_seis s) {
+  return use_persistent(s->A1) && use_persistent(s->A2) && s->A1->constant_order == s->A2->constant_order;
+}
+
+// nsteps seismic steps in ONE persistent launch (the kernel rotates the state buffers by level)
+int seis_enqueue_persistent(fw_seis s, int nsteps) {
+  fw::Step2DParams x{};
+  x.seismic = 1;
+  x.prev = s->prev();
+  x.ap = s->ap();
+  x.c = s->c;
+  x.eta = s->eta;
+  x.tc = s->tc;
+  x.next = s->ubuf[(s->lvl + 1) % 3];
+  x.tau = s->tau;
+  x.thr = s->thr;
+  x.step = (int)(s->n + 1);
+  x.flag = s->flag;
+  x.nsteps = nsteps;
+  for (int i = 0; i < 3; ++i) x.ub[i] = s->ubuf[i];
+  for (int i = 0; i < 2; ++i) x.ab[i] = s->abuf[i];
+  x.lvl0 = s->lvl;
+  fw_op ops[2] = {s->A1, s->A2};
+  double* outs[2] = {s->l1, s->abuf[s->lvl % 2]};
+  FW_TRY(launch_persistent(s->ctx, ops, 2, 0, s->cur(), outs, nullptr, &x));
+  s->n += nsteps;
+  s->lvl += nsteps;
+  return FW_OK;
+}
+
 int seis_enqueue_step(fw_seis s) {
   fw_ctx ctx = s->ctx;
   const fw::GridGeom& g = s->g;
@@ -865,6 +899,16 @@ void fw_seis_destroy(fw_seis s) {
 
 int fw_seis_enqueue(fw_seis s, int nsteps) {
   if (!s || nsteps < 0) return set_err(FW_E_ARG, "bad argument");
+  if (seis_persistent(s) && nsteps > 0) {
+    const int per = s->ctx->steps_per_launch > 0 ? s->ctx->steps_per_launch : nsteps;
+    for (int done = 0; done < nsteps;) {
+      const int k = std::min(per, nsteps - done);
+      FW_TRY(seis_enqueue_persistent(s, k));
+      done += k;
+    }
+    FW_CUDA(cudaGetLastError());
+    return FW_OK;
+  }
   for (int i = 0; i < nsteps; ++i) FW_TRY(seis_enqueue_step(s));
   FW_CUDA(cudaGetLastError());
   return FW_OK;

@@ -97,13 +97,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// optional instrumentation: trace[(sel*32 + warp)*136 + t][8] = globaltimer at phase marks
+// optional instrumentation (build with -DFW_STEP2D_TRACE=1, then FW_TRACE=1 at run time):
+// trace[(sel*32 + warp)*136 + t][8] = globaltimer at phase marks.  Compiled out by default:
+// the address arithmetic would cost registers in the hot loops.
+#ifndef FW_STEP2D_TRACE
+#define FW_STEP2D_TRACE 0
+#endif
+#if FW_STEP2D_TRACE
 #define FW_TRACE(t, slot)                                                                              \
   do {                                                                                                 \
     if (prm.trace && (threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 100))               \
       prm.trace[(((size_t)(blockIdx.x == 0 ? 0 : 1) * 32 + (threadIdx.x >> 5)) * 136 + (t)) * 8 + (slot)] = \
           gtimer();                                                                                    \
   } while (0)
+#else
+#define FW_TRACE(t, slot) \
+  do {                    \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- TMEM as accumulator storage
 // Row accumulators live in tensor memory (tcgen05.ld/st, 32 lanes x 32 columns of 32 bit
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
 
   // launch marks (tracing only): warp slot 31 of the trace, [step % 64][entry, exit]
   auto launch_mark = [&](int which) {
-    if (prm.trace && tid == 0 && (b == 0 || b == 100))
+    if (FW_STEP2D_TRACE && prm.trace && tid == 0 && (b == 0 || b == 100))
       prm.trace[((size_t)(b == 0 ? 0 : 1) * 32 + 31) * 136 * 8 + (size_t)(prm.step & 63) * 2 + which] = gtimer();
   };
   launch_mark(0);
@@ -498,9 +509,12 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       // this thread's uhat values: TMEM lane (32 (warp & 3) + lane), columns TM_U + g 4 CR0 + [0, 4 CR0)
       const unsigned tu = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_U + g * 4 * CR0);
 
+      double rmax = 0.0;
+#pragma unroll 1
+      for (int s = 0; s < prm.nsteps; ++s) {  // launch steps (counters are cumulative over them)
       // ---- F2: forward columns -> uhat (pass 0 straight from Y) -> tensor memory
       FW_TRACE(135, 0);
-      warp_wait(cY, (unsigned long long)J0);
+      warp_wait(cY, (unsigned long long)(s + 1) * J0);
       FW_TRACE(135, 1);
       gb();  // every thread of the group has seen all rows
       {
@@ -546,8 +560,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       }
       FW_TRACE(135, 2);
 
-      double rmax = 0.0;
-      // ---- C(t): inverse columns -> pre-processed Z[t % KRING], column-major Z[k][k0]
+      // ---- C(t): inverse columns -> pre-processed Z[gt % KRING] (gt = s ntot + t), column-major Z[k][k0]
       for (int t = 0; t < ntot; ++t) {
         FW_TRACE(t, 0);
         const int op = t / nterms, m = prm.m_first + t % nterms;
@@ -573,9 +586,10 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           }
         }
         FW_TRACE(t, 1);
-        if (t >= KRING) warp_wait(&cR[t - KRING], (unsigned long long)J0);
+        const int gt = s * ntot + t;  // term index over the launch
+        if (gt >= KRING) warp_wait(&cR[(gt - KRING) % ntot], (unsigned long long)((gt - KRING) / ntot + 1) * J0);
         FW_TRACE(t, 2);
-        double2* Z = prm.T + (size_t)(t % KRING) * J0 * h;
+        double2* Z = prm.T + (size_t)(gt % KRING) * J0 * h;
         // the previous term's Z columns are published once this term's pass 0 is done:
         // by then its stores have drained and the release fence is cheap
         if (prm.dbg & 8) Z = prm.T + (size_t)(KRING - 1) * J0 * h;  // all terms into one slot
@@ -606,6 +620,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         FW_TRACE(t, 6);
       }
       if (cg == 0 && ntot > 0) red_release_add(&cC[ntot - 1], (unsigned long long)nz);
+      }  // steps
       if (prm.residue && rmax > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(prm.residue),
                   (unsigned long long)__double_as_longlong(rmax));
@@ -645,36 +660,43 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       // ---- tile producer (one lane of an otherwise idle warp): Z[t] -> tile by TMA as soon as
       // the columns of term t are published and the consumers are done with tile t-1
       if (lane == 0) {
-        for (int t = 0; t < ntot; ++t) {
-          // term t's columns first (its latency overlaps the consumers' pass 0 of term t-1)
-          while (ld_acquire(&cC[t]) < (unsigned long long)h) {
+        const int gtot = prm.nsteps * ntot;
+        for (int gt = 0; gt < gtot; ++gt) {  // term index over the launch's steps
+          const int t = gt % ntot;
+          // term t's columns first (its latency overlaps the consumers' pass 0 of the previous term)
+          while (ld_acquire(&cC[t]) < (unsigned long long)(gt / ntot + 1) * h) {
           }
-          if (t > 0) {
-            mbar_wait(&tile_empty, (unsigned)(t - 1) & 1u);
-            // the CTA's rows of Z[t-1] are consumed (in shared memory / registers): the ring
-            // slot may be reused.  No release fence needed.
-            red_relaxed_add(&cR[t - 1], (unsigned long long)nr);
+          if (gt > 0) {
+            mbar_wait(&tile_empty, (unsigned)(gt - 1) & 1u);
+            // the CTA's rows of the previous term are consumed (in shared memory / registers):
+            // the ring slot may be reused.  No release fence needed.
+            red_relaxed_add(&cR[(gt - 1) % ntot], (unsigned long long)nr);
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy Z stores -> TMA reads
           if (!(prm.dbg & 4)) {
             mbar_expect_tx(&tile_full, (unsigned)(G::TILE_ELEMS * sizeof(double2)));
             for (int bx = 0; bx < h / 256; ++bx)
-              tma_load_3d(tile + (size_t)bx * 256 * 8, &zmap, 2 * r0, bx * 256, t % KRING, &tile_full);
+              tma_load_3d(tile + (size_t)bx * 256 * 8, &zmap, 2 * r0, bx * 256, gt % KRING, &tile_full);
           } else {
             mbar_arrive(&tile_full);
           }
         }
-        if (ntot > 0) {
-          mbar_wait(&tile_empty, (unsigned)(ntot - 1) & 1u);
+        if (gtot > 0) {
+          mbar_wait(&tile_empty, (unsigned)(gtot - 1) & 1u);
           red_relaxed_add(&cR[ntot - 1], (unsigned long long)nr);
         }
       }
     }
 
-    if (active) {
+    // this step's state buffers (multi-step launches rotate them with the level)
+    auto lvl_u = [&](int s, int d) -> double* { return prm.ub[(int)((prm.lvl0 + s + d) % 3)]; };
+    auto lvl_a = [&](int s, int d) -> double* { return prm.ab[(int)((prm.lvl0 + s + d) % 2)]; };
+#pragma unroll 1
+    for (int s = 0; active && s < prm.nsteps; ++s) {
+    {
       FW_TRACE(135, 0);
       // ---- F1: R2C of the row -> Y
-      const double2* u2 = reinterpret_cast<const double2*>(prm.u) + (size_t)row * h;
+      const double2* u2 = reinterpret_cast<const double2*>(prm.nsteps > 1 ? lvl_u(s, 0) : prm.u) + (size_t)row * h;
 #pragma unroll
       for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = u2[l + r * G::RT];
       pairbar(pair);
@@ -710,7 +732,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
     }
 
     // ---- R(t): h-point C2C of the pre-processed row + recombination
-    for (int t = 0; active && t < ntot; ++t) {
+    for (int t = 0; t < ntot; ++t) {
       const int op = t / nterms;
       const int m = prm.m_first + t % nterms;
       FW_TRACE(t, 0);
@@ -718,7 +740,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         const double2* d = dev_row(t + 1);
         if (d) prefetch_l2(d, J1 * sizeof(double));
       }
-      mbar_wait(&tile_full, (unsigned)t & 1u);
+      mbar_wait(&tile_full, (unsigned)(s * ntot + t) & 1u);
       FW_TRACE(t, 2);
       {  // pass 0 (p = 1): tile -> work (natural positions)
         double2 a[8];
@@ -792,20 +814,24 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
     }
 
     // ---- seismic update (seismic.cpp:116-129)
-    if (active && prm.seismic) {
+    if (prm.seismic) {
       bool bad = false;
       const double tau = prm.tau;
       const double t2 = tau * tau;
       const size_t rowoff = (size_t)row * J1;
-      const double2* cur = reinterpret_cast<const double2*>(prm.u + rowoff);
-      const double2* prev = reinterpret_cast<const double2*>(prm.prev + rowoff);
-      const double2* ap = reinterpret_cast<const double2*>(prm.ap + rowoff);
+      const bool ms = prm.nsteps > 1;
+      const double2* cur = reinterpret_cast<const double2*>((ms ? lvl_u(s, 0) : prm.u) + rowoff);
+      const double2* prev = reinterpret_cast<const double2*>((ms ? lvl_u(s, 2) : prm.prev) + rowoff);
+      const double2* ap = reinterpret_cast<const double2*>((ms ? lvl_a(s, 1) : prm.ap) + rowoff);
+      // a blow-up in an EARLIER step of this launch: keep the state the host restores
+      // (this step would overwrite the offending step's prev / L2prev)
+      const bool frozen = s > 0 && *reinterpret_cast<volatile int*>(prm.flag) < prm.step + s;
       const double2* l1 = reinterpret_cast<const double2*>(prm.out[0] + rowoff);
       const double2* c = reinterpret_cast<const double2*>(prm.c + rowoff);
       const double2* eta = reinterpret_cast<const double2*>(prm.eta + rowoff);
       const double2* tc = reinterpret_cast<const double2*>(prm.tc + rowoff);
-      double2* nx = reinterpret_cast<double2*>(prm.next + rowoff);
-      double2* l2o = reinterpret_cast<double2*>(prm.out[1] + rowoff);
+      double2* nx = reinterpret_cast<double2*>((ms ? lvl_u(s, 1) : prm.next) + rowoff);
+      double2* l2o = reinterpret_cast<double2*>((ms ? lvl_a(s, 0) : prm.out[1]) + rowoff);
 #pragma unroll 1
       for (int r = 0; r < 8; ++r) {
         unsigned v[4];
@@ -816,12 +842,15 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         const double c2x = cc.x * cc.x, c2y = cc.y * cc.y;
         const double nx0 = 2.0 * vc.x - vp.x + t2 * c2x * (ve.x * v1.x + vt.x * (l2x - va.x) / tau);
         const double nx1 = 2.0 * vc.y - vp.y + t2 * c2y * (ve.y * v1.y + vt.y * (l2y - va.y) / tau);
-        nx[q] = make_double2(nx0, nx1);
-        l2o[q] = make_double2(l2x, l2y);
+        if (!frozen) {
+          nx[q] = make_double2(nx0, nx1);
+          l2o[q] = make_double2(l2x, l2y);
+        }
         bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
       }
-      if (__any_sync(0xffffffffu, bad) && lane == 0 && !prm.dbg) atomicMin(prm.flag, prm.step);
+      if (__any_sync(0xffffffffu, bad) && lane == 0 && !prm.dbg) atomicMin(prm.flag, prm.step + s);
     }
+    }  // steps
   }
   // everyone is done with tensor memory: release it
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

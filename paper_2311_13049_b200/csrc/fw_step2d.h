@@ -29,8 +29,15 @@ struct Step2DParams {
   const double *prev, *ap, *c, *eta, *tc;
   double* next;
   double tau, thr;
-  int step;
+  int step;   // step number of the launch's first step (blow-up flag value)
   int* flag;
+  // multi-step seismic launches: nsteps steps, buffers rotating with the level L = lvl0 + s:
+  // cur = ub[L % 3], prev = ub[(L + 2) % 3], next = ub[(L + 1) % 3], ap = ab[(L + 1) % 2],
+  // new L2prev = ab[L % 2].  Applies and single steps use the plain pointers (nsteps = 1).
+  int nsteps;
+  double* ub[3];
+  double* ab[2];
+  long long lvl0;
   int dbg;  // timing experiments (FW_STEP2D_DBG), 0 in production
 };
 

@@ -1,4 +1,5 @@
-"""Run a few C2 steps with FW_TRACE=1 and print the per-warp phase timeline of CTA 0 / CTA 100
+"""(Needs a library built with FW_BUILD_TRACE=1 python -c "import __graft_entry__ as g; g.build_library(True)".)
+Run a few C2 steps with FW_TRACE=1 and print the per-warp phase timeline of CTA 0 / CTA 100
 of the persistent step kernel (fw_step2d.cu, FW_TRACE marks; 8 marks per warp and term).
 
 column warps: 0 term start | 1 weights + uhat loaded | 2 ring slot free | 3 pass 0 | 4 pass 1
