@@ -103,6 +103,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef FW_STEP2D_TRACE
 #define FW_STEP2D_TRACE 0
 #endif
+// timing experiments (build with -DFW_STEP2D_EXPERIMENTS=1, select with FW_STEP2D_DBG=bits; the
+// results are wrong by design): compiled out of the product kernel
+#ifndef FW_STEP2D_EXPERIMENTS
+#define FW_STEP2D_EXPERIMENTS 0
+#endif
+#define FW_DBG(bits) (FW_STEP2D_EXPERIMENTS && (prm.dbg & (bits)))
 #if FW_STEP2D_TRACE
 #define FW_TRACE(t, slot)                                                                              \
   do {                                                                                                 \
@@ -574,7 +580,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         {
           double wk[CR0];  // all weight loads in flight before the first use (one L2 latency)
 #pragma unroll
-          for (int r = 0; r < CR0; ++r) wk[r] = (mycol >= 0 && !(prm.dbg & 2)) ? __ldg(&w[r * CT0]) : 0.5;
+          for (int r = 0; r < CR0; ++r) wk[r] = (mycol >= 0 && !FW_DBG(2)) ? __ldg(&w[r * CT0]) : 0.5;
 #pragma unroll
           for (int c = 0; c < 4 * CR0; c += 32) {
             unsigned v[32];
@@ -592,8 +598,8 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         double2* Z = prm.T + (size_t)(gt % KRING) * J0 * h;
         // the previous term's Z columns are published once this term's pass 0 is done:
         // by then its stores have drained and the release fence is cheap
-        if (prm.dbg & 8) Z = prm.T + (size_t)(KRING - 1) * J0 * h;  // all terms into one slot
-        if (prm.dbg & 32) {  // timing experiment: columns skip the FFT
+        if (FW_DBG(8)) Z = prm.T + (size_t)(KRING - 1) * J0 * h;  // all terms into one slot
+        if (FW_DBG(32)) {  // timing experiment: columns skip the FFT
           gb();
           if (cg == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz);
           continue;
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
             red_relaxed_add(&cR[(gt - 1) % ntot], (unsigned long long)nr);
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy Z stores -> TMA reads
-          if (!(prm.dbg & 4)) {
+          if (!FW_DBG(4)) {
             mbar_expect_tx(&tile_full, (unsigned)(G::TILE_ELEMS * sizeof(double2)));
             for (int bx = 0; bx < h / 256; ++bx)
               tma_load_3d(tile + (size_t)bx * 256 * 8, &zmap, 2 * r0, bx * 256, gt % KRING, &tile_full);
@@ -753,7 +759,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty);  // this warp is done with tile t
       FW_TRACE(t, 4);
-      if (prm.dbg & 16) continue;  // timing experiment: rows do pass 0 only
+      if (FW_DBG(16)) continue;  // timing experiment: rows do pass 0 only
       pairbar(pair);
       {
         double2 a[8];
@@ -765,7 +771,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       }
       pairbar(pair);
       FW_TRACE(t, 5);
-      const double2* dv = (prm.dbg & 1) ? nullptr : dev_row(t);
+      const double2* dv = FW_DBG(1) ? nullptr : dev_row(t);
       {
         double2 a[8];
 #pragma unroll
@@ -848,7 +854,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         }
         bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
       }
-      if (__any_sync(0xffffffffu, bad) && lane == 0 && !prm.dbg) atomicMin(prm.flag, prm.step + s);
+      if (__any_sync(0xffffffffu, bad) && lane == 0 && !FW_DBG(-1)) atomicMin(prm.flag, prm.step + s);
     }
     }  // steps
   }
