@@ -92,6 +92,16 @@ __device__ __forceinline__ void setmaxnreg_inc() {
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ unsigned vtid() {
+  unsigned x;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(x));
+  return x;
+}
+__device__ __forceinline__ unsigned vctaid() {
+  unsigned x;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(x));
+  return x;
+}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -656,7 +666,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       return tile[l_ * 8 + (rs ^ (l_ & 7)) + r * 64 * 8];
     };
     // (s-s0)^m row of term t: global (streamed once), L2-prefetched one term ahead
-    auto dev_row = [&](int t) -> const double2* {
+    auto dev_row = [&](int t, int row) -> const double2* {
       const int op1 = t / nterms, m1 = prm.m_first + t % nterms;
       return m1 < 1 ? nullptr
                     : reinterpret_cast<const double2*>(prm.dev[op1] + (size_t)(m1 - 1) * J0 * J1 + (size_t)row * J1);
@@ -739,53 +749,60 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
 
     // ---- R(t): h-point C2C of the pre-processed row + recombination
     for (int t = 0; t < ntot; ++t) {
+      // per-thread constants re-derived from the special registers each term (volatile reads
+      // are not hoisted): cheaper than keeping them live, the row warps run at 64 registers
+      const int tidr = (int)vtid();
+      const int rw_ = (tidr >> 5) - 8, pair_ = rw_ >> 1, l_ = (rw_ & 1) * 32 + (tidr & 31);
+      const int row_ = (int)(((long long)vctaid() * J0) / nblk) + pair_;
+      double2* work_ = sm + G::OFF_RW + (size_t)pair_ * G::LROW;
+      const unsigned tacc_ = tmem_base + ((unsigned)(32 * ((tidr >> 5) & 3)) << 16) + 32u * (unsigned)(rw_ >> 2);
       const int op = t / nterms;
       const int m = prm.m_first + t % nterms;
       FW_TRACE(t, 0);
-      if (l == 0 && t + 1 < ntot) {  // the next term's (s-s0)^m row -> L2
-        const double2* d = dev_row(t + 1);
+      if (l_ == 0 && t + 1 < ntot) {  // the next term's (s-s0)^m row_ -> L2
+        const double2* d = dev_row(t + 1, row_);
         if (d) prefetch_l2(d, J1 * sizeof(double));
       }
       mbar_wait(&tile_full, (unsigned)(s * ntot + t) & 1u);
       FW_TRACE(t, 2);
-      {  // pass 0 (p = 1): tile -> work (natural positions)
+      {  // pass 0 (p = 1): tile -> work_ (natural positions)
         double2 a[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r] = tile_at(l, pair, r);
+        for (int r = 0; r < 8; ++r) a[r] = tile_at(l_, pair_, r);
         Dft<8, +1>::run(a);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = a[r];
+        for (int r = 0; r < 8; ++r) work_[G::rpad(l_) + r * G::RS0] = a[r];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty);  // this warp is done with tile t
       FW_TRACE(t, 4);
       if (FW_DBG(16)) continue;  // timing experiment: rows do pass 0 only
-      pairbar(pair);
+      pairbar(pair_);
       {
         double2 a[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r] = work[G::r_p1in(l) + r * G::RS1];
-        butterfly<h, 1, +1>(a, l, twr);
+        for (int r = 0; r < 8; ++r) a[r] = work_[G::r_p1in(l_) + r * G::RS1];
+        butterfly<h, 1, +1>(a, l_, twr);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) work[G::r_p1in(l) + r * G::RS1] = a[r];
+        for (int r = 0; r < 8; ++r) work_[G::r_p1in(l_) + r * G::RS1] = a[r];
       }
-      pairbar(pair);
+      pairbar(pair_);
       FW_TRACE(t, 5);
-      const double2* dv = FW_DBG(1) ? nullptr : dev_row(t);
+      const double2* dv = FW_DBG(1) ? nullptr : dev_row(t, row_);
       {
         double2 a[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l) + r * G::RS2];
-        butterfly<h, 2, +1>(a, l, twr);
+        for (int r = 0; r < 8; ++r) a[r] = work_[G::r_p2in(l_) + r * G::RS2];
+        butterfly<h, 2, +1>(a, l_, twr);
 #pragma unroll
         for (int qt = 0; qt < 4; ++qt) {
           double2 d[2];
           if (dv) {
 #pragma unroll
-            for (int r = 0; r < 2; ++r) d[r] = __ldcg(&dv[l + (2 * qt + r) * G::RT]);
+            for (int r = 0; r < 2; ++r) d[r] = __ldcg(&dv[l_ + (2 * qt + r) * G::RT]);
           }
           unsigned v[8];
-          tmem_ld8_nw(tacc + 8u * qt, v);
+          tmem_ld8_nw(tacc_ + 8u * qt, v);
           tmem_wait_ld();
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
@@ -800,22 +817,22 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
             tm_put(v, 2 * r, tm_d(v, 2 * r) + p0);
             tm_put(v, 2 * r + 1, tm_d(v, 2 * r + 1) + p1);
           }
-          tmem_st8_nw(tacc + 8u * qt, v);
+          tmem_st8_nw(tacc_ + 8u * qt, v);
         }
         tmem_wait_st();
       }
       FW_TRACE(t, 6);
-      pairbar(pair);  // pass-2 reads of the work buffer are done
+      pairbar(pair_);  // pass-2 reads of the work_ buffer are done
       FW_TRACE(t, 7);
       if (m == M && !(prm.seismic && op == prm.nops - 1)) {  // operator complete: hand over
-        double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)row * J1);
+        double2* o = reinterpret_cast<double2*>(prm.out[op] + (size_t)row_ * J1);
         unsigned v[32];
-        tmem_ld32(tacc, v);
+        tmem_ld32(tacc_, v);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) o[l + r * G::RT] = make_double2(tm_d(v, 2 * r), tm_d(v, 2 * r + 1));
+        for (int r = 0; r < 8; ++r) o[l_ + r * G::RT] = make_double2(tm_d(v, 2 * r), tm_d(v, 2 * r + 1));
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = 0u;
-        tmem_st32(tacc, v);
+        tmem_st32(tacc_, v);
       }
     }
 
