@@ -578,23 +578,36 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
 
       // ---- C(t): inverse columns -> pre-processed Z[gt % KRING] (gt = s ntot + t), column-major Z[k][k0]
       for (int t = 0; t < ntot; ++t) {
+        // per-thread constants re-derived from the special registers each term (volatile reads
+        // are not hoisted): fewer live registers across the FFT passes
+        const int tidc = (int)vtid();
+        const int g_ = tidc >> 7, cg_ = tidc & 127;
+        const int slot_ = (int)vctaid() + g_ * nblk;
+        const int i0_ = cg_ % CT0;
+        const int kA_ = slot_ == 0 ? 0 : slot_;
+        const int kB_ = slot_ == 0 ? h : (slot_ == h / 2 ? -1 : h - slot_);
+        const int mycol_ = (cg_ / CT0) ? kB_ : kA_;
+        const int nz_ = (kA_ < h) + (kB_ >= 0 && kB_ < h);
+        double2* work_ = sm + G::OFF_CW + (size_t)g_ * 2 * G::LCOL;
+        const unsigned tu_ = tmem_base + ((unsigned)(32 * ((tidc >> 5) & 3)) << 16) + (unsigned)(G::TM_U + g_ * 4 * CR0);
+        auto gb_ = [g_] { groupbar(g_); };
         FW_TRACE(t, 0);
         const int op = t / nterms, m = prm.m_first + t % nterms;
-        const double* w = prm.w[op] + ((size_t)m * prm.wcols + (mycol >= 0 ? mycol : 0)) * J0 + i0;
-        if (cg == 0 && t + 1 < ntot) {  // the next term's weights of both columns -> L2
+        const double* w = prm.w[op] + ((size_t)m * prm.wcols + (mycol_ >= 0 ? mycol_ : 0)) * J0 + i0_;
+        if (cg_ == 0 && t + 1 < ntot) {  // the next term's weights of both columns -> L2
           const int op1 = (t + 1) / nterms, m1 = prm.m_first + (t + 1) % nterms;
-          if (kA >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kA) * J0, J0 * sizeof(double));
-          if (kB >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kB) * J0, J0 * sizeof(double));
+          if (kA_ >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kA_) * J0, J0 * sizeof(double));
+          if (kB_ >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kB_) * J0, J0 * sizeof(double));
         }
         double2 a[CR0];
         {
           double wk[CR0];  // all weight loads in flight before the first use (one L2 latency)
 #pragma unroll
-          for (int r = 0; r < CR0; ++r) wk[r] = (mycol >= 0 && !FW_DBG(2)) ? __ldg(&w[r * CT0]) : 0.5;
+          for (int r = 0; r < CR0; ++r) wk[r] = (mycol_ >= 0 && !FW_DBG(2)) ? __ldg(&w[r * CT0]) : 0.5;
 #pragma unroll
           for (int c = 0; c < 4 * CR0; c += 32) {
             unsigned v[32];
-            tmem_ld32_nw(tu + c, v);
+            tmem_ld32_nw(tu_ + c, v);
             tmem_wait_ld();
 #pragma unroll
             for (int k = 0; k < 8; ++k)
@@ -610,29 +623,29 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         // by then its stores have drained and the release fence is cheap
         if (FW_DBG(8)) Z = prm.T + (size_t)(KRING - 1) * J0 * h;  // all terms into one slot
         if (FW_DBG(32)) {  // timing experiment: columns skip the FFT
-          gb();
-          if (cg == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz);
+          gb_();
+          if (cg_ == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz_);
           continue;
         }
-        column_pair<G, +1>(work, twc, cg, a, gb, [&] {
-          if (cg == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz);
+        column_pair<G, +1>(work_, twc, cg_, a, gb_, [&] {
+          if (cg_ == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz_);
         }, [&](int i, const double2* xa, const double2* xb) {
 #pragma unroll
           for (int r = 0; r < G::CR2; ++r) {
             const int k0 = i + r * G::CT2;
-            if (kA == 0) {  // Z_0 from X_0 and X_h (member 1 = column h has no Z of its own)
+            if (kA_ == 0) {  // Z_0 from X_0 and X_h (member 1 = column h has no Z of its own)
               if (prm.residue) rmax = fmax(rmax, fabs(xa[r].y) + fabs(xb[r].y));
               __stcg(&Z[k0], pre_c2r(xa[r], xb[r], true, twp[0]));
-            } else if (kA == h / 2) {
-              __stcg(&Z[(size_t)kA * J0 + k0], pre_c2r(xa[r], xa[r], false, twp[kA]));
+            } else if (kA_ == h / 2) {
+              __stcg(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xa[r], false, twp[kA_]));
             } else {
-              __stcg(&Z[(size_t)kA * J0 + k0], pre_c2r(xa[r], xb[r], false, twp[kA]));
-              __stcg(&Z[(size_t)kB * J0 + k0], pre_c2r(xb[r], xa[r], false, twp[kB]));
+              __stcg(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xb[r], false, twp[kA_]));
+              __stcg(&Z[(size_t)kB_ * J0 + k0], pre_c2r(xb[r], xa[r], false, twp[kB_]));
             }
           }
         }, [&](int sl) { FW_TRACE(t, sl); });
         FW_TRACE(t, 5);
-        gb();  // work buffers free again; all Z stores of the group issued
+        gb_();  // work_ buffers free again; all Z stores of the group issued
         FW_TRACE(t, 6);
       }
       if (cg == 0 && ntot > 0) red_release_add(&cC[ntot - 1], (unsigned long long)nz);
