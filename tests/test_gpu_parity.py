@@ -457,3 +457,29 @@ def test_register_row_c2r_equal_shared_memory_path(J):
         a, ra = op_a.apply(u, m_first, residue=True)
         b, rb = op_b.apply(u, m_first, residue=True)
         assert np.array_equal(a, b) and ra == rb
+
+
+@pytest.mark.parametrize("J", [(1024, 1024), (512, 1024)])
+def test_persistent_multistep_blowup_state(J):
+    """A blow-up in the middle of a multi-step persistent launch: the later steps of the
+    launch must not overwrite the state the host restores (same offending step and
+    pre-step state as the multi-pass path, which matches the reference)."""
+    m = fw()
+    lo, hi = (-16.0, -16.0), (16.0, 16.0)
+    g = grid_of(J, lo, hi)
+    phi = np.exp(-(np.linspace(-16, 16, J[0], endpoint=False)[:, None] ** 2
+                   + np.linspace(-16, 16, J[1], endpoint=False)[None, :] ** 2) / 0.5)
+    gamma = np.full(J, 0.05)
+    tau = 0.08  # far beyond stability: |u| explodes within a few dozen steps
+    med = m.build_medium(g, gamma, np.ones(J), 1.0, 4)
+    st_p = m.SeismicStepper(med, phi, np.zeros(J), tau)
+    st_g = m.SeismicStepper(med, phi, np.zeros(J), tau, ctx=generic_context())
+    with pytest.raises(m.BlowupDetected):
+        st_g.advance(400)
+    with pytest.raises(m.BlowupDetected):
+        st_p.advance(400)  # one launch of 400 steps
+    ref = st_g.state()
+    got = st_p.state()
+    assert got[3] == ref[3] and 2 < got[3] < 400  # blew up inside the launch, steps left after it
+    for a, b in zip(got[:3], ref[:3]):
+        assert np.array_equal(a, b)
