@@ -89,6 +89,39 @@ __device__ __forceinline__ void setmaxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
 }
 // bulk prefetch of [p, p + bytes) into L2 (bytes multiple of 16)
+// L2 residency: the streamed tables (weights, deviation powers) are read once per step and
+// marked evict-first, the term ring Z (re-read a term later, rewritten 6 terms later)
+// evict-last, so that most of the ring is overwritten in L2 instead of written back.
+__device__ __forceinline__ unsigned long long pol_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long pol_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_stream(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream2(const double2* p, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(double2* p, double2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_hint(const void* p, unsigned bytes, unsigned long long pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -596,14 +629,16 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         const double* w = prm.w[op] + ((size_t)m * prm.wcols + (mycol_ >= 0 ? mycol_ : 0)) * J0 + i0_;
         if (cg_ == 0 && t + 1 < ntot) {  // the next term's weights of both columns -> L2
           const int op1 = (t + 1) / nterms, m1 = prm.m_first + (t + 1) % nterms;
-          if (kA_ >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kA_) * J0, J0 * sizeof(double));
-          if (kB_ >= 0) prefetch_l2(prm.w[op1] + ((size_t)m1 * prm.wcols + kB_) * J0, J0 * sizeof(double));
+          const unsigned long long pf = pol_evict_first();
+          if (kA_ >= 0) prefetch_l2_hint(prm.w[op1] + ((size_t)m1 * prm.wcols + kA_) * J0, J0 * sizeof(double), pf);
+          if (kB_ >= 0) prefetch_l2_hint(prm.w[op1] + ((size_t)m1 * prm.wcols + kB_) * J0, J0 * sizeof(double), pf);
         }
         double2 a[CR0];
         {
           double wk[CR0];  // all weight loads in flight before the first use (one L2 latency)
 #pragma unroll
-          for (int r = 0; r < CR0; ++r) wk[r] = (mycol_ >= 0 && !FW_DBG(2)) ? __ldg(&w[r * CT0]) : 0.5;
+          for (int r = 0; r < CR0; ++r)
+            wk[r] = (mycol_ >= 0 && !FW_DBG(2)) ? ld_stream(&w[r * CT0], pol_evict_first()) : 0.5;
 #pragma unroll
           for (int c = 0; c < 4 * CR0; c += 32) {
             unsigned v[32];
@@ -635,12 +670,12 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
             const int k0 = i + r * G::CT2;
             if (kA_ == 0) {  // Z_0 from X_0 and X_h (member 1 = column h has no Z of its own)
               if (prm.residue) rmax = fmax(rmax, fabs(xa[r].y) + fabs(xb[r].y));
-              __stcg(&Z[k0], pre_c2r(xa[r], xb[r], true, twp[0]));
+              st_keep(&Z[k0], pre_c2r(xa[r], xb[r], true, twp[0]), pol_evict_last());
             } else if (kA_ == h / 2) {
-              __stcg(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xa[r], false, twp[kA_]));
+              st_keep(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xa[r], false, twp[kA_]), pol_evict_last());
             } else {
-              __stcg(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xb[r], false, twp[kA_]));
-              __stcg(&Z[(size_t)kB_ * J0 + k0], pre_c2r(xb[r], xa[r], false, twp[kB_]));
+              st_keep(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xb[r], false, twp[kA_]), pol_evict_last());
+              st_keep(&Z[(size_t)kB_ * J0 + k0], pre_c2r(xb[r], xa[r], false, twp[kB_]), pol_evict_last());
             }
           }
         }, [&](int sl) { FW_TRACE(t, sl); });
@@ -774,7 +809,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       FW_TRACE(t, 0);
       if (l_ == 0 && t + 1 < ntot) {  // the next term's (s-s0)^m row_ -> L2
         const double2* d = dev_row(t + 1, row_);
-        if (d) prefetch_l2(d, J1 * sizeof(double));
+        if (d) prefetch_l2_hint(d, J1 * sizeof(double), pol_evict_first());
       }
       mbar_wait(&tile_full, (unsigned)(s * ntot + t) & 1u);
       FW_TRACE(t, 2);
@@ -812,7 +847,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           double2 d[2];
           if (dv) {
 #pragma unroll
-            for (int r = 0; r < 2; ++r) d[r] = __ldcg(&dv[l_ + (2 * qt + r) * G::RT]);
+            for (int r = 0; r < 2; ++r) d[r] = ld_stream2(&dv[l_ + (2 * qt + r) * G::RT], pol_evict_first());
           }
           unsigned v[8];
           tmem_ld8_nw(tacc_ + 8u * qt, v);
