@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
                    help="c2 (default): fused seismic step; c3/c4: slab-decomposed 3D apply; c5: batched 2D sweep")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--transpose", default="fused", choices=["fused", "nccl"],
+                   help="c3/c4: slab transposes fused into the C2C stages (peer stores) or NCCL all-to-all")
     return p.parse_args()
 
 
@@ -181,12 +183,14 @@ def run_reference_arm(args):
 
 def run_slab(args, cfg_fn, name):
     """configs[2]/[3]: slab-decomposed 3D apply of the dispersion operator over N ranks
-    (strong scaling: the global grid is fixed); one NCCL all-to-all forward + one batched
-    all-to-all backward per apply."""
+    (strong scaling: the global grid is fixed).  Transposes: fused into the C2C stages
+    (each rank's last FFT pass stores into the owning rank's buffer through CUDA IPC /
+    NVLink, default) or one NCCL all-to-all forward + one batched all-to-all backward."""
     import torch
 
     import paper_2311_13049_b200 as fw
-    from paper_2311_13049_b200.slab import SlabGeometry, slab_apply_device
+    from paper_2311_13049_b200.slab import (DeviceStages, FusedSlabApply, IpcPeers, LocalPeers, SlabGeometry,
+                                            slab_apply_device)
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -201,6 +205,14 @@ def run_slab(args, cfg_fn, name):
     geo = SlabGeometry(cfg.J, world, rank)
     u = torch.from_numpy(np.ascontiguousarray(cfg.phi[geo.rows])).cuda()
     stream = torch.cuda.ExternalStream(ctx.stream)
+    if args.transpose == "fused":
+        st = DeviceStages(ctx)
+        wl, dl, ml = st.local_tables(op, geo)
+        peers = (IpcPeers if world > 1 else LocalPeers)(geo, cfg.M + 1, ctx)
+        fused = FusedSlabApply(geo, st, peers, wl, dl, ml)
+
+        def slab_apply_device(op_, u_, geo_, ctx_):  # noqa: F811 (same call shape as the NCCL path)
+            return fused.apply(u_)
     for _ in range(args.warmup):
         slab_apply_device(op, u, geo, ctx)
     ctx.sync()
@@ -247,6 +259,8 @@ def run_slab(args, cfg_fn, name):
                 "config": {"workload": f"{name}: slab-decomposed apply of order 1+gamma "
                                        f"({'x'.join(map(str, cfg.J))}, M={cfg.M}); one step = one apply",
                            "grid": list(cfg.J), "M": cfg.M, "parallelism": f"slab P={world} (axis 0)",
+                           "transpose": ("fused into the C2C stages (peer stores)" if args.transpose == "fused"
+                                         else "NCCL all_to_all_single"),
                            "l2": "working set > 126 MB L2; no flush"},
                 "roofline": {"bound": "hbm", "achieved": B / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                              "frac": B / (ms * 1e-3) / 1e9 / hbm, "traffic": None,

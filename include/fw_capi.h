@@ -167,13 +167,30 @@ int fw_irfftn(fw_ctx ctx, int dim, const int* J, const double* H_host, double* x
  *                      the source element-wise; x scale when != 1
  *   fw_stage_c2r_accum per row: out = sum_{m=m_first}^{m_last} (s-s0)^m .* C2R(src_m),
  *                      ascending m, (s-s0)^m regenerated from dev1 = s - s0
- *   fw_op_device_tables  the operator's resident tables: w[(M+1)][N_half], dev1[N] */
+ *   fw_op_device_tables  the operator's resident tables: w[(M+1)][N_half], dev1[N]
+ *   fw_stage_c2c_scatter  fw_stage_c2c with the slab transpose FUSED into its last pass:
+ *                      output element j of line (o, in) of term t goes to
+ *                      dst_q[j / blk][t*tstride + (j % blk)*jstride + o*ostride + in + base]
+ *                      (complex elements), i.e. straight into the destination ranks'
+ *                      receive buffers (peer memory mapped on this device: NVLink stores),
+ *                      no separate all-to-all; nq <= 8, axis length 256 / 512 / 1024
+ *                      (else FW_E_UNSUPPORTED).  Replaces the copy + all-to-all the
+ *                      reference's FFTW path has no equivalent of (grid.cpp:134-137 is serial). */
 int fw_stage_r2c(fw_ctx ctx, int dim, const int* J, const double* x_dev, double* H_dev, double scale);
 int fw_stage_c2c(fw_ctx ctx, int dim, const int* J, int axis, int dir, const double* src_dev, double* dst_dev,
                  const double* w_dev, long long src_ts, long long dst_ts, long long w_ts, int nterms, double scale);
 int fw_stage_c2r_accum(fw_ctx ctx, int dim, const int* J, const double* src_dev, long long src_ts, int m_first,
                        int m_last, const double* dev1_dev, double* out_dev, double* residue_dev);
 int fw_op_device_tables(fw_op op, const double** w_dev, const double** dev1_dev, int* m_last);
+/* CUDA IPC helpers for the fused-transpose slab path (one process per GPU of a node):
+ * export a device allocation, map a peer's allocation into this device's address space */
+int fw_ipc_handle(const void* dev_ptr, unsigned char handle_out[64]);
+int fw_ipc_open(const unsigned char handle[64], void** dev_ptr_out);
+int fw_ipc_close(void* dev_ptr);
+int fw_stage_c2c_scatter(fw_ctx ctx, int dim, const int* J, int axis, int dir, const double* src_dev,
+                         const double* w_dev, long long src_ts, long long w_ts, int nterms, double scale, int nq,
+                         double* const* dst_q, long long blk, long long jstride, long long ostride,
+                         long long tstride, long long base);
 
 #ifdef __cplusplus
 }

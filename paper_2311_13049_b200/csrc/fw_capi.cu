@@ -1126,6 +1126,62 @@ int fw_stage_c2c(fw_ctx ctx, int dim, const int* J, int axis, int dir, const dou
   return FW_OK;
 }
 
+int fw_ipc_handle(const void* dev_ptr, unsigned char handle_out[64]) {
+  if (!dev_ptr || !handle_out) return set_err(FW_E_ARG, "null argument");
+  cudaIpcMemHandle_t h;
+  FW_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+  memcpy(handle_out, &h, 64);
+  return FW_OK;
+}
+
+int fw_ipc_open(const unsigned char handle[64], void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return set_err(FW_E_ARG, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  FW_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return FW_OK;
+}
+
+int fw_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return set_err(FW_E_ARG, "null argument");
+  FW_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return FW_OK;
+}
+
+int fw_stage_c2c_scatter(fw_ctx ctx, int dim, const int* J, int axis, int dir, const double* src_dev,
+                         const double* w_dev, long long src_ts, long long w_ts, int nterms, double scale, int nq,
+                         double* const* dst_q, long long blk, long long jstride, long long ostride,
+                         long long tstride, long long base) {
+  if (!ctx || !src_dev || !dst_q || nterms < 1 || nq < 1 || nq > fw::kMaxScatter || blk < 1)
+    return set_err(FW_E_ARG, "bad argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
+  if (axis < 0 || axis > dim - 2) return set_err(FW_E_ARG, "axis must be < dim-1 (the last axis is the halved one)");
+  const int n = g.J[axis];
+  if ((long long)nq * blk < n) return set_err(FW_E_ARG, "nq * blk must cover the axis");
+  fw::Scatter sc{};
+  for (int q = 0; q < nq; ++q) {
+    if (!dst_q[q]) return set_err(FW_E_ARG, "null destination");
+    sc.dst[q] = reinterpret_cast<double2*>(dst_q[q]);
+  }
+  sc.nq = nq;
+  sc.blk = blk;
+  sc.jstride = jstride;
+  sc.ostride = ostride;
+  sc.tstride = tstride;
+  sc.base = base;
+  long long S = g.hp1;
+  for (int b = axis + 1; b <= g.d - 2; ++b) S *= g.J[b];
+  long long outer = 1;
+  for (int b = 0; b < axis; ++b) outer *= g.J[b];
+  if (!fw::launch_lines(ctx->L(), n, dir < 0 ? -1 : +1, (const double2*)src_dev, nullptr, w_dev, S, outer, S, src_ts,
+                        0, w_ts, nterms, 1, scale, scale != 1.0, nullptr, &sc))
+    return set_err(FW_E_UNSUPPORTED, "fused transpose: axis length must be 256, 512 or 1024");
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
 int fw_stage_c2r_accum(fw_ctx ctx, int dim, const int* J, const double* src_dev, long long src_ts, int m_first,
                        int m_last, const double* dev1_dev, double* out_dev, double* residue_dev) {
   if (!ctx || !src_dev || !out_dev || m_last < m_first) return set_err(FW_E_ARG, "bad argument");

@@ -93,10 +93,21 @@ void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const Ba
 void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_first, int m_last,
                           const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2);
 
+// fused transpose: the last pass of a line C2C writes output element j of line (o, in), term t
+// to dst[q] + t tstride + (j - q blk) jstride + o ostride + in + base, q = j / blk -- the
+// destination ranks' buffers (peer memory over NVLink), or local buffers (nq = 1 / tests)
+constexpr int kMaxScatter = 8;
+struct Scatter {
+  double2* dst[kMaxScatter];
+  long long blk, jstride, ostride, tstride, base;
+  int nq;
+};
+
 // register-resident line FFTs (fw_lines.cu) for n in {256, 512, 1024}; false = not served
 bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double2* dst, const double* w,
                   long long S, long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts,
-                  int nterms, int nfields, double sc, bool scale, const BatchLine* bl);
+                  int nterms, int nfields, double sc, bool scale, const BatchLine* bl,
+                  const Scatter* scatter = nullptr);
 
 // register-resident row C2R + ascending-m recombination (fw_lines.cu) for nl in {256, 512, 1024}
 bool launch_rows_c2r(const LaunchCtx& L, int nl, const double2* src, long long src_ts, int m_first, int m_last,

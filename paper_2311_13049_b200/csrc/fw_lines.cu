@@ -68,12 +68,12 @@ __device__ __forceinline__ void bfly(double2* a, int i, const double2* __restric
 
 // C2C of lines of length N along an axis of stride S (line (o, in): o*N*S + in + j*S).
 // blockIdx.y = term (src/dst/w advance by their term strides), blockIdx.z = field (bl).
-template <int N, int DIR>
+template <int N, int DIR, bool SCAT>
 __global__ void __launch_bounds__(256) k_lines(const double2* __restrict__ src, double2* __restrict__ dst,
                                                const double* __restrict__ w, long long S, long long inner,
                                                long long src_ts, long long dst_ts, long long w_ts, double sc,
                                                int do_scale, const double2* __restrict__ master,
-                                               const BatchLine* __restrict__ bl) {
+                                               const BatchLine* __restrict__ bl, const Scatter scat) {
   using PL = Plan<N>;
   constexpr int L = PL::L;
   extern __shared__ double2 sm[];  // L lines x LS
@@ -143,7 +143,14 @@ __global__ void __launch_bounds__(256) k_lines(const double2* __restrict__ src, 
             v.x *= sc;
             v.y *= sc;
           }
-          dst[base + (long long)(i + r * T) * S] = v;
+          const int j = i + r * T;
+          if constexpr (SCAT) {  // fused transpose: straight into the destination rank's buffer
+            const int q = (int)(j / scat.blk);
+            scat.dst[q][term * scat.tstride + (j - q * scat.blk) * scat.jstride + o * scat.ostride + in0 + l +
+                        scat.base] = v;
+          } else {
+            dst[base + (long long)j * S] = v;
+          }
         }
       }
     }
@@ -153,23 +160,37 @@ __global__ void __launch_bounds__(256) k_lines(const double2* __restrict__ src, 
 template <int N>
 bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
               long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
-              int nfields, double sc, bool scale, const BatchLine* bl) {
+              int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
   constexpr int LPB = Plan<N>::L;
   constexpr size_t SMEM = (size_t)LPB * Plan<N>::LS * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_lines<N, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(k_lines<N, +1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, +1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     attr = true;
   }
   const long long bpo = (inner + LPB - 1) / LPB;
   const dim3 grid((unsigned)(outer * bpo), (unsigned)nterms, (unsigned)nfields);
-  if (dir < 0)
-    k_lines<N, -1><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, scale ? 1 : 0,
-                                                   L.master, bl);
-  else
-    k_lines<N, +1><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, scale ? 1 : 0,
-                                                   L.master, bl);
+  const Scatter none{};
+  const Scatter& sc_ = scatter ? *scatter : none;
+  const int f = scale ? 1 : 0;
+  if (dir < 0) {
+    if (scatter)
+      k_lines<N, -1, true><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
+                                                           bl, sc_);
+    else
+      k_lines<N, -1, false><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
+                                                            L.master, bl, sc_);
+  } else {
+    if (scatter)
+      k_lines<N, +1, true><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
+                                                           bl, sc_);
+    else
+      k_lines<N, +1, false><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
+                                                            L.master, bl, sc_);
+  }
   if (L.launches) *L.launches += 1;
   return true;
 }
@@ -330,17 +351,17 @@ bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m
 
 bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double2* dst, const double* w,
                   long long S, long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts,
-                  int nterms, int nfields, double sc, bool scale, const BatchLine* bl) {
+                  int nterms, int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
   switch (n) {
     case 256:
       return lines::launch_n<256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
-                                  scale, bl);
+                                  scale, bl, scatter);
     case 512:
       return lines::launch_n<512>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
-                                  scale, bl);
+                                  scale, bl, scatter);
     case 1024:
       return lines::launch_n<1024>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
-                                   scale, bl);
+                                   scale, bl, scatter);
     default:
       return false;
   }

@@ -184,6 +184,23 @@ class DeviceStages:
                                          nh * src_ts, nh, nh * w_ts, nterms, scale))
         return dst
 
+    def c2c_scatter(self, src, shape, axis, dir, dst_ptrs, blk, jstride, ostride, tstride, base, w=None, nterms=1,
+                    src_ts=0, w_ts=0, scale=1.0):
+        """C2C along `axis` with the transpose fused into its last pass: output element j of
+        line (o, in), term t -> dst_ptrs[j // blk][t*tstride + (j % blk)*jstride + o*ostride + in + base]
+        (complex elements).  dst_ptrs: device addresses (peer memory or local)."""
+        lib = self.lib
+        h = shape[2] // 2 + 1
+        nh = shape[0] * shape[1] * h
+        P = C.c_void_p * len(dst_ptrs)
+        lib.fw_stage_c2c_scatter.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_void_p,
+                                             C.c_void_p, C.c_longlong, C.c_longlong, C.c_int, C.c_double, C.c_int,
+                                             C.POINTER(C.c_void_p)] + [C.c_longlong] * 5
+        self.check(lib.fw_stage_c2c_scatter(self.ctx.handle, 3, self._J(shape), axis, dir, src.data_ptr(),
+                                            w.data_ptr() if w is not None else None, nh * src_ts, nh * w_ts, nterms,
+                                            scale, len(dst_ptrs), P(*[C.c_void_p(int(x)) for x in dst_ptrs]),
+                                            blk, jstride, ostride, tstride, base))
+
     def c2r(self, src, shape, m_first, m_last, dev1):
         out = self.empty(shape, complex_=False)
         nh = shape[0] * shape[1] * (shape[2] // 2 + 1)
@@ -207,6 +224,136 @@ class DeviceStages:
             wl = wt[:, :, geo.cols, :].contiguous()
             dl = dt[geo.rows].contiguous()
         return wl, dl, ml.value
+
+
+class FusedSlabApply:
+    """Slab apply with both transposes FUSED into the C2C stages (fw_stage_c2c_scatter):
+    the last pass of the local axis-1 C2C stores each output straight into the owning
+    rank's [J0][J1/P][H] spectrum buffer, and the last pass of the all-terms axis-0 inverse
+    stores into the owning rank's [nt][J0/P][J1][H] buffer -- peer memory over NVLink on a
+    multi-GPU node, so the transpose overlaps the FFT instead of following it as a separate
+    all-to-all.  Between the two halves of each transpose the ranks only synchronise
+    (``peers.barrier()``: every rank's stores are complete).
+
+    peers: ``T_ptrs`` / ``Ts_ptrs`` (device addresses of every rank's receive buffers, valid
+    on this device), ``T(rank)`` / ``Ts(rank)`` (this rank's buffers as tensors), ``barrier()``.
+    """
+
+    def __init__(self, geo: SlabGeometry, stages, peers, w_local, dev1_local, m_last: int):
+        self.g, self.st, self.peers = geo, stages, peers
+        self.w, self.dev1, self.m_last = w_local, dev1_local, m_last
+
+    # the three phases (separated by peers.barrier(); a single-process test interleaves the
+    # phases of several virtual ranks)
+    def phase_forward(self, u_slab):
+        g, st, pe = self.g, self.st, self.peers
+        J0, J1, J2 = g.J
+        loc = (g.J0l, J1, J2)
+        Y = st.r2c(u_slab, loc)  # R2C (axis 2), then C2C (axis 1) + transpose into every rank's T
+        st.c2c_scatter(Y, loc, 1, -1, pe.T_ptrs, blk=g.J1l, jstride=g.H, ostride=g.J1l * g.H, tstride=0,
+                       base=g.rank * g.J0l * g.J1l * g.H)
+
+    def phase_inverse(self, m_first: int = 0):
+        g, st, pe = self.g, self.st, self.peers
+        J0, J1, J2 = g.J
+        tshape = (J0, g.J1l, J2)
+        uhat = st.c2c(pe.T(g.rank), tshape, axis=0, dir=-1, scale=1.0 / g.N)
+        nt = self.m_last - m_first + 1
+        # all terms: axis-0 C2C (x w_m) + transpose into every rank's Ts[nt][J0l][J1][H]
+        st.c2c_scatter(uhat, tshape, 0, +1, pe.Ts_ptrs, blk=g.J0l, jstride=J1 * g.H, ostride=0,
+                       tstride=g.J0l * J1 * g.H, base=g.rank * g.J1l * g.H, w=self.w[m_first:], nterms=nt,
+                       src_ts=0, w_ts=1)
+
+    def phase_finish(self, m_first: int = 0):
+        g, st, pe = self.g, self.st, self.peers
+        loc = (g.J0l, g.J[1], g.J[2])
+        nt = self.m_last - m_first + 1
+        Ts = st.c2c(pe.Ts(g.rank), loc, axis=1, dir=+1, nterms=nt, src_ts=1)
+        return st.c2r(Ts, loc, m_first, self.m_last, self.dev1)
+
+    def apply(self, u_slab, m_first: int = 0):
+        if m_first > self.m_last:  # perturbation of a constant order: exact zeros (flap.cpp:163-166)
+            return u_slab * 0.0
+        self.phase_forward(u_slab)
+        self.peers.barrier()
+        self.phase_inverse(m_first)
+        self.peers.barrier()
+        return self.phase_finish(m_first)
+
+
+class LocalPeers:
+    """Receive buffers of P virtual ranks on ONE device (tests / single-GPU use of the fused
+    path): the pointer tables address local tensors; barrier() is a stream sync."""
+
+    def __init__(self, geo: SlabGeometry, nt_max: int, ctx):
+        import torch
+
+        J0, J1, _ = geo.J
+        self.ctx = ctx
+        self._T = [torch.empty((J0, geo.J1l, geo.H), dtype=torch.complex128, device="cuda") for _ in range(geo.P)]
+        self._Ts = [torch.empty((nt_max, geo.J0l, J1, geo.H), dtype=torch.complex128, device="cuda")
+                    for _ in range(geo.P)]
+        self.T_ptrs = [t.data_ptr() for t in self._T]
+        self.Ts_ptrs = [t.data_ptr() for t in self._Ts]
+
+    def T(self, r):
+        return self._T[r]
+
+    def Ts(self, r):
+        return self._Ts[r]
+
+    def barrier(self):
+        self.ctx.sync()
+
+
+class IpcPeers(LocalPeers):
+    """Receive buffers of the P ranks of a torch.distributed job on one node: each rank
+    allocates its own, exports CUDA IPC handles, and maps the others' (peer memory over
+    NVLink); barrier() = device sync + process-group barrier."""
+
+    def __init__(self, geo: SlabGeometry, nt_max: int, ctx):
+        import torch
+        import torch.distributed as dist
+
+        J0, J1, _ = geo.J
+        self.ctx, self.dist = ctx, dist
+        self._mine_T = torch.empty((J0, geo.J1l, geo.H), dtype=torch.complex128, device="cuda")
+        self._mine_Ts = torch.empty((nt_max, geo.J0l, J1, geo.H), dtype=torch.complex128, device="cuda")
+        from . import _capi
+
+        lib, check = _capi.load_library(), _capi.check
+        lib.fw_ipc_handle.argtypes = [C.c_void_p, C.c_char_p]
+        lib.fw_ipc_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        handles = []
+        for t in (self._mine_T, self._mine_Ts):
+            hbuf = C.create_string_buffer(64)
+            check(lib.fw_ipc_handle(C.c_void_p(t.data_ptr()), hbuf))
+            handles.append(hbuf.raw)
+        allh = [None] * geo.P
+        dist.all_gather_object(allh, handles)
+        self.T_ptrs, self.Ts_ptrs = [], []
+        for r, (hT, hTs) in enumerate(allh):
+            if r == geo.rank:
+                self.T_ptrs.append(self._mine_T.data_ptr())
+                self.Ts_ptrs.append(self._mine_Ts.data_ptr())
+                continue
+            for hnd, lst in ((hT, self.T_ptrs), (hTs, self.Ts_ptrs)):
+                p = C.c_void_p()
+                check(lib.fw_ipc_open(C.create_string_buffer(hnd, 64), C.byref(p)))
+                lst.append(p.value)
+        self.rank = geo.rank
+
+    def T(self, r):
+        assert r == self.rank
+        return self._mine_T
+
+    def Ts(self, r):
+        assert r == self.rank
+        return self._mine_Ts
+
+    def barrier(self):
+        self.ctx.sync()
+        self.dist.barrier()
 
 
 class TorchComm:

@@ -483,3 +483,40 @@ def test_persistent_multistep_blowup_state(J):
     assert got[3] == ref[3] and 2 < got[3] < 400  # blew up inside the launch, steps left after it
     for a, b in zip(got[:3], ref[:3]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("P,J", [(2, (256, 256, 32)), (4, (512, 256, 16)), (2, (256, 1024, 8))])
+def test_fused_transpose_slab_equals_single_gpu_apply(P, J):
+    """Slab decomposition with both transposes fused into the C2C stages
+    (fw_stage_c2c_scatter): P virtual ranks on one device, their phases interleaved by the
+    host (no kernel waits on another rank); the gathered result is the single-GPU apply's bits."""
+    import torch
+
+    m = fw()
+    from paper_2311_13049_b200.slab import DeviceStages, FusedSlabApply, LocalPeers, SlabGeometry
+
+    lo, hi = tuple(-3.0 for _ in J), tuple(3.0 for _ in J)
+    g = grid_of(J, lo, hi)
+    rng = np.random.default_rng(P * 1000 + J[0])
+    s = 0.8 + 0.4 * rng.random(J)
+    u = rng.standard_normal(J)
+    M = 6
+    op = m.build_expansion(m.OrderField(g, s), M)
+    st = DeviceStages(op.ctx)
+    peers = LocalPeers(SlabGeometry(J, P, 0), M + 1, op.ctx)
+    for m_first in (0, 1):
+        ranks = []
+        for r in range(P):
+            geo = SlabGeometry(J, P, r)
+            wl, dl, ml = st.local_tables(op, geo)
+            ranks.append((geo, FusedSlabApply(geo, st, peers, wl, dl, ml)))
+        for geo, fa in ranks:
+            fa.phase_forward(torch.from_numpy(np.ascontiguousarray(u[geo.rows])).cuda())
+        peers.barrier()
+        for geo, fa in ranks:
+            fa.phase_inverse(m_first)
+        peers.barrier()
+        parts = [fa.phase_finish(m_first) for geo, fa in ranks]
+        op.ctx.sync()
+        got = np.concatenate([p.cpu().numpy() for p in parts])
+        assert np.array_equal(got, op.apply(u, m_first))
