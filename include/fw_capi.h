@@ -182,6 +182,21 @@ int fw_stage_c2c(fw_ctx ctx, int dim, const int* J, int axis, int dir, const dou
 int fw_stage_c2r_accum(fw_ctx ctx, int dim, const int* J, const double* src_dev, long long src_ts, int m_first,
                        int m_last, const double* dev1_dev, double* out_dev, double* residue_dev);
 int fw_op_device_tables(fw_op op, const double** w_dev, const double** dev1_dev, int* m_last);
+/* distributed seismic stepper pieces (slab.SlabSeismicStepper), element-wise on a slab:
+ *   fw_medium_coefficients  host: c, eta, tau_c from gamma, c0 (derive_medium, seismic.cpp:30-39; glibc
+ *                           pow/cos/sin exactly as the reference), FW_E_GAMMA_RANGE outside [0, 0.5)
+ *   fw_stage_seis_start     cur = phi + tau psi + tau^2/2 c^2 (eta L1phi + tau_c L2psi)   (seismic.cpp:100-106)
+ *   fw_stage_seis_update    next = 2 cur - prev + tau^2 c^2 (eta L1 + tau_c (L2 - L2prev)/tau)
+ *                           (seismic.cpp:116-122); *flag_dev = min(*flag_dev, step) when
+ *                           |next| > thr somewhere (the blow-up check of seismic.cpp:124-129) */
+int fw_medium_coefficients(long long n, const double* gamma, const double* c0, double omega0, double* c_out,
+                           double* eta_out, double* tau_coef_out);
+int fw_stage_seis_start(fw_ctx ctx, long long n, double tau, const double* phi, const double* psi, const double* c,
+                        const double* eta, const double* tau_coef, const double* l1phi, const double* l2psi,
+                        double* cur);
+int fw_stage_seis_update(fw_ctx ctx, long long n, double tau, const double* cur, const double* prev,
+                         const double* l2prev, const double* l1, const double* l2, const double* c, const double* eta,
+                         const double* tau_coef, double* next, double thr, int step, int* flag_dev);
 /* CUDA IPC helpers for the fused-transpose slab path (one process per GPU of a node):
  * export a device allocation, map a peer's allocation into this device's address space */
 int fw_ipc_handle(const void* dev_ptr, unsigned char handle_out[64]);

@@ -153,7 +153,8 @@ def check(rc: int) -> None:
 EXPORTED_SYMBOLS = [
     "fw_last_error", "fw_version", "fw_ctx_create", "fw_ctx_destroy", "fw_ctx_sync", "fw_ctx_stream",
     "fw_ctx_launches", "fw_ctx_trace", "fw_op_create", "fw_op_create_from_tables", "fw_op_destroy", "fw_op_info",
-    "fw_apply", "fw_apply_device", "fw_apply_batch_device", "fw_stage_c2c_scatter", "fw_ipc_handle", "fw_ipc_open", "fw_ipc_close", "fw_seis_create", "fw_seis_destroy",
+    "fw_apply", "fw_apply_device", "fw_apply_batch_device", "fw_stage_c2c_scatter", "fw_ipc_handle", "fw_ipc_open", "fw_ipc_close",
+    "fw_medium_coefficients", "fw_stage_seis_start", "fw_stage_seis_update", "fw_seis_create", "fw_seis_destroy",
     "fw_seis_step", "fw_seis_enqueue", "fw_seis_get", "fw_seis_set_current",
     "fw_seis_current_device", "fw_seis_ops", "fw_seis_medium", "fw_tsfp2_create",
     "fw_tsfp2_destroy", "fw_tsfp2_step", "fw_tsfp2_get", "fw_rfftn", "fw_irfftn",

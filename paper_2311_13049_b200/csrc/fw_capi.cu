@@ -1126,6 +1126,47 @@ int fw_stage_c2c(fw_ctx ctx, int dim, const int* J, int axis, int dir, const dou
   return FW_OK;
 }
 
+int fw_medium_coefficients(long long n, const double* gamma, const double* c0, double omega0, double* c_out,
+                           double* eta_out, double* tau_coef_out) {
+  if (n < 0 || !gamma || !c0 || !c_out || !eta_out || !tau_coef_out) return set_err(FW_E_ARG, "null argument");
+  for (long long j = 0; j < n; ++j)  // seismic.cpp:14-19
+    if (!(gamma[j] >= 0.0) || !(gamma[j] < 0.5)) {
+      char b[128];
+      snprintf(b, sizeof b, "gamma = %f outside [0, 0.5)", gamma[j]);
+      return set_err(FW_E_GAMMA_RANGE, b);
+    }
+  for (long long j = 0; j < n; ++j) {  // seismic.cpp:30-39 (the same expressions as fw_seis_create)
+    const double gj = gamma[j];
+    const double cg = c0[j];
+    const double scale = pow(cg, 2.0 * gj) * pow(omega0, -2.0 * gj);
+    c_out[j] = cg * cos(0.5 * M_PI * gj);
+    eta_out[j] = -scale * cos(M_PI * gj);
+    tau_coef_out[j] = -(scale / cg) * sin(M_PI * gj);
+  }
+  return FW_OK;
+}
+
+int fw_stage_seis_start(fw_ctx ctx, long long n, double tau, const double* phi, const double* psi, const double* c,
+                        const double* eta, const double* tau_coef, const double* l1phi, const double* l2psi,
+                        double* cur) {
+  if (!ctx || n < 0 || !phi || !psi || !c || !eta || !tau_coef || !l1phi || !l2psi || !cur)
+    return set_err(FW_E_ARG, "null argument");
+  fw::launch_seis_start(ctx->L(), (size_t)n, tau, phi, psi, c, eta, tau_coef, l1phi, l2psi, cur);
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+int fw_stage_seis_update(fw_ctx ctx, long long n, double tau, const double* cur, const double* prev,
+                         const double* l2prev, const double* l1, const double* l2, const double* c, const double* eta,
+                         const double* tau_coef, double* next, double thr, int step, int* flag_dev) {
+  if (!ctx || n < 0 || !cur || !prev || !l2prev || !l1 || !l2 || !c || !eta || !tau_coef || !next || !flag_dev)
+    return set_err(FW_E_ARG, "null argument");
+  fw::launch_seis_update(ctx->L(), (size_t)n, tau, cur, prev, l2prev, l1, l2, c, eta, tau_coef, next, thr, step,
+                         flag_dev);
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
 int fw_ipc_handle(const void* dev_ptr, unsigned char handle_out[64]) {
   if (!dev_ptr || !handle_out) return set_err(FW_E_ARG, "null argument");
   cudaIpcMemHandle_t h;

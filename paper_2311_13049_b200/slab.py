@@ -253,11 +253,17 @@ class FusedSlabApply:
         st.c2c_scatter(Y, loc, 1, -1, pe.T_ptrs, blk=g.J1l, jstride=g.H, ostride=g.J1l * g.H, tstride=0,
                        base=g.rank * g.J0l * g.J1l * g.H)
 
-    def phase_inverse(self, m_first: int = 0):
+    def forward_spectrum(self):
+        """This rank's columns of the forward spectrum (after phase_forward and a barrier)."""
+        g, st, pe = self.g, self.st, self.peers
+        return st.c2c(pe.T(g.rank), (g.J[0], g.J1l, g.J[2]), axis=0, dir=-1, scale=1.0 / g.N)
+
+    def phase_inverse(self, m_first: int = 0, uhat=None):
         g, st, pe = self.g, self.st, self.peers
         J0, J1, J2 = g.J
         tshape = (J0, g.J1l, J2)
-        uhat = st.c2c(pe.T(g.rank), tshape, axis=0, dir=-1, scale=1.0 / g.N)
+        if uhat is None:
+            uhat = self.forward_spectrum()
         nt = self.m_last - m_first + 1
         # all terms: axis-0 C2C (x w_m) + transpose into every rank's Ts[nt][J0l][J1][H]
         st.c2c_scatter(uhat, tshape, 0, +1, pe.Ts_ptrs, blk=g.J0l, jstride=J1 * g.H, ostride=0,
@@ -279,6 +285,125 @@ class FusedSlabApply:
         self.phase_inverse(m_first)
         self.peers.barrier()
         return self.phase_finish(m_first)
+
+
+class SlabSeismicStepper:
+    """``SeismicStepper`` (seismic.hpp:36-46, seismic.cpp:85-142) on a slab-decomposed 3D
+    grid: every rank owns planes [r J0/P, (r+1) J0/P) of the wavefields.  Per step one
+    forward transform (fused transpose) shared by the two operators (orders 1+gamma and
+    1/2+gamma), their all-terms inverses (fused transposes into per-operator buffers), and
+    the fused update; the blow-up flag is combined over the ranks every step, and on a
+    blow-up every rank keeps its pre-step state (reference semantics).
+
+    grid: the global ``Grid``; gamma, c0, phi, psi: global numpy fields (every rank passes the
+    same arrays; only its slab is uploaded); peers_factory(op_index, geo, nt_max, ctx) -> peers
+    (IpcPeers across processes; shared LocalPeers for virtual ranks in one process).
+    With construct=False the caller runs the constructor's three applies itself and calls
+    start() (tests interleave virtual ranks that way)."""
+
+    def __init__(self, grid, gamma, c0, omega0, M, phi, psi, tau, geo: SlabGeometry, ctx, peers_factory,
+                 blowup_factor: float = 1e8, flag_reduce=None, construct: bool = True):
+        import torch
+
+        from . import api
+        from ._capi import check, load_library
+
+        self.torch, self.lib, self.check = torch, load_library(), check
+        self.g, self.ctx, self.tau = geo, ctx, float(tau)
+        rows = geo.rows
+        J = tuple(geo.J)
+        gamma, c0, phi, psi = (np.array(np.broadcast_to(np.asarray(a, dtype=np.float64), J))
+                               for a in (gamma, c0, phi, psi))
+        # medium coefficients of this slab (derive_medium, glibc, as the single-GPU stepper)
+        self.nloc = n = geo.J0l * J[1] * J[2]
+        co, eta, tc = (np.empty(n) for _ in range(3))
+        lib = self.lib
+        dp = C.POINTER(C.c_double)
+        lib.fw_medium_coefficients.argtypes = [C.c_longlong, dp, dp, C.c_double, dp, dp, dp]
+        g_loc, c0_loc = np.ascontiguousarray(gamma[rows]), np.ascontiguousarray(c0[rows])
+        check(lib.fw_medium_coefficients(n, g_loc.ctypes.data_as(dp), c0_loc.ctypes.data_as(dp), float(omega0),
+                                         co.ctypes.data_as(dp), eta.ctypes.data_as(dp), tc.ctypes.data_as(dp)))
+        self._dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        self.c, self.eta, self.tc = self._dev(co), self._dev(eta), self._dev(tc)
+        # the two operators (full tables on every rank, sliced to the slab)
+        self.stages = DeviceStages(ctx)
+        self.ops = [api.build_expansion(api.OrderField(grid, 1.0 + gamma), M, ctx=ctx),
+                    api.build_expansion(api.OrderField(grid, 0.5 + gamma), M, ctx=ctx)]
+        self.apps = []
+        for k, op in enumerate(self.ops):
+            wl, dl, ml = self.stages.local_tables(op, geo)
+            self.apps.append(FusedSlabApply(geo, self.stages, peers_factory(k, geo, ml + 1, ctx), wl, dl, ml))
+        self.peers = self.apps[0].peers
+        self.flag = torch.full((1,), 0x7FFFFFFF, dtype=torch.int32, device="cuda")
+        self.flag_reduce = flag_reduce
+        self.thr = blowup_factor * max(float(np.max(np.abs(phi))), 1e-300)  # seismic.cpp:93
+        lib.fw_stage_seis_start.argtypes = [C.c_void_p, C.c_longlong, C.c_double] + [C.c_void_p] * 8
+        lib.fw_stage_seis_update.argtypes = ([C.c_void_p, C.c_longlong, C.c_double] + [C.c_void_p] * 9
+                                             + [C.c_double, C.c_int, C.c_void_p])
+        self.phi_l, self.psi_l = self._dev(phi[rows]), self._dev(psi[rows])
+        if construct:  # seismic.cpp:85-109 (one process per rank)
+            self.start(self.apps[0].apply(self.phi_l), self.apps[1].apply(self.psi_l), self.apps[1].apply(self.phi_l))
+
+    def start(self, l1phi, l2psi, l2phi):
+        """cur = phi + tau psi + tau^2/2 c^2 (eta L1phi + tau_c L2psi), prev = phi, L2prev = L2phi, n = 1."""
+        cur = self.torch.empty_like(self.phi_l)
+        self.check(self.lib.fw_stage_seis_start(self.ctx.handle, self.nloc, self.tau, self.phi_l.data_ptr(),
+                                                self.psi_l.data_ptr(), self.c.data_ptr(), self.eta.data_ptr(),
+                                                self.tc.data_ptr(), l1phi.data_ptr(), l2psi.data_ptr(),
+                                                cur.data_ptr()))
+        self.prev, self.cur, self.l2prev, self.n = self.phi_l, cur, l2phi, 1
+
+    # ---- one step in three phases (peers.barrier() between them; step() does it all) ----
+    def phase_forward(self):
+        self.apps[0].phase_forward(self.cur)  # shared forward transform (into operator 0's buffers)
+
+    def phase_inverse(self):
+        uhat = self.apps[0].forward_spectrum()
+        self.apps[0].phase_inverse(0, uhat)
+        self.apps[1].phase_inverse(0, uhat)
+
+    def phase_update(self):
+        l1, l2 = self.apps[0].phase_finish(0), self.apps[1].phase_finish(0)
+        self._next = self.torch.empty_like(self.cur)
+        self._l2 = l2
+        self.check(self.lib.fw_stage_seis_update(self.ctx.handle, self.nloc, self.tau, self.cur.data_ptr(),
+                                                 self.prev.data_ptr(), self.l2prev.data_ptr(), l1.data_ptr(),
+                                                 l2.data_ptr(), self.c.data_ptr(), self.eta.data_ptr(),
+                                                 self.tc.data_ptr(), self._next.data_ptr(), self.thr, self.n + 1,
+                                                 self.flag.data_ptr()))
+
+    def blown(self):
+        """The offending step over all ranks (flag_reduce = a min all-reduce), or None."""
+        f = self.flag.clone()
+        if self.flag_reduce is not None:
+            f = self.flag_reduce(f)
+        v = int(f.item())
+        return None if v == 0x7FFFFFFF else v
+
+    def commit(self):
+        self.prev, self.cur, self.l2prev = self.cur, self._next, self._l2
+        self.n += 1
+
+    def step(self):
+        from ._capi import BlowupDetected
+
+        self.phase_forward()
+        self.peers.barrier()
+        self.phase_inverse()
+        self.peers.barrier()
+        self.phase_update()
+        bad = self.blown()
+        if bad is not None:  # the state stays the pre-step one (seismic.cpp:124-129)
+            raise BlowupDetected(f"sup|u| > {self.thr:g} at step {bad}")
+        self.commit()
+
+    def advance(self, steps: int):
+        for _ in range(int(steps)):
+            self.step()
+
+    def state(self):
+        """(cur, prev, L2prev) of this rank's slab (torch CUDA tensors) and n."""
+        return self.cur, self.prev, self.l2prev, self.n
 
 
 class LocalPeers:

@@ -520,3 +520,70 @@ def test_fused_transpose_slab_equals_single_gpu_apply(P, J):
         op.ctx.sync()
         got = np.concatenate([p.cpu().numpy() for p in parts])
         assert np.array_equal(got, op.apply(u, m_first))
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_slab_seismic_stepper_equals_single_gpu(P):
+    """The slab-decomposed SeismicStepper (fused transposes, shared forward transform, fused
+    update) with P virtual ranks on one device (phases interleaved by the host): cur, prev,
+    L2prev and n identical to the single-GPU SeismicStepper after 5 steps."""
+    import torch
+
+    m = fw()
+    from paper_2311_13049_b200.slab import LocalPeers, SlabGeometry, SlabSeismicStepper
+
+    # the fused transposes need axis lengths 256/512/1024 for the two transposed axes
+    J, lo, hi = (256, 256, 8), (-4.0, -4.0, -1.0), (4.0, 4.0, 1.0)
+    x = [lo[a] + (hi[a] - lo[a]) * np.arange(J[a]) / J[a] for a in range(3)]
+    X, Y, Z = np.meshgrid(*x, indexing="ij")
+    gamma = 0.02 + 0.015 * np.sin(X) * np.cos(0.5 * Y)
+    phi = np.exp(-(X**2 + Y**2 + Z**2) / 0.5)
+
+    class Cfg:
+        pass
+
+    cfg = Cfg()
+    cfg.gamma, cfg.c0, cfg.omega0, cfg.phi, cfg.psi, cfg.tau = gamma, np.ones(J), 1.0, phi, np.zeros(J), 1e-3
+    g = m.Grid(list(zip(lo, hi)), list(J))
+    ref = m.SeismicStepper(m.build_medium(g, cfg.gamma, cfg.c0, cfg.omega0, 6), cfg.phi, cfg.psi, cfg.tau)
+    ref.advance(5)
+    ctx = m.default_context()
+    shared = {}
+
+    def peers_factory(k, geo, nt, ctx_):
+        if k not in shared:
+            shared[k] = LocalPeers(SlabGeometry(J, P, 0), nt, ctx_)
+        return shared[k]
+
+    sts = [SlabSeismicStepper(g, cfg.gamma, cfg.c0, cfg.omega0, 6, cfg.phi, cfg.psi, cfg.tau, SlabGeometry(J, P, r),
+                              ctx, peers_factory, construct=False) for r in range(P)]
+    # constructor applies, phase by phase over the virtual ranks
+    outs = {}
+    for key, k, field in (("l1phi", 0, "phi_l"), ("l2psi", 1, "psi_l"), ("l2phi", 1, "phi_l")):
+        for st in sts:
+            st.apps[k].phase_forward(getattr(st, field))
+        ctx.sync()
+        for st in sts:
+            st.apps[k].phase_inverse(0)
+        ctx.sync()
+        outs[key] = [st.apps[k].phase_finish(0) for st in sts]
+    for r, st in enumerate(sts):
+        st.start(outs["l1phi"][r], outs["l2psi"][r], outs["l2phi"][r])
+    for _ in range(5):
+        for st in sts:
+            st.phase_forward()
+        ctx.sync()
+        for st in sts:
+            st.phase_inverse()
+        ctx.sync()
+        for st in sts:
+            st.phase_update()
+        assert all(st.blown() is None for st in sts)
+        for st in sts:
+            st.commit()
+    ctx.sync()
+    cur_r, prev_r, ap_r, n_r = ref.state()
+    got = [np.concatenate([st.state()[i].cpu().numpy() for st in sts]) for i in range(3)]
+    assert sts[0].n == n_r
+    for a, b in zip(got, (cur_r, prev_r, ap_r)):
+        assert np.array_equal(a, b)
