@@ -109,6 +109,9 @@ bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double
                   int nterms, int nfields, double sc, bool scale, const BatchLine* bl,
                   const Scatter* scatter = nullptr);
 
+// register-resident row R2C (fw_lines.cu) for nl in {256, 512, 1024}
+bool launch_rows_r2c(const LaunchCtx& L, int nl, const double* u, double2* Uh, long long rows, int nfields,
+                     double sc, bool scale, const BatchLine* bl);
 // register-resident row C2R + ascending-m recombination (fw_lines.cu) for nl in {256, 512, 1024}
 bool launch_rows_c2r(const LaunchCtx& L, int nl, const double2* src, long long src_ts, int m_first, int m_last,
                      const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,

@@ -368,13 +368,16 @@ void init_kernels() {
 void launch_forward(const LaunchCtx& L, const GridGeom& g, const double* u, double2* Uh, bool scale) {
   const double inv = 1.0 / (double)g.N;
   const int h = g.nl / 2;
-  const int lpb = std::max(1, std::min(8, 2048 / h));
-  const size_t sm = smem_bytes(h + 1, lpb);
-  allow_smem(k_r2c_rows, sm);
-  const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
-  k_r2c_rows<<<nb, kThreads, sm, L.stream>>>(u, Uh, g.nl, (long long)g.rows, lpb, inv,
-                                             (scale && g.d == 1) ? 1 : 0, L.master, nullptr);
-  count(L);
+  if (L.generic_lines ||
+      !launch_rows_r2c(L, g.nl, u, Uh, (long long)g.rows, 1, inv, scale && g.d == 1, nullptr)) {
+    const int lpb = std::max(1, std::min(8, 2048 / h));
+    const size_t sm = smem_bytes(h + 1, lpb);
+    allow_smem(k_r2c_rows, sm);
+    const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
+    k_r2c_rows<<<nb, kThreads, sm, L.stream>>>(u, Uh, g.nl, (long long)g.rows, lpb, inv,
+                                               (scale && g.d == 1) ? 1 : 0, L.master, nullptr);
+    count(L);
+  }
   for (int a = g.d - 2; a >= 0; --a)
     c2c_axis(L, g, a, -1, Uh, Uh, nullptr, 0, 0, 0, 1, inv, scale && a == 0);
 }
@@ -472,6 +475,7 @@ namespace fw {
 // single-device pipeline, applied to a local sub-array
 void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, double2* H, double scale,
                       bool do_scale) {
+  if (!L.generic_lines && launch_rows_r2c(L, g.nl, u, H, (long long)g.rows, 1, scale, do_scale, nullptr)) return;
   const int h = g.nl / 2;
   const int lpb = std::max(1, std::min(8, 2048 / h));
   const size_t sm = smem_bytes(h + 1, lpb);
@@ -494,12 +498,15 @@ void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const Ba
                           const BatchLine* tab_c2c, bool scale) {
   const double inv = 1.0 / (double)g.N;
   const int h = g.nl / 2;
-  const int lpb = std::max(1, std::min(8, 2048 / h));
-  const size_t sm = smem_bytes(h + 1, lpb);
-  const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
-  k_r2c_rows<<<dim3(nb, 1, F), kThreads, sm, L.stream>>>(nullptr, nullptr, g.nl, (long long)g.rows, lpb, inv,
-                                                         (scale && g.d == 1) ? 1 : 0, L.master, tab_r2c);
-  count(L);
+  if (L.generic_lines ||
+      !launch_rows_r2c(L, g.nl, nullptr, nullptr, (long long)g.rows, F, inv, scale && g.d == 1, tab_r2c)) {
+    const int lpb = std::max(1, std::min(8, 2048 / h));
+    const size_t sm = smem_bytes(h + 1, lpb);
+    const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
+    k_r2c_rows<<<dim3(nb, 1, F), kThreads, sm, L.stream>>>(nullptr, nullptr, g.nl, (long long)g.rows, lpb, inv,
+                                                           (scale && g.d == 1) ? 1 : 0, L.master, tab_r2c);
+    count(L);
+  }
   for (int a = g.d - 2; a >= 0; --a) {
     const int n = g.J[a];
     long long S = g.hp1;

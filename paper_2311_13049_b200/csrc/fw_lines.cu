@@ -330,6 +330,95 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
     atomicMax(reinterpret_cast<unsigned long long*>(residue), (unsigned long long)__double_as_longlong(rmax));
 }
 
+// Per row of the last axis: R2C of NL = 2H reals (z_j = x_2j + i x_2j+1, H-point C2C,
+// split X_k = f(Z_k, Z_{H-k})) into H+1 bins, x scale when do_scale.  Same plan/threads as
+// k_rows_c2r; pass 0 reads the row straight from global memory.
+template <int H>
+__global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, double2* __restrict__ Uh,
+                                                  long long rows, double sc, int do_scale,
+                                                  const double2* __restrict__ master,
+                                                  const BatchLine* __restrict__ bl) {
+  using RP = RowPlan<H>;
+  using PL = Plan<H>;
+  constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL;
+  if (bl) {
+    u = static_cast<const double*>(bl[blockIdx.z].src);
+    Uh = static_cast<double2*>(bl[blockIdx.z].dst);
+  }
+  extern __shared__ double2 sm[];
+  const int rl = threadIdx.x / TM, i = threadIdx.x % TM;
+  const long long row = (long long)blockIdx.x * RPB + rl;
+  const bool live = row < rows;
+  double2* Wk = sm + rl * PL::LS;  // FFT work, then the natural-order result
+  const double2* z = reinterpret_cast<const double2*>(u) + row * H;
+  {  // pass 0 straight from global
+    constexpr int R = PL::R0, T = PL::T0;
+    if (i < T) {
+      double2 a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = live ? z[i + r * T] : make_double2(0.0, 0.0);
+      Dft<R, -1>::run(a);
+#pragma unroll
+      for (int r = 0; r < R; ++r) Wk[PL::p0out(i * R + r)] = a[r];
+    }
+  }
+  __syncthreads();
+  if constexpr (PL::P == 3) {
+    constexpr int R = PL::R1, T = PL::T1;
+    if (i < T) {
+      double2 a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = Wk[PL::p1(i, r)];
+      bfly<H, 1, -1>(a, i, master);
+#pragma unroll
+      for (int r = 0; r < R; ++r) Wk[PL::p1(i, r)] = a[r];
+    }
+    __syncthreads();
+  }
+  {
+    constexpr int LAST = PL::P - 1;
+    double2 a[RL];
+    if (i < TL) {
+#pragma unroll
+      for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * TL)];
+      bfly<H, LAST, -1>(a, i, master);
+    }
+    __syncthreads();  // every read of the work layout is done: store the natural-order result
+    if (i < TL) {
+#pragma unroll
+      for (int r = 0; r < RL; ++r) Wk[i + r * TL] = a[r];
+    }
+  }
+  __syncthreads();
+  if (live) {
+    double2* X = Uh + row * (H + 1);
+    for (int k = i; k <= H; k += TM) {
+      double2 v = r2c_post(Wk, k, H, master);
+      if (do_scale) {
+        v.x *= sc;
+        v.y *= sc;
+      }
+      X[k] = v;
+    }
+  }
+}
+
+template <int H>
+bool launch_rows_r2c_t(const LaunchCtx& L, const double* u, double2* Uh, long long rows, int nfields, double sc,
+                       bool scale, const BatchLine* bl) {
+  using RP = RowPlan<H>;
+  constexpr size_t SMEM = (size_t)RP::RPB * Plan<H>::LS * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rows_r2c<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    attr = true;
+  }
+  const dim3 grid((unsigned)((rows + RP::RPB - 1) / RP::RPB), 1, (unsigned)nfields);
+  k_rows_r2c<H><<<grid, RP::NT, SMEM, L.stream>>>(u, Uh, rows, sc, scale ? 1 : 0, L.master, bl);
+  if (L.launches) *L.launches += 1;
+  return true;
+}
+
 template <int H>
 bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m_first, int m_last,
                  const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
@@ -362,6 +451,20 @@ bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double
     case 1024:
       return lines::launch_n<1024>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
                                    scale, bl, scatter);
+    default:
+      return false;
+  }
+}
+
+bool launch_rows_r2c(const LaunchCtx& L, int nl, const double* u, double2* Uh, long long rows, int nfields,
+                     double sc, bool scale, const BatchLine* bl) {
+  switch (nl / 2) {
+    case 128:
+      return lines::launch_rows_r2c_t<128>(L, u, Uh, rows, nfields, sc, scale, bl);
+    case 256:
+      return lines::launch_rows_r2c_t<256>(L, u, Uh, rows, nfields, sc, scale, bl);
+    case 512:
+      return lines::launch_rows_r2c_t<512>(L, u, Uh, rows, nfields, sc, scale, bl);
     default:
       return false;
   }
