@@ -9,7 +9,8 @@ LIB_NAME = "libfw_b200.so"
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "lib", LIB_NAME)
+    # FW_LIBRARY: an alternative build of the same library (A/B timing of kernel variants)
+    return os.environ.get("FW_LIBRARY") or os.path.join(_HERE, "lib", LIB_NAME)
 
 
 # ---- errors: one class per fwave::Error subtype the path raises (errors.hpp:10-60)

@@ -289,7 +289,7 @@ int fw_ctx_create(int device, fw_ctx* out) {
   FW_CUDA(cudaMemset(c->counters, 0, 2 * (size_t)fw::kStep2dCStride * sizeof(unsigned long long)));
   const char* tr = getenv("FW_TRACE");
   if (tr && tr[0] == '1') {
-    const size_t n = 2 * 32 * 136 * 8;
+    const size_t n = 2 * 32 * 136 * 8 + 2 * 160 * 2 * 136;  // + per-CTA column-group term ends
     if (dalloc(&c->trace, n) == FW_OK) cudaMemset(c->trace, 0, n * sizeof(unsigned long long));
   }
   fw::init_kernels();
@@ -320,11 +320,13 @@ int fw_ctx_sync(fw_ctx c) {
 
 void* fw_ctx_stream(fw_ctx c) { return c ? (void*)c->stream : nullptr; }
 
-/* diagnostics: copy the persistent-kernel trace (2 x 32 x 136 x 8 u64) to host; FW_E_ARG if tracing is off */
+/* diagnostics: copy the persistent-kernel trace (2 x 32 x 136 x 8 + 2 x 160 x 2 x 136 u64) to host; FW_E_ARG if
+   tracing is off */
 int fw_ctx_trace(fw_ctx c, unsigned long long* out) {
   if (!c || !c->trace || !out) return set_err(FW_E_ARG, "tracing disabled (set FW_TRACE=1 before fw_ctx_create)");
   FW_CUDA(cudaStreamSynchronize(c->stream));
-  FW_CUDA(cudaMemcpy(out, c->trace, 2 * 32 * 136 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  FW_CUDA(cudaMemcpy(out, c->trace, (2 * 32 * 136 * 8 + 2 * 160 * 2 * 136) * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost));
   return FW_OK;
 }
 long long fw_ctx_launches(fw_ctx c) { return c ? c->launches : 0; }

@@ -653,6 +653,10 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         const int gt = s * ntot + t;  // term index over the launch
         if (gt >= KRING) warp_wait(&cR[(gt - KRING) % ntot], (unsigned long long)((gt - KRING) / ntot + 1) * J0);
         FW_TRACE(t, 2);
+#if FW_STEP2D_TRACE
+        if (prm.trace && cg_ == 0 && vctaid() < 160)
+          prm.trace[2 * 32 * 136 * 8 + 160 * 2 * 136 + ((size_t)vctaid() * 2 + g_) * 136 + t] = gtimer();
+#endif
         double2* Z = prm.T + (size_t)(gt % KRING) * J0 * h;
         // the previous term's Z columns are published once this term's pass 0 is done:
         // by then its stores have drained and the release fence is cheap
@@ -682,6 +686,10 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         FW_TRACE(t, 5);
         gb_();  // work_ buffers free again; all Z stores of the group issued
         FW_TRACE(t, 6);
+#if FW_STEP2D_TRACE
+        if (prm.trace && cg_ == 0 && vctaid() < 160)
+          prm.trace[2 * 32 * 136 * 8 + ((size_t)vctaid() * 2 + g_) * 136 + t] = gtimer();
+#endif
       }
       if (cg == 0 && ntot > 0) red_release_add(&cC[ntot - 1], (unsigned long long)nz);
       }  // steps
@@ -728,10 +736,13 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         for (int gt = 0; gt < gtot; ++gt) {  // term index over the launch's steps
           const int t = gt % ntot;
           // term t's columns first (its latency overlaps the consumers' pass 0 of the previous term)
+          FW_TRACE(t, 0);
           while (ld_acquire(&cC[t]) < (unsigned long long)(gt / ntot + 1) * h) {
           }
+          FW_TRACE(t, 1);
           if (gt > 0) {
             mbar_wait(&tile_empty, (unsigned)(gt - 1) & 1u);
+            FW_TRACE(t, 2);
             // the CTA's rows of the previous term are consumed (in shared memory / registers):
             // the ring slot may be reused.  No release fence needed.
             red_relaxed_add(&cR[(gt - 1) % ntot], (unsigned long long)nr);
@@ -741,6 +752,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
             mbar_expect_tx(&tile_full, (unsigned)(G::TILE_ELEMS * sizeof(double2)));
             for (int bx = 0; bx < h / 256; ++bx)
               tma_load_3d(tile + (size_t)bx * 256 * 8, &zmap, 2 * r0, bx * 256, gt % KRING, &tile_full);
+            FW_TRACE(t, 3);
           } else {
             mbar_arrive(&tile_full);
           }

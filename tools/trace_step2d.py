@@ -25,9 +25,11 @@ st = fw.SeismicStepper(fw.build_medium(g, cfg.gamma, cfg.c0, 1.0, cfg.M), cfg.ph
 st.advance(6)
 lib = fw.load_library()
 lib.fw_ctx_trace.argtypes = [C.c_void_p, C.c_void_p]
-buf = np.zeros(2 * 32 * 136 * 8, dtype=np.uint64)
+buf = np.zeros(2 * 32 * 136 * 8 + 2 * 160 * 2 * 136, dtype=np.uint64)
 fw._capi.check(lib.fw_ctx_trace(ctx.handle, buf.ctypes.data))
-tr = buf.reshape(2, 32, 136, 8).astype(np.int64)
+tr = buf[:2 * 32 * 136 * 8].reshape(2, 32, 136, 8).astype(np.int64)
+colend = buf[2 * 32 * 136 * 8:2 * 32 * 136 * 8 + 160 * 2 * 136].reshape(160, 2, 136).astype(np.int64)
+colgo = buf[2 * 32 * 136 * 8 + 160 * 2 * 136:].reshape(160, 2, 136).astype(np.int64)  # after the ring wait
 ntot = 34
 t0 = tr[:, :24][tr[:, :24] > 0].min()
 COL = ["w+uhat", "ring", "pass0", "pass1", "pass2+Z", "gbar"]
@@ -56,7 +58,7 @@ for sel in range(2):
               + f" | start {d[0, 0]:6.1f} end {d[ntot - 1, nm - 1]:6.1f}")
 
 # launch marks: warp slot 31, [step % 64][entry, exit] (CTA 0)
-lm = buf.reshape(2, 32, 136 * 8)[0, 31, :128].reshape(64, 2).astype(np.int64)
+lm = buf[:2 * 32 * 136 * 8].reshape(2, 32, 136 * 8)[0, 31, :128].reshape(64, 2).astype(np.int64)
 ok = np.nonzero(lm[:, 0] > 0)[0]
 if len(ok):
     print("launch marks (CTA 0, us): step: entry -> exit (duration), gap from previous exit")
@@ -72,7 +74,51 @@ if len(ok):
 # rows [0] F1 start, [1] F1 signalled
 for sel in range(2):
     c = (tr[sel, 0, 135, :3] - t0) / 1000.0
-    r = (tr[sel, 8, 135, :2] - t0) / 1000.0
+    r = (tr[sel, 8, 135, :7] - t0) / 1000.0
+    lt = (tr[sel, 8, ntot - 1, :8] - t0) / 1000.0
     f = (tr[sel, 0, 0, 0] - t0) / 1000.0
     print(f"CTA {0 if sel == 0 else 100}: rows F1 {r[0]:.1f} -> {r[1]:.1f} us; columns wait F1 {c[0]:.1f} -> {c[1]:.1f},"
           f" F2 done {c[2]:.1f}, first term starts {f:.1f} us (t0 = earliest mark)")
+    print(f"  rows' last term: start {lt[0]:.1f}, tile {lt[2]:.1f}, pass 2 done {lt[6]:.1f}, pairbar {lt[7]:.1f};"
+          f" update start {r[6]:.1f} flag read {r[3]:.1f} iter0 {r[4]:.1f} iter3 {r[5]:.1f} done {r[2]:.1f} us")
+
+# producer (warp 22 lane 0): [0] loop top, [1] cC[t] complete, [2] tile_empty(t-1), [3] TMA issued;
+# consumers (warp 8): [0] term start, [2] tile landed; columns (warp 0): [6] term done
+for sel in range(2):
+    P = (tr[sel, 22, :ntot, :4] - t0) / 1000.0
+    R = (tr[sel, 8, :ntot, :8] - t0) / 1000.0
+    Cw = (tr[sel, 0, :ntot, :8] - t0) / 1000.0
+    print(f"CTA {0 if sel == 0 else 100}: t | cols done | cC ready | empty(t-1) | TMA issue | landed | row wants")
+    for t in range(1, ntot):
+        print(f"  {t:2d} | {Cw[t, 6]:7.1f} | {P[t, 1]:7.1f} | {P[t, 2]:7.1f} | {P[t, 3]:7.1f} | {R[t, 2]:7.1f} | {R[t, 0]:7.1f}")
+
+# every CTA's column groups: mean term duration (terms 2..ntot-1) and finishing time of the last term
+ce = colend[:148, :, :ntot]
+act = (ce > 0).all(axis=2)
+dur = np.where(act, (ce[:, :, ntot - 1] - ce[:, :, 1]) / 1000.0 / (ntot - 2), np.nan)
+fin = np.where(act, (ce[:, :, ntot - 1] - t0) / 1000.0, np.nan)
+print("column groups: mean us/term (terms 2..): min %.2f median %.2f max %.2f" % (np.nanmin(dur), np.nanmedian(dur), np.nanmax(dur)))
+order = np.argsort(-np.nan_to_num(dur, nan=-1).ravel())[:12]
+print("slowest groups (cta, group, us/term, last term done):",
+      [(int(i // 2), int(i % 2), round(float(dur.ravel()[i]), 2), round(float(fin.ravel()[i]), 1)) for i in order])
+ng = act.sum(axis=1)
+for k in (1, 2):
+    sel = ng == k
+    if sel.any():
+        print(f"CTAs with {k} active group(s): {int(sel.sum())}, mean us/term {np.nanmean(dur[sel]):.2f}")
+
+# own work per term (ring wait excluded) = term end - after-ring-wait, terms 2..ntot-1
+cg_ = colgo[:148, :, :ntot]
+own = np.where(act, (ce[:, :, 2:ntot] - cg_[:, :, 2:ntot]).mean(axis=2) / 1000.0, np.nan)
+print("own column work us/term: min %.2f median %.2f max %.2f" % (np.nanmin(own), np.nanmedian(own), np.nanmax(own)))
+order = np.argsort(-np.nan_to_num(own, nan=-1).ravel())[:16]
+print("largest own work (cta, group, us):", [(int(i // 2), int(i % 2), round(float(own.ravel()[i]), 2)) for i in order])
+for k in (1, 2):
+    sel = ng == k
+    if sel.any():
+        print(f"CTAs with {k} group(s): own work mean {np.nanmean(own[sel]):.2f} max {np.nanmax(own[sel]):.2f}")
+nrows = np.array([((b + 1) * 1024) // 148 - (b * 1024) // 148 for b in range(148)])
+for nr in (6, 7):
+    sel = (nrows == nr) & (ng == 2)
+    if sel.any():
+        print(f"2-group CTAs with {nr} rows: {int(sel.sum())}, own work mean {np.nanmean(own[sel]):.2f}")
