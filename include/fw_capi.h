@@ -20,6 +20,8 @@
  *   fw_seis_step            SeismicStepper::step / advance               seismic.cpp:111-137
  *   fw_seis_get             SeismicStepper::current / n                  seismic.hpp:44-46
  *   fw_tsfp2_*              Stepper (Method::TSFP2) ctor / step            stepping.cpp:119-138, 266-304
+ *   fw_wave_*               Stepper (Method::LFFP / CNFP) ctor / step      stepping.cpp:88-104, 119-138, 170-264
+ *                           (the Laplacian seam stepping.hpp:52-60 served by the device apply)
  *   fw_grid_dft             Grid::dft on a real/Hermitian field           grid.cpp:134-137 (canonical FFT, test hook)
  */
 #ifndef FW_CAPI_H
@@ -48,13 +50,16 @@ enum fw_status {
   FW_E_OOM = 11,            /* device allocation failed */
   FW_E_CUDA = 12,           /* CUDA runtime error / no device */
   FW_E_UNSUPPORTED = 13,    /* valid for the reference but not for this backend (non-power-of-two axis) */
-  FW_E_NCCL = 14            /* collective failure (slab-decomposed grids) */
+  FW_E_NCCL = 14,           /* collective failure (slab-decomposed grids) */
+  FW_E_PICARD_DIVERGED = 15,/* fwave::PicardDiverged */
+  FW_E_CG_STAGNATED = 16    /* fwave::CgStagnated */
 };
 
 typedef struct fw_ctx_s* fw_ctx;
 typedef struct fw_op_s* fw_op;
 typedef struct fw_seis_s* fw_seis;
 typedef struct fw_tsfp2_s* fw_tsfp2;
+typedef struct fw_wave_s* fw_wave;
 
 const char* fw_last_error(void);
 int fw_version(void);
@@ -150,6 +155,22 @@ int fw_tsfp2_create(fw_ctx ctx, int dim, const int* J, const double* lo, const d
 void fw_tsfp2_destroy(fw_tsfp2 t);
 int fw_tsfp2_step(fw_tsfp2 t, int nsteps);
 int fw_tsfp2_get(fw_tsfp2 t, double* u_host, double* v_host, long* n);
+
+/* ---- two-level integrators (Stepper, Method::LFFP = 0 / Method::CNFP = 1) ----
+ * u_tt = -kappa (-Delta)^{s(x)} u + f(u), f: 0 = none, 1 = cubic u^3.  The constructor
+ * takes the Taylor start u^0 = phi, u^1 = phi + tau psi + tau^2/2 (-kappa L phi + f(phi))
+ * (n = 1).  StepperConfig fields as in stepping.hpp:39-48 (use_dense is not offered: the
+ * dense operator is out of scope).  State and every CG / Picard vector stay on the device;
+ * the operator is the hot-path apply.  step: FW_E_BLOWUP (n incremented, state = the
+ * pre-step levels, as the reference), FW_E_CG_STAGNATED, FW_E_PICARD_DIVERGED. */
+int fw_wave_create(fw_ctx ctx, int method, int dim, const int* J, const double* lo, const double* hi,
+                   const double* order_values, int M, double kappa, int f_kind, const double* phi,
+                   const double* psi, double tau, double picard_tol, int picard_max_iters,
+                   double inner_cg_tol, int cg_max_iters, double blowup_factor, fw_wave* out);
+void fw_wave_destroy(fw_wave w);
+int fw_wave_step(fw_wave w, int nsteps);
+/* cur = u^n, prev = u^{n-1} (host, nullable); n; total Picard iterations (CNFP) */
+int fw_wave_get(fw_wave w, double* cur_host, double* prev_host, long* n, long* picard_total);
 
 /* ---- canonical transforms (test hooks) ----
  * forward: real x[N] -> half spectrum H[N_half] (interleaved re,im), unscaled;

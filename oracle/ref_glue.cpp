@@ -42,6 +42,8 @@ int code_of(const std::exception& e) {
   if (dynamic_cast<const OddSize*>(&e)) return 8;
   if (dynamic_cast<const EmptyInterval*>(&e)) return 9;
   if (dynamic_cast<const DimOutOfRange*>(&e)) return 10;
+  if (dynamic_cast<const PicardDiverged*>(&e)) return 15;
+  if (dynamic_cast<const CgStagnated*>(&e)) return 16;
   return 99;
 }
 
@@ -216,6 +218,48 @@ int ref_lffp(int d, const int* J, const double* lo, const double* hi, const doub
     Stepper st(p, cfg);
     for (int i = 0; i < nsteps; ++i) st.step();
     std::memcpy(u_out, st.current().values().data(), N * sizeof(double));
+  });
+}
+
+// Stepper with Method::LFFP (0) / CNFP (1) (stepping.cpp:119-138, 170-264), f none (0) or
+// cubic (1), the StepperConfig fields as given.  After `nsteps` step() calls (or the one
+// that threw) cur_out = current(), *n_out = n(), *picard_out = total_picard_iterations().
+int ref_wave(int method, int d, const int* J, const double* lo, const double* hi, const double* s, int M,
+             double kappa, int cubic, const double* phi, const double* psi, double tau, double picard_tol,
+             int picard_max_iters, double inner_cg_tol, int cg_max_iters, double blowup_factor, int nsteps,
+             double* cur_out, long* n_out, long* picard_out) {
+  return guard([&] {
+    Grid g = make_grid(d, J, lo, hi);
+    const std::size_t N = g.total();
+    WaveProblem p;
+    p.grid = g;
+    p.order = OrderField(g, vec(s, N));
+    p.kappa = kappa;
+    p.f = cubic ? Nonlinearity::cubic() : Nonlinearity::none();
+    p.phi = Field(g, vec(phi, N));
+    p.psi = Field(g, vec(psi, N));
+    p.M = M;
+    StepperConfig cfg;
+    cfg.method = method == 0 ? Method::LFFP : Method::CNFP;
+    cfg.tau = tau;
+    cfg.picard_tol = picard_tol;
+    cfg.picard_max_iters = picard_max_iters;
+    cfg.inner_cg_tol = inner_cg_tol;
+    cfg.cg_max_iters = cg_max_iters;
+    cfg.blowup_factor = blowup_factor;
+    Stepper st(p, cfg);
+    auto out = [&] {
+      std::memcpy(cur_out, st.current().values().data(), N * sizeof(double));
+      *n_out = st.n();
+      *picard_out = st.total_picard_iterations();
+    };
+    try {
+      for (int i = 0; i < nsteps; ++i) st.step();
+    } catch (...) {
+      out();
+      throw;
+    }
+    out();
   });
 }
 

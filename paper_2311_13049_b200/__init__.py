@@ -17,6 +17,7 @@ from __future__ import annotations
 
 from ._capi import (  # noqa: F401
     BlowupDetected,
+    CgStagnated,
     CudaError,
     DeviationTooLarge,
     DimOutOfRange,
@@ -28,6 +29,7 @@ from ._capi import (  # noqa: F401
     OddSize,
     OrderOutOfRange,
     OutOfMemory,
+    PicardDiverged,
     Unsupported,
     library_path,
     load_library,
@@ -39,7 +41,10 @@ from .api import (  # noqa: F401
     OrderField,
     SeismicMedium,
     SeismicStepper,
+    Stepper,
+    StepperConfig,
     TSFP2Stepper,
+    WaveProblem,
     apply_batch,
     apply_batch_device,
     apply_matrix_free,

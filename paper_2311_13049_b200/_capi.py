@@ -68,13 +68,22 @@ class Unsupported(Error):
     code = 13
 
 
+class PicardDiverged(Error):
+    code = 15
+
+
+class CgStagnated(Error):
+    code = 16
+
+
 class ArgumentError(Error, ValueError):
     code = 1
 
 
 _BY_CODE = {c.code: c for c in (ArgumentError, GridMismatch, NegativeM, OrderOutOfRange,
                                  DeviationTooLarge, GammaOutOfRange, BlowupDetected, OddSize,
-                                 EmptyInterval, DimOutOfRange, OutOfMemory, CudaError, Unsupported)}
+                                 EmptyInterval, DimOutOfRange, OutOfMemory, CudaError, Unsupported,
+                                 PicardDiverged, CgStagnated)}
 
 
 class OpInfo(C.Structure):
@@ -139,6 +148,13 @@ def load_library():
     lib.fw_tsfp2_destroy.restype = None
     lib.fw_tsfp2_step.argtypes = [_vp, C.c_int]
     lib.fw_tsfp2_get.argtypes = [_vp, _dp, _dp, C.POINTER(C.c_long)]
+    lib.fw_wave_create.argtypes = [_vp, C.c_int, C.c_int, _ip, _dp, _dp, _dp, C.c_int, C.c_double, C.c_int, _dp,
+                                   _dp, C.c_double, C.c_double, C.c_int, C.c_double, C.c_int, C.c_double,
+                                   C.POINTER(_vp)]
+    lib.fw_wave_destroy.argtypes = [_vp]
+    lib.fw_wave_destroy.restype = None
+    lib.fw_wave_step.argtypes = [_vp, C.c_int]
+    lib.fw_wave_get.argtypes = [_vp, _dp, _dp, C.POINTER(C.c_long), C.POINTER(C.c_long)]
     lib.fw_rfftn.argtypes = [_vp, C.c_int, _ip, _dp, _dp]
     lib.fw_irfftn.argtypes = [_vp, C.c_int, _ip, _dp, _dp]
     _lib = lib
@@ -158,5 +174,6 @@ EXPORTED_SYMBOLS = [
     "fw_medium_coefficients", "fw_stage_seis_start", "fw_stage_seis_update", "fw_seis_create", "fw_seis_destroy",
     "fw_seis_step", "fw_seis_enqueue", "fw_seis_get", "fw_seis_set_current",
     "fw_seis_current_device", "fw_seis_ops", "fw_seis_medium", "fw_tsfp2_create",
-    "fw_tsfp2_destroy", "fw_tsfp2_step", "fw_tsfp2_get", "fw_rfftn", "fw_irfftn",
+    "fw_tsfp2_destroy", "fw_tsfp2_step", "fw_tsfp2_get", "fw_wave_create", "fw_wave_destroy", "fw_wave_step",
+    "fw_wave_get", "fw_rfftn", "fw_irfftn",
 ]

@@ -10,12 +10,13 @@ build_medium / SeismicStepper (seismic.hpp:13-55), Stepper TSFP2
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass
 from typing import Optional, Sequence
 
 import numpy as np
 
 from . import _capi
-from ._capi import DimOutOfRange, EmptyInterval, GridMismatch, OddSize, check, load_library
+from ._capi import ArgumentError, DimOutOfRange, EmptyInterval, GridMismatch, OddSize, check, load_library
 
 _dp = C.POINTER(C.c_double)
 
@@ -403,6 +404,125 @@ class TSFP2Stepper:
         try:
             if getattr(self, "_h", None):
                 load_library().fw_tsfp2_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+@dataclass
+class WaveProblem:
+    """u_tt = -kappa (-Delta)^{s(x)} u + f(u) (stepping.hpp:30-37); f in {"none", "cubic"}
+    (the reference's expression-valued f is out of scope)."""
+    order: OrderField
+    phi: object
+    psi: object
+    kappa: float = 1.0
+    f: str = "none"
+    M: int = 15
+
+
+@dataclass
+class StepperConfig:
+    """stepping.hpp:39-48 (use_dense is not offered: the dense operator is out of scope)."""
+    method: str = "TSFP2"  # "LFFP", "CNFP" or "TSFP2"
+    tau: float = 1e-3
+    picard_tol: float = 1e-12
+    picard_max_iters: int = 200
+    inner_cg_tol: float = 1e-14
+    cg_max_iters: int = 500
+    blowup_factor: float = 1e8
+
+
+class Stepper:
+    """The reference's Stepper (stepping.hpp:72-104) with the Laplacian seam served by
+    the device apply.  LFFP / CNFP keep both levels, and CNFP every Picard / CG vector,
+    on the device (fw_wave_*); TSFP2 delegates to TSFP2Stepper (fw_tsfp2_*).  LFFP and
+    TSFP2 are bit-identical to the reference; CNFP agrees to the CG tolerance (its
+    dot products are deterministic tree sums, not the reference's serial sums)."""
+
+    _METHODS = {"LFFP": 0, "CNFP": 1}
+
+    def __init__(self, problem: WaveProblem, config: StepperConfig, ctx: Optional[Context] = None):
+        if problem.f not in ("none", "cubic"):
+            raise ArgumentError(f"f must be 'none' or 'cubic', not {problem.f!r}")
+        self.ctx = ctx or default_context()
+        self.config = config
+        g = problem.order.grid
+        self.grid = g
+        self.method = config.method.upper()
+        if self.method == "TSFP2":
+            if config.blowup_factor != 1e8:
+                raise ArgumentError("TSFP2 uses the reference's default blow-up factor 1e8")
+            self._ts = TSFP2Stepper(problem.order, problem.M, problem.kappa, problem.phi, problem.psi, config.tau,
+                                    f=problem.f, ctx=self.ctx)
+            return
+        if self.method not in self._METHODS:
+            raise ArgumentError(f"unknown method {config.method!r}")
+        self._ts = None
+        N = g.total()
+        J, lo, hi = g._carrays()
+        h = C.c_void_p()
+        check(load_library().fw_wave_create(
+            self.ctx.handle, self._METHODS[self.method], g.dim, J, lo, hi, _ptr(problem.order.values),
+            int(problem.M), float(problem.kappa), 1 if problem.f == "cubic" else 0, _ptr(_f64(problem.phi, N)),
+            _ptr(_f64(problem.psi, N)), float(config.tau), float(config.picard_tol), int(config.picard_max_iters),
+            float(config.inner_cg_tol), int(config.cg_max_iters), float(config.blowup_factor), C.byref(h)))
+        self._h = h
+
+    def advance(self, steps: int):
+        if self._ts is not None:
+            self._ts.advance(steps)
+            return
+        check(load_library().fw_wave_step(self._h, int(steps)))
+
+    def step(self):
+        self.advance(1)
+
+    def advance_to(self, t_final: float):
+        target = int(round(t_final / self.config.tau))  # std::lround (stepping.cpp:165-168)
+        if target > self.n():
+            self.advance(target - self.n())
+
+    def _get(self):
+        cur, prev = np.empty(self.grid.shape), np.empty(self.grid.shape)
+        n, pt = C.c_long(), C.c_long()
+        check(load_library().fw_wave_get(self._h, _ptr(cur), _ptr(prev), C.byref(n), C.byref(pt)))
+        return cur, prev, n.value, pt.value
+
+    def current(self):
+        return self._ts.current() if self._ts is not None else self._get()[0]
+
+    def previous(self):
+        """u^{n-1} (two-level methods)."""
+        return self._get()[1]
+
+    def velocity(self):
+        if self._ts is None:
+            raise ArgumentError("velocity() is TSFP2 only")
+        return self._ts.velocity()
+
+    def n(self) -> int:
+        n, pt = C.c_long(), C.c_long()
+        if self._ts is not None:
+            check(load_library().fw_tsfp2_get(self._ts._h, None, None, C.byref(n)))
+        else:
+            check(load_library().fw_wave_get(self._h, None, None, C.byref(n), C.byref(pt)))
+        return n.value
+
+    def time(self) -> float:
+        return self.n() * self.config.tau
+
+    def total_picard_iterations(self) -> int:
+        if self._ts is not None:
+            return 0
+        n, pt = C.c_long(), C.c_long()
+        check(load_library().fw_wave_get(self._h, None, None, C.byref(n), C.byref(pt)))
+        return pt.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().fw_wave_destroy(self._h)
                 self._h = None
         except Exception:
             pass

@@ -1102,6 +1102,254 @@ int fw_tsfp2_get(fw_tsfp2 t, double* u_host, double* v_host, long* n) {
 }  // extern "C"
 
 // ===========================================================================
+// LFFP / CNFP two-level integrators (stepping.cpp:88-104, 119-138, 170-264): the
+// reference's Stepper with the Laplacian seam served by the device apply; the state
+// and every CG / Picard vector stay in HBM, only scalars cross to the host.
+
+struct fw_wave_s {
+  fw_ctx ctx = nullptr;
+  fw::GridGeom g;
+  fw_op A = nullptr;
+  int method = 0, cubic = 0;
+  double tau = 0, kappa = 1, thr = 0, picard_tol = 0, cg_tol = 0;
+  int picard_max = 0, cg_max = 0;
+  double* ub[3] = {nullptr, nullptr, nullptr};  // level L lives in ub[L % 3]
+  long lvl = 1;                                 // level of cur (= n except after a blow-up)
+  long n = 1, picard_total = 0;
+  double *lu = nullptr, *rhs0 = nullptr, *rhs = nullptr, *wa = nullptr, *wb = nullptr;
+  double *r = nullptr, *p = nullptr, *ap = nullptr, *part = nullptr, *scal = nullptr;
+  double* hs = nullptr;  // pinned host scalars
+  int* flag = nullptr;
+};
+
+namespace {
+
+void wave_free(fw_wave t) {
+  if (!t) return;
+  fw_op_destroy(t->A);
+  for (double* q : {t->ub[0], t->ub[1], t->ub[2], t->lu, t->rhs0, t->rhs, t->wa, t->wb, t->r, t->p, t->ap, t->part,
+                    t->scal})
+    if (q) cudaFree(q);
+  if (t->hs) cudaFreeHost(t->hs);
+  if (t->flag) cudaFree(t->flag);
+  delete t;
+}
+
+// host values of k reductions queued into scal[0..k)
+int wave_scalars(fw_wave t, int k) {
+  FW_CUDA(cudaMemcpyAsync(t->hs, t->scal, k * sizeof(double), cudaMemcpyDeviceToHost, t->ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(t->ctx->stream));
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+// CG on (I + alpha L) x = rhs, warm start at rhs (stepping.cpp:183-221)
+int wave_cg(fw_wave t, const double* rhs, double* x, double alpha) {
+  auto L = t->ctx->L();
+  const size_t N = t->g.N;
+  cudaStream_t st = t->ctx->stream;
+  FW_CUDA(cudaMemcpyAsync(x, rhs, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  FW_TRY(apply_device(t->A, x, t->lu, 0, nullptr, nullptr));
+  fw::launch_cg_apply_a(L, N, alpha, x, t->lu, rhs, t->r);  // r = rhs - A x
+  fw::launch_dot(L, N, 0, rhs, rhs, t->part, t->scal + 0);
+  fw::launch_dot(L, N, 0, t->r, t->r, t->part, t->scal + 1);
+  FW_TRY(wave_scalars(t, 2));
+  const double rhs_norm = std::max(std::sqrt(t->hs[0]), 1e-300);
+  double rr = t->hs[1];
+  if (std::sqrt(rr) <= t->cg_tol * rhs_norm) return FW_OK;
+  FW_CUDA(cudaMemcpyAsync(t->p, t->r, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  for (int it = 0; it < t->cg_max; ++it) {
+    FW_TRY(apply_device(t->A, t->p, t->lu, 0, nullptr, nullptr));
+    fw::launch_cg_apply_a(L, N, alpha, t->p, t->lu, nullptr, t->ap);  // ap = A p
+    fw::launch_dot(L, N, 0, t->p, t->ap, t->part, t->scal);
+    FW_TRY(wave_scalars(t, 1));
+    const double pap = t->hs[0];
+    if (pap == 0.0) return set_err(FW_E_CG_STAGNATED, "zero curvature in conjugate gradient");
+    const double a = rr / pap;
+    fw::launch_cg_step(L, N, a, t->p, t->ap, x, t->r);
+    fw::launch_dot(L, N, 0, t->r, t->r, t->part, t->scal);
+    FW_TRY(wave_scalars(t, 1));
+    const double rr_new = t->hs[0];
+    if (std::sqrt(rr_new) <= t->cg_tol * rhs_norm) return FW_OK;
+    const double beta = rr_new / rr;
+    rr = rr_new;
+    fw::launch_cg_dir(L, N, beta, t->r, t->p);
+  }
+  return set_err(FW_E_CG_STAGNATED,
+                 "conjugate gradient failed to converge in " + std::to_string(t->cg_max) + " iterations");
+}
+
+// one CNFP step into ub[(lvl + 1) % 3] (stepping.cpp:223-264); blow-up check left to the caller
+int wave_cnfp(fw_wave t) {
+  auto L = t->ctx->L();
+  const size_t N = t->g.N;
+  const double t2 = t->tau * t->tau;
+  const double alpha = 0.5 * t->kappa * t2;
+  const double* cur = t->ub[t->lvl % 3];
+  const double* prev = t->ub[(t->lvl + 2) % 3];
+  double* out = t->ub[(t->lvl + 1) % 3];
+  FW_TRY(apply_device(t->A, prev, t->lu, 0, nullptr, nullptr));
+  fw::launch_cnfp_rhs0(L, N, t2, alpha, t->cubic, cur, prev, t->lu, t->rhs0);
+  if (!t->cubic) {
+    FW_TRY(wave_cg(t, t->rhs0, out, alpha));
+    ++t->picard_total;
+    return FW_OK;
+  }
+  // Picard on w = u^{n+1}, starting from u^n; iterates alternate between two buffers
+  double* w = t->wa;
+  double* wn = t->wb;
+  FW_CUDA(cudaMemcpyAsync(w, cur, N * sizeof(double), cudaMemcpyDeviceToDevice, t->ctx->stream));
+  for (int it = 0; it < t->picard_max; ++it) {
+    fw::launch_cnfp_rhs(L, N, t2, t->rhs0, w, t->rhs);
+    FW_TRY(wave_cg(t, t->rhs, wn, alpha));
+    fw::launch_dot(L, N, 1, wn, w, t->part, t->scal + 0);  // sum (w_next - w)^2
+    fw::launch_dot(L, N, 0, wn, wn, t->part, t->scal + 1);  // |w_next|^2
+    FW_TRY(wave_scalars(t, 2));
+    ++t->picard_total;
+    std::swap(w, wn);
+    if (std::sqrt(t->hs[0]) <= t->picard_tol * std::max(1.0, std::sqrt(t->hs[1]))) {
+      FW_CUDA(cudaMemcpyAsync(out, w, N * sizeof(double), cudaMemcpyDeviceToDevice, t->ctx->stream));
+      return FW_OK;
+    }
+  }
+  return set_err(FW_E_PICARD_DIVERGED, "fixed-point iteration cap hit at step " + std::to_string(t->n));
+}
+
+}  // namespace
+
+extern "C" {
+
+int fw_wave_create(fw_ctx ctx, int method, int dim, const int* J, const double* lo, const double* hi,
+                   const double* order_values, int M, double kappa, int f_kind, const double* phi,
+                   const double* psi, double tau, double picard_tol, int picard_max_iters, double inner_cg_tol,
+                   int cg_max_iters, double blowup_factor, fw_wave* out) {
+  if (!ctx || !out || !lo || !hi || !phi || !psi) return set_err(FW_E_ARG, "null argument");
+  if (method != 0 && method != 1) return set_err(FW_E_ARG, "method must be 0 (LFFP) or 1 (CNFP)");
+  if (f_kind != 0 && f_kind != 1) return set_err(FW_E_ARG, "f must be 0 (none) or 1 (cubic)");
+  fw::GridGeom g;
+  FW_TRY(check_grid(dim, J, lo, hi, &g));
+  FW_CUDA(cudaSetDevice(ctx->device));
+  fw_wave t = new fw_wave_s();
+  t->ctx = ctx;
+  t->g = g;
+  t->method = method;
+  t->cubic = f_kind;
+  t->tau = tau;
+  t->kappa = kappa;
+  t->picard_tol = picard_tol;
+  t->picard_max = picard_max_iters;
+  t->cg_tol = inner_cg_tol;
+  t->cg_max = cg_max_iters;
+  int rc = op_create_internal(ctx, g, lo, hi, order_values, nullptr, M, &t->A);
+  for (double** q : {&t->ub[0], &t->ub[1], &t->ub[2], &t->lu})
+    if (rc == FW_OK) rc = dalloc(q, g.N);
+  if (method == 1)
+    for (double** q : {&t->rhs0, &t->rhs, &t->wa, &t->wb, &t->r, &t->p, &t->ap})
+      if (rc == FW_OK) rc = dalloc(q, g.N);
+  if (rc == FW_OK) rc = dalloc(&t->part, fw::wave_partials());
+  if (rc == FW_OK) rc = dalloc(&t->scal, 4);
+  if (rc == FW_OK) rc = dalloc(&t->flag, 1);
+  if (rc == FW_OK && cudaMallocHost((void**)&t->hs, 4 * sizeof(double)) != cudaSuccess) rc = FW_E_OOM;
+  if (rc != FW_OK) {
+    wave_free(t);
+    return rc == FW_E_OOM ? set_err(FW_E_OOM, "wave stepper allocation") : rc;
+  }
+  // blowup_threshold_ = factor * max(sup|phi|, 1e-300) (stepping.cpp:121), std::max semantics
+  double sup = 0.0;
+  for (size_t j = 0; j < g.N; ++j) sup = std::max(sup, std::fabs(phi[j]));
+  t->thr = blowup_factor * std::max(sup, 1e-300);
+  cudaStream_t st = ctx->stream;
+  const int none = fw::kNoBlowup;
+  cudaMemcpyAsync(t->flag, &none, sizeof(int), cudaMemcpyHostToDevice, st);
+  // initial_levels (stepping.cpp:88-104): u^0 = phi, u^1 = Taylor start; psi staged in ub[2]
+  cudaMemcpyAsync(t->ub[0], phi, g.N * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(t->ub[2], psi, g.N * 8, cudaMemcpyHostToDevice, st);
+  rc = apply_device(t->A, t->ub[0], t->lu, 0, nullptr, nullptr);
+  if (rc == FW_OK) {
+    fw::launch_wave_start(ctx->L(), g.N, tau, kappa, t->cubic, t->ub[0], t->ub[2], t->lu, t->ub[1]);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) rc = set_err(FW_E_CUDA, std::string("wave setup: ") + cudaGetErrorString(e));
+  }
+  if (rc != FW_OK) {
+    wave_free(t);
+    return rc;
+  }
+  t->lvl = 1;
+  t->n = 1;  // cur_ is u^1
+  *out = t;
+  return FW_OK;
+}
+
+void fw_wave_destroy(fw_wave t) {
+  if (t && t->ctx) cudaStreamSynchronize(t->ctx->stream);
+  wave_free(t);
+}
+
+int fw_wave_step(fw_wave t, int nsteps) {
+  if (!t || nsteps < 0) return set_err(FW_E_ARG, "bad argument");
+  auto L = t->ctx->L();
+  const size_t N = t->g.N;
+  cudaStream_t st = t->ctx->stream;
+  const double t2 = t->tau * t->tau;
+  const long lvl0 = t->lvl, n0 = t->n;
+  if (t->method == 0) {
+    // LFFP: the whole batch is enqueued; a blow-up freezes the later updates (stepping.cpp:170-181)
+    for (int i = 0; i < nsteps; ++i) {
+      const long l = lvl0 + i;
+      FW_TRY(apply_device(t->A, t->ub[l % 3], t->lu, 0, nullptr, nullptr));
+      fw::launch_lffp_update(L, N, t2, t->kappa, t->cubic, t->ub[l % 3], t->ub[(l + 2) % 3], t->lu,
+                             t->ub[(l + 1) % 3], t->flag);
+      fw::launch_sup_check(L, N, t->ub[(l + 1) % 3], t->thr, (int)(n0 + i + 1), t->flag);
+    }
+    t->lvl = lvl0 + nsteps;
+    t->n = n0 + nsteps;
+  } else {
+    for (int i = 0; i < nsteps; ++i) {
+      int rc = wave_cnfp(t);
+      if (rc != FW_OK) return rc;  // state unchanged, n not incremented (the reference throws before ++n_)
+      fw::launch_sup_check(L, N, t->ub[(t->lvl + 1) % 3], t->thr, (int)(t->n + 1), t->flag);
+      int flag = fw::kNoBlowup;
+      FW_CUDA(cudaMemcpyAsync(&flag, t->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+      FW_CUDA(cudaStreamSynchronize(st));
+      t->n += 1;
+      if (flag != fw::kNoBlowup) break;
+      t->lvl += 1;
+    }
+  }
+  int flag = fw::kNoBlowup;
+  FW_CUDA(cudaMemcpyAsync(&flag, t->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FW_CUDA(cudaStreamSynchronize(st));
+  FW_CUDA(cudaGetLastError());
+  if (flag != fw::kNoBlowup) {
+    // the reference increments n_ and throws before rotating: state = the levels before step `flag`
+    t->n = flag;
+    t->lvl = lvl0 + (flag - n0) - 1;
+    const int none = fw::kNoBlowup;
+    FW_CUDA(cudaMemcpyAsync(t->flag, &none, sizeof(int), cudaMemcpyHostToDevice, st));
+    FW_CUDA(cudaStreamSynchronize(st));
+    char b[128];
+    snprintf(b, sizeof b, "sup|u| > %g at step %d", t->thr, flag);
+    return set_err(FW_E_BLOWUP, b);
+  }
+  return FW_OK;
+}
+
+int fw_wave_get(fw_wave t, double* cur_host, double* prev_host, long* n, long* picard_total) {
+  if (!t) return set_err(FW_E_ARG, "null stepper");
+  cudaStream_t st = t->ctx->stream;
+  if (cur_host) FW_CUDA(cudaMemcpyAsync(cur_host, t->ub[t->lvl % 3], t->g.N * 8, cudaMemcpyDeviceToHost, st));
+  if (prev_host)
+    FW_CUDA(cudaMemcpyAsync(prev_host, t->ub[(t->lvl + 2) % 3], t->g.N * 8, cudaMemcpyDeviceToHost, st));
+  FW_CUDA(cudaStreamSynchronize(st));
+  if (n) *n = t->n;
+  if (picard_total) *picard_total = t->picard_total;
+  return FW_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
 // stage entry points: the pipeline's kernels on caller-provided device sub-arrays
 // (used by the slab-decomposed multi-GPU apply, paper_2311_13049_b200/slab.py)
 

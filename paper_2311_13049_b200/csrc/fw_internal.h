@@ -76,6 +76,23 @@ void launch_tsfp2_kick(const LaunchCtx& L, size_t N, double tau, double kappa, i
 void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x);
 void launch_sup_check(const LaunchCtx& L, size_t N, const double* u, double thr, int step, int* flag);
 
+// two-level integrators LFFP / CNFP (stepping.cpp:88-104, 170-264), fw_wave.cu
+size_t wave_partials();
+void launch_wave_start(const LaunchCtx& L, size_t N, double tau, double kappa, int cubic, const double* phi,
+                       const double* psi, const double* lphi, double* u1);
+void launch_lffp_update(const LaunchCtx& L, size_t N, double t2, double kappa, int cubic, const double* cur,
+                        const double* prev, const double* lu, double* next, const int* flag);
+void launch_cnfp_rhs0(const LaunchCtx& L, size_t N, double t2, double alpha, int cubic, const double* cur,
+                      const double* prev, const double* lprev, double* rhs0);
+void launch_cnfp_rhs(const LaunchCtx& L, size_t N, double t2, const double* rhs0, const double* w, double* rhs);
+void launch_cg_apply_a(const LaunchCtx& L, size_t N, double alpha, const double* w, const double* lw,
+                       const double* rhs, double* out);
+void launch_cg_step(const LaunchCtx& L, size_t N, double a, const double* p, const double* ap, double* x, double* r);
+void launch_cg_dir(const LaunchCtx& L, size_t N, double beta, const double* r, double* p);
+// *out = sum a*b (mode 0) or sum (a-b)^2 (mode 1), deterministic order; partial: wave_partials() doubles
+void launch_dot(const LaunchCtx& L, size_t N, int mode, const double* a, const double* b, double* partial,
+                double* out);
+
 // batched multi-field pipeline (many independent fields of one grid, e.g. configs[4]):
 // per-field pointers of one kernel launch, indexed by blockIdx.z
 struct BatchLine {

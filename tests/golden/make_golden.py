@@ -110,6 +110,28 @@ manifest["cases"]["tsfp2_256"] = {
     "files": {"s": snap("tsfp2_256_s", s3, lo3, hi3), "phi": snap("tsfp2_256_phi", phi3, lo3, hi3),
               "u": snap("tsfp2_256_u", u, lo3, hi3), "v": snap("tsfp2_256_v", v, lo3, hi3)}}
 
+# LFFP / CNFP (stepping.cpp:170-264) through the reference's Stepper: 1D s1 profile (f none and
+# cubic, the CNFP cubic case runs Picard) and a 2D variable order
+def wave_case(key, method, lo, hi, s, M, kappa, cubic, phi, tau, steps):
+    J = phi.shape
+    cur, n, pt = O.ref_wave(method, J, lo, hi, s, M, kappa, cubic, phi, np.zeros(J), tau, steps)
+    manifest["cases"][key] = {
+        "kind": "wave", "method": method, "J": list(J), "lo": list(lo), "hi": list(hi), "M": M, "kappa": kappa,
+        "f": "cubic" if cubic else "none", "tau": tau, "steps": steps, "n": n, "picard_total": pt,
+        "files": {"s": snap(key + "_s", s, lo, hi), "phi": snap(key + "_phi", phi, lo, hi),
+                  "cur": snap(key + "_cur", cur, lo, hi, n * tau)}}
+
+
+wave_case("lffp_256", "LFFP", lo3, hi3, s3, 15, 1.0, 0, phi3, 1e-3, 30)
+wave_case("lffp_cubic_256", "LFFP", lo3, hi3, s3, 15, 1.0, 1, phi3, 1e-3, 30)
+wave_case("cnfp_256", "CNFP", lo3, hi3, s3, 15, 1.0, 0, phi3, 1e-2, 10)
+wave_case("cnfp_cubic_256", "CNFP", lo3, hi3, s3, 15, 1.0, 1, phi3, 1e-2, 8)
+X2, Y2 = np.meshgrid(*[-8.0 + np.arange(64) * 0.25 for _ in range(2)], indexing="ij")
+s_2d = 1.0 - 0.4 * np.cos(np.pi * X2 / 4.0) * np.cos(np.pi * Y2 / 4.0)
+phi_2d = np.exp(-(X2**2 + Y2**2))
+wave_case("lffp_2d_64", "LFFP", (-8.0, -8.0), (8.0, 8.0), s_2d, 12, 1.0, 0, phi_2d, 2e-3, 25)
+wave_case("cnfp_2d_64", "CNFP", (-8.0, -8.0), (8.0, 8.0), s_2d, 12, 1.0, 0, phi_2d, 1e-2, 6)
+
 with open(os.path.join(HERE, "manifest.json"), "w") as fh:
     json.dump(manifest, fh, indent=1, sort_keys=True)
 print("wrote", len(manifest["cases"]), "cases")

@@ -131,6 +131,44 @@ def test_restatement_reproduces_golden_tsfp2(manifest):
     assert np.array_equal(u, load_golden(c, "u")) and np.array_equal(v, load_golden(c, "v"))
 
 
+def _port_lffp(J, lo, hi, s, M, kappa, cubic, phi, tau, steps):
+    """LFFP (stepping.cpp:88-104, 170-181) on the C restatement's apply; the elementwise
+    updates in numpy with the reference's evaluation order (IEEE, no contraction)."""
+    def L(u):
+        return O.port_apply(J, lo, hi, s, u, M)[0].reshape(np.shape(u))
+
+    def f(u):
+        return u * u * u if cubic else np.zeros_like(u)
+
+    half_t2 = 0.5 * tau * tau
+    prev = np.array(phi, dtype=np.float64)
+    cur = prev + tau * np.zeros_like(prev) + half_t2 * (-kappa * L(prev) + f(prev))
+    t2 = tau * tau
+    for _ in range(steps):
+        nxt = 2.0 * cur - prev + t2 * (-kappa * L(cur) + f(cur))
+        prev, cur = cur, nxt
+    return cur
+
+
+@pytest.mark.parametrize("key", ["lffp_256", "lffp_cubic_256", "lffp_2d_64"])
+def test_restatement_reproduces_golden_lffp(manifest, key):
+    """The restatement's apply + the reference's LFFP update reproduce the reference's
+    Stepper(Method::LFFP) bit for bit (the CNFP fixtures pin the device CG to tolerance)."""
+    c = manifest["cases"][key]
+    cur = _port_lffp(tuple(c["J"]), c["lo"], c["hi"], load_golden(c, "s"), c["M"], c["kappa"], c["f"] == "cubic",
+                     load_golden(c, "phi"), c["tau"], c["steps"])
+    assert np.array_equal(cur, load_golden(c, "cur")), key
+
+
+@needs_ref
+def test_reference_wave_reproduces_golden(manifest):
+    for key in ("lffp_256", "cnfp_256", "cnfp_cubic_256"):
+        c = manifest["cases"][key]
+        cur, n, pt = O.ref_wave(c["method"], c["J"], c["lo"], c["hi"], load_golden(c, "s"), c["M"], c["kappa"],
+                                c["f"] == "cubic", load_golden(c, "phi"), np.zeros(c["J"]), c["tau"], c["steps"])
+        assert n == c["n"] and pt == c["picard_total"] and np.array_equal(cur, load_golden(c, "cur")), key
+
+
 @needs_ref
 @pytest.mark.parametrize("J,lo,hi,M,m_first,s0", [
     ((64,), (-32.0,), (32.0,), 0, 0, None),
