@@ -59,3 +59,13 @@ def test_cpp_gpu_seismic_stepper(tmp_path):
     r = subprocess.run([os.path.join(BUILD, "seismic_gpu_check")], cwd=tmp_path, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "[PASS]" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(os.path.join(BUILD, "stepper_gpu_check")), reason="drop-in not built")
+def test_cpp_gpu_stepper(tmp_path):
+    """fwave::gpu::Stepper (reference Stepper API; LFFP / CNFP / TSFP2 on the device)
+    against the reference's own Stepper on the same WaveProblem / StepperConfig."""
+    r = subprocess.run([os.path.join(BUILD, "stepper_gpu_check")], cwd=tmp_path, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "[PASS]" in r.stdout, r.stdout + r.stderr
