@@ -152,6 +152,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define FW_STEP2D_EXPERIMENTS 0
 #endif
 #define FW_DBG(bits) (FW_STEP2D_EXPERIMENTS && (prm.dbg & (bits)))
+// per-thread FFT twiddles (column passes 1-2, row pass 2) held in tensor memory instead of
+// being re-read from shared memory every term
+#ifndef FW_S2D_TWTM
+#define FW_S2D_TWTM 1
+#endif
 #if FW_STEP2D_TRACE
 #define FW_TRACE(t, slot)                                                                              \
   do {                                                                                                 \
@@ -316,8 +321,13 @@ struct Geo {
   static constexpr size_t SMEM = NELEM * sizeof(double2);
   // tensor memory: [0,128) row accumulators (16 warps x 32 columns), [128, 128 + 8 CR0) uhat
   static constexpr int TM_U = 128;
-  static constexpr int TM_COLS = 256;
-  static_assert(TM_U + 2 * 4 * CR0 <= TM_COLS, "tensor memory budget");
+  // (FW_S2D_TWTM) [256, 368) column twiddles (2 groups x 2 passes x 28), [368, 480) row pass-2
+  // twiddles (4 warps x 28), per lane quadrant
+  static constexpr int TM_TWC = 256;
+  static constexpr int TM_TWR = 368;
+  static constexpr int TM_COLS = FW_S2D_TWTM ? 512 : 256;
+  static_assert(TM_U + 2 * 4 * CR0 <= 256 && TM_TWR + 4 * 28 <= 512, "tensor memory budget");
+  static_assert(CR1 == 8 && CR2 == 8, "radix-8 column passes 1-2");
   static_assert(2 * CT0 == 128, "column pass 0: one butterfly per group thread");
   static_assert(npass(J0) == 3 && npass(h) == 3, "3-pass plans");
   static_assert(RR0 == 8 && RR1 == 8 && RR2 == 8 && RT == 64, "row pair: one radix-8 butterfly per lane");
@@ -368,6 +378,16 @@ __device__ __forceinline__ void tmem_ld4(unsigned taddr, unsigned* v) {
                : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_ld4_nw(unsigned taddr, unsigned* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st4_nw(unsigned taddr, const unsigned* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld8_nw(unsigned taddr, unsigned* v) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -385,6 +405,63 @@ __device__ __forceinline__ void tm_put(unsigned* v, int k, double x) {
   v[2 * k] = (unsigned)__double2loint(x);
   v[2 * k + 1] = (unsigned)__double2hiint(x);
 }
+// this thread's 7 twiddles of one radix-8 pass (butterfly index fixed across terms): 28 TMEM
+// columns = 7 x (re, im) as pairs of 32-bit halves.  Values = the table entries, so the
+// butterflies below are bit-identical to butterfly() reading shared memory.
+__device__ __forceinline__ void tw_park(unsigned taddr, const double2* t) {
+  unsigned v[28];
+#pragma unroll
+  for (int r = 0; r < 7; ++r) {
+    tm_put(v, 2 * r, t[r].x);
+    tm_put(v, 2 * r + 1, t[r].y);
+  }
+  tmem_st16_nw(taddr, v);
+  tmem_st8_nw(taddr + 16, v + 16);
+  tmem_st4_nw(taddr + 24, v + 24);
+  tmem_wait_st();
+}
+template <int DIR>
+__device__ __forceinline__ void tw_load(unsigned taddr, double2 (&w)[7]) {
+  unsigned v[28];
+  tmem_ld16_nw(taddr, v);
+  tmem_ld8_nw(taddr + 16, v + 16);
+  tmem_ld4_nw(taddr + 24, v + 24);
+  tmem_wait_ld();
+#pragma unroll
+  for (int r = 0; r < 7; ++r) w[r] = dirw<DIR>(make_double2(tm_d(v, 2 * r), tm_d(v, 2 * r + 1)));
+}
+// the same, twiddles applied in two halves (row warps run at 64 registers)
+template <int DIR>
+__device__ __forceinline__ void butterfly_tm8_lean(double2* a, unsigned taddr) {
+  {
+    unsigned v[16];
+    tmem_ld16_nw(taddr, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int r = 1; r <= 4; ++r) {
+      const double2 w = dirw<DIR>(make_double2(tm_d(v, 2 * (r - 1)), tm_d(v, 2 * (r - 1) + 1)));
+      a[r] = cmulw(a[r], w.x, w.y);
+    }
+  }
+  {
+    unsigned v[12];
+    tmem_ld8_nw(taddr + 16, v);
+    tmem_ld4_nw(taddr + 24, v + 8);
+    tmem_wait_ld();
+#pragma unroll
+    for (int r = 5; r <= 7; ++r) {
+      const double2 w = dirw<DIR>(make_double2(tm_d(v, 2 * (r - 5)), tm_d(v, 2 * (r - 5) + 1)));
+      a[r] = cmulw(a[r], w.x, w.y);
+    }
+  }
+  Dft<8, DIR>::run(a);
+}
+template <int DIR>
+__device__ __forceinline__ void butterfly_w8(double2* a, const double2 (&w)[7]) {
+#pragma unroll
+  for (int r = 1; r < 8; ++r) a[r] = cmulw(a[r], w[r - 1].x, w[r - 1].y);
+  Dft<8, DIR>::run(a);
+}
 __device__ __forceinline__ void pairbar(int p) { asm volatile("bar.sync %0, 64;" ::"r"(4 + p) : "memory"); }
 
 // ---------------------------------------------------------------- column group: 2 x J0-point C2C
@@ -393,8 +470,9 @@ __device__ __forceinline__ void pairbar(int p) { asm volatile("bar.sync %0, 64;"
 // passes 1 and 2 run one butterfly at a time in place; pass 2 hands the natural-order
 // outputs q = i + r CT2 of both members to epilogue(i, X0[], X1[]).
 template <class G, int DIR, class GBar, class Hook, class Epi, class Mark>
-__device__ __forceinline__ void column_pair(double2* work, const double2* tw, int cg, double2 (&a)[G::CR0], GBar gbar,
-                                            Hook after_pass0, Epi epilogue, Mark mark) {
+__device__ __forceinline__ void column_pair(double2* work, const double2* tw, unsigned ttw, int cg,
+                                            double2 (&a)[G::CR0], GBar gbar, Hook after_pass0, Epi epilogue,
+                                            Mark mark) {
   constexpr int J0 = G::CT0 * G::CR0;
   {
     const int mbr = cg / G::CT0, I = cg % G::CT0;
@@ -406,6 +484,7 @@ __device__ __forceinline__ void column_pair(double2* work, const double2* tw, in
   gbar();
   mark(3);
   after_pass0();
+  static_assert(!FW_S2D_TWTM || (G::CT1 <= 128 && G::CT2 <= 128), "one butterfly per thread and pass");
 #pragma unroll 1
   for (int i = cg; i < G::CT1; i += 128) {  // butterfly i of both members (same twiddles)
     double2 c0[G::CR1], c1[G::CR1];
@@ -414,8 +493,15 @@ __device__ __forceinline__ void column_pair(double2* work, const double2* tw, in
       c0[r] = work[G::c_p1(i, 0) + r];
       c1[r] = work[G::LCOL + G::c_p1(i, 0) + r];
     }
-    butterfly<J0, 1, DIR>(c0, i, tw);
-    butterfly<J0, 1, DIR>(c1, i, tw);
+    if (FW_S2D_TWTM) {  // i == cg: the thread's parked pass-1 twiddles
+      double2 w[7];
+      tw_load<DIR>(ttw, w);
+      butterfly_w8<DIR>(c0, w);
+      butterfly_w8<DIR>(c1, w);
+    } else {
+      butterfly<J0, 1, DIR>(c0, i, tw);
+      butterfly<J0, 1, DIR>(c1, i, tw);
+    }
 #pragma unroll
     for (int r = 0; r < G::CR1; ++r) {
       work[G::c_p1(i, 0) + r] = c0[r];
@@ -433,8 +519,15 @@ __device__ __forceinline__ void column_pair(double2* work, const double2* tw, in
       c0[r] = work[p];
       c1[r] = work[G::LCOL + p];
     }
-    butterfly<J0, 2, DIR>(c0, i, tw);
-    butterfly<J0, 2, DIR>(c1, i, tw);
+    if (FW_S2D_TWTM) {
+      double2 w[7];
+      tw_load<DIR>(ttw + 28, w);
+      butterfly_w8<DIR>(c0, w);
+      butterfly_w8<DIR>(c1, w);
+    } else {
+      butterfly<J0, 2, DIR>(c0, i, tw);
+      butterfly<J0, 2, DIR>(c1, i, tw);
+    }
     epilogue(i, c0, c1);
   }
 }
@@ -557,6 +650,12 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       if (kB >= 0 && kB < h) ++nz;  // column h feeds Z_0 and produces no Z of its own
       // this thread's uhat values: TMEM lane (32 (warp & 3) + lane), columns TM_U + g 4 CR0 + [0, 4 CR0)
       const unsigned tu = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_U + g * 4 * CR0);
+      // this thread's pass-1 / pass-2 twiddles (butterfly index cg in both passes) -> TMEM
+      const unsigned ttw = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_TWC + g * 56);
+      if (FW_S2D_TWTM) {
+        tw_park(ttw, twc + twoff(J0, 1) + (cg & (pprod(J0, 1) - 1)) * 7);
+        tw_park(ttw + 28, twc + twoff(J0, 2) + (cg & (pprod(J0, 2) - 1)) * 7);
+      }
 
       double rmax = 0.0;
 #pragma unroll 1
@@ -574,7 +673,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         double2 x0[G::CR2], x1[G::CR2];
         int ix = 0;
         column_pair<G, -1>(
-            work, twc, cg, a, gb, [] {},
+            work, twc, ttw, cg, a, gb, [] {},
             [&](int i, const double2* c0, const double2* c1) {
               ix = i;
 #pragma unroll
@@ -666,7 +765,8 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           if (cg_ == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz_);
           continue;
         }
-        column_pair<G, +1>(work_, twc, cg_, a, gb_, [&] {
+        const unsigned ttw_ = tmem_base + ((unsigned)(32 * ((tidc >> 5) & 3)) << 16) + (unsigned)(G::TM_TWC + g_ * 56);
+        column_pair<G, +1>(work_, twc, ttw_, cg_, a, gb_, [&] {
           if (cg_ == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz_);
         }, [&](int i, const double2* xa, const double2* xb) {
 #pragma unroll
@@ -710,6 +810,10 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
     const int row = r0 + (active ? pair : 0);
     // this warp's 32 TMEM columns in its lane quadrant: (s-s0)^m-weighted sums of outputs l + 64 r
     const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 32u * (unsigned)(rw >> 2);
+    // this lane's pass-2 twiddles (butterfly index l) -> TMEM, once per launch
+    if (FW_S2D_TWTM)
+      tw_park(tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_TWR + 28 * (rw >> 2)),
+              twr + twoff(h, 2) + (l & (pprod(h, 2) - 1)) * 7);
     double2* work = sm + G::OFF_RW + (size_t)(active ? pair : 0) * G::LROW;
     // the tile: rows r0..r0+7 of Z[t] as two [256 k][8 rows] TMA boxes, 128-B swizzled
     double2* tile;
@@ -853,7 +957,11 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         double2 a[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) a[r] = work_[G::r_p2in(l_) + r * G::RS2];
-        butterfly<h, 2, +1>(a, l_, twr);
+        if (FW_S2D_TWTM)
+          butterfly_tm8_lean<+1>(a, tmem_base + ((unsigned)(32 * ((tidr >> 5) & 3)) << 16) +
+                                        (unsigned)(G::TM_TWR + 28 * (rw_ >> 2)));
+        else
+          butterfly<h, 2, +1>(a, l_, twr);
 #pragma unroll
         for (int qt = 0; qt < 4; ++qt) {
           double2 d[2];
