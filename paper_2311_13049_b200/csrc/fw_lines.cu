@@ -195,37 +195,111 @@ bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, con
   return true;
 }
 
+// ---------------------------------------------------------------- tensor memory (per-thread state)
+// A warp reaches the 32 TMEM lanes of its quadrant (warp % 4); thread = lane, 32-bit columns.
+__host__ __device__ constexpr int pow2ceil(int n) { return n <= 1 ? 1 : 2 * pow2ceil((n + 1) / 2); }
+__device__ __forceinline__ void tm_ld16(unsigned taddr, unsigned* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tm_st16(unsigned taddr, const unsigned* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+               ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                 "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ double tm_get(const unsigned* v, int k) {
+  return __hiloint2double((int)v[2 * k + 1], (int)v[2 * k]);
+}
+__device__ __forceinline__ void tm_set(unsigned* v, int k, double x) {
+  v[2 * k] = (unsigned)__double2loint(x);
+  v[2 * k + 1] = (unsigned)__double2hiint(x);
+}
+
+// twiddled butterfly of pass PASS with the twiddles from a shared-memory table [k][r-1]
+// (values = master entries: bit-identical to bfly())
+template <int N, int PASS, int DIR>
+__device__ __forceinline__ void bfly_s(double2* a, int i, const double2* tw) {
+  constexpr int R = radix(N, PASS);
+  constexpr int p = pprod(N, PASS);
+  if constexpr (p > 1) {
+    const double2* t = tw + (i & (p - 1)) * (R - 1);
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double2 w = t[r - 1];
+      a[r] = cmulw(a[r], w.x, DIR < 0 ? -w.y : w.y);
+    }
+  }
+  Dft<R, DIR>::run(a);
+}
+
+// C2R pre-processing (c2r_pre) with W_{2h}^k given
+__device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, double2 w) {
+  double2 B = make_double2(Xhk.x, -Xhk.y);
+  if (k0) {
+    A.y = 0.0;
+    B.y = 0.0;
+  }
+  const double2 E = make_double2(A.x + B.x, A.y + B.y);
+  const double2 D = make_double2(A.x - B.x, A.y - B.y);
+  const double2 O = cmulw(D, w.x, w.y);
+  return make_double2(E.x - O.y, E.y + O.x);
+}
+
 // Per row of the last axis (NL reals, h = NL/2 complex, rows contiguous): for every
 // term m = m_first..m_last in ascending order, C2R of the half-spectrum row src_m
 // (flap.cpp:21-36: pre-processing Z_q = f(X_q, X_{h-q}), h-point C2C, real parts
 // interleaved) and acc += 0 + (s-s0)^m .* x with (s-s0)^m = (s-s0)^{m-1} (s-s0) carried
 // per element (flap.cpp:61-91, 124-133).  Thread (row, i) owns butterfly i of every
 // pass; its outputs q = i + r T_last and their accumulators stay in registers across
-// the terms, the running powers in shared memory.
+// the terms.  Everything a term needs besides its spectrum row is on chip: (s-s0) and
+// the running power (s-s0)^{m-1} of the thread's outputs live in TENSOR MEMORY (loaded
+// once per launch), the twiddles in one shared-memory table per block; the next term's
+// row lands by cp.async while the current term's passes run.
+#ifndef FW_C2R_MINB
+#define FW_C2R_MINB 2  // blocks per SM the register allocation is bounded for
+#endif
 template <int H>
-struct RowPlan {
+struct C2RPlan {
   using P = Plan<H>;
   static constexpr int TM = P::TMAX;                 // threads per row
   static constexpr int RL = radix(H, P::P - 1);      // last-pass radix
   static constexpr int TL = H / RL;
   static constexpr int XS = (H + 1) | 1;             // X row stride (natural order, odd)
-  static constexpr size_t ROWB = (size_t)(XS + P::LS) * sizeof(double2) + (size_t)2 * H * sizeof(double);
-  // rows per block: up to 256 threads, at most ~110 KB of shared memory (two blocks per SM)
-  static constexpr int RPB = (256 / TM) * ROWB <= 112640 ? 256 / TM : (int)(112640 / ROWB);
+  // twiddles: pre-processing W_{2H}^k (k <= H), pass 1 [k < R0][R1 - 1], pass 2 [k < R0 R1][R2 - 1]
+  static constexpr int TW1 = P::R0 * (P::R1 - 1);
+  static constexpr int TW2 = P::P > 2 ? P::R0 * P::R1 * (P::R2 - 1) : 0;
+  static constexpr int TWN = (H + 1) + TW1 + TW2;
+  static constexpr size_t ROWB = (size_t)(XS + P::LS) * sizeof(double2);
+  static constexpr size_t CAP = 112640;  // two blocks per SM
+  static constexpr int RPB = (size_t)(256 / TM) * ROWB + TWN * sizeof(double2) <= CAP
+                                 ? 256 / TM
+                                 : (int)((CAP - TWN * sizeof(double2)) / ROWB);
   static constexpr int NT = RPB * TM;
-  static constexpr size_t SMEM = (size_t)RPB * ROWB;
-  static_assert(RPB >= 1, "row fits");
+  static constexpr size_t SMEM = (size_t)TWN * sizeof(double2) + (size_t)RPB * ROWB;
+  // tensor memory per warp: (s-s0) at [0, 4 RL), (s-s0)^{m-1} at [4 RL, 8 RL) (two columns per double)
+  static constexpr int TMC = 8 * RL;
+  static constexpr int NSLOT = (NT / 32 + 3) / 4;
+  static constexpr int TMALLOC = pow2ceil(NSLOT * TMC < 32 ? 32 : NSLOT * TMC);
+  static_assert(RPB >= 1 && NT % 32 == 0, "whole warps");
+  static_assert(TL == TM, "every thread owns RL outputs");
+  static_assert(RL % 4 == 0, "16-column chunks");
+  static_assert(TMALLOC <= 256, "two blocks per SM in tensor memory");
 };
 
 template <int H>
-__global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ src, long long src_ts, int m_first,
-                                                  int m_last, const double* __restrict__ dev1,
-                                                  double* __restrict__ out, long long rows, double* residue,
-                                                  const int* guard, const double2* __restrict__ master,
-                                                  const BatchLine* __restrict__ bl) {
-  using RP = RowPlan<H>;
+__global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const double2* __restrict__ src, long long src_ts,
+                                                            int m_first, int m_last, const double* __restrict__ dev1,
+                                                            double* __restrict__ out, long long rows, double* residue,
+                                                            const int* guard, const double2* __restrict__ master,
+                                                            const BatchLine* __restrict__ bl) {
+  using RP = C2RPlan<H>;
   using PL = Plan<H>;
-  constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL, NL = 2 * H;
+  constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL, NL = 2 * H, NT = RP::NT;
   if (guard && *guard != kNoBlowup) return;
   if (bl) {
     src = static_cast<const double2*>(bl[blockIdx.z].src);
@@ -233,17 +307,19 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
     out = bl[blockIdx.z].out;
   }
   extern __shared__ double2 sm[];
-  const int rl = threadIdx.x / TM, i = threadIdx.x % TM;
+  __shared__ unsigned tbase_sh;
+  double2* twpre = sm;
+  double2* tw1 = sm + (H + 1);
+  double2* tw2 = tw1 + RP::TW1;
+  double2* rsm = sm + RP::TWN;
+  const int tid = threadIdx.x;
+  const int rl = tid / TM, i = tid % TM;
   const long long row = (long long)blockIdx.x * RPB + rl;
   const bool live = row < rows;
-  double2* X = sm + rl * RP::XS;                            // natural-order X of this row
-  double2* Wk = sm + RPB * RP::XS + rl * PL::LS;           // FFT work (in-place layout)
-  double* devm = reinterpret_cast<double*>(sm + RPB * (RP::XS + PL::LS)) + (size_t)rl * NL;
-  double acc[2 * RL];
-#pragma unroll
-  for (int e = 0; e < 2 * RL; ++e) acc[e] = 0.0;
-  double rmax = 0.0;
-  const double* d1row = dev1 ? dev1 + row * NL : nullptr;
+  double2* X = rsm + rl * RP::XS;                  // natural-order X of this row
+  double2* Wk = rsm + RPB * RP::XS + rl * PL::LS;  // FFT work (in-place layout)
+
+  const double* d1row = dev1 ? dev1 + (live ? row : 0) * NL : nullptr;
   // X rows arrive by cp.async one term ahead: the next term's copy is issued as soon as
   // pass 0 of this term has read the buffer, and lands during the remaining passes
   auto fetch = [&](int m) {
@@ -257,6 +333,54 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   fetch(m_first);
+
+  // twiddle tables (values = master entries, as twiddle() / bfly() read them)
+  for (int e = tid; e <= H; e += NT) twpre[e] = master[e * (kTwMaster / (2 * H))];
+  for (int e = tid; e < RP::TW1; e += NT) {
+    constexpr int R = PL::R1, p = PL::R0;
+    const int k = e / (R - 1), r = e % (R - 1) + 1;
+    tw1[e] = master[(r * k) * (kTwMaster / (p * R))];
+  }
+  if constexpr (PL::P > 2) {
+    for (int e = tid; e < RP::TW2; e += NT) {
+      constexpr int R = PL::R2, p = PL::R0 * PL::R1;
+      const int k = e / (R - 1), r = e % (R - 1) + 1;
+      tw2[e] = master[(r * k) * (kTwMaster / (p * R))];
+    }
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tbase_sh)),
+                 "n"(RP::TMALLOC)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int warp = tid >> 5;
+  const unsigned tdev = tbase_sh + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * RP::TMC);
+  const unsigned tpow = tdev + 4 * RL;
+  if (d1row) {  // (s-s0) of this thread's outputs -> tensor memory, once
+#pragma unroll
+    for (int c4 = 0; c4 < RL / 4; ++c4) {
+      unsigned v[16];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int q = i + (4 * c4 + rr) * TL;
+        const double2 d = live ? __ldg(reinterpret_cast<const double2*>(d1row) + q) : make_double2(0.0, 0.0);
+        tm_set(v, 2 * rr, d.x);
+        tm_set(v, 2 * rr + 1, d.y);
+      }
+      tm_st16(tdev + 16 * c4, v);
+    }
+    tm_wait_st();
+  }
+
+  double acc[2 * RL];
+#pragma unroll
+  for (int e = 0; e < 2 * RL; ++e) acc[e] = 0.0;
+  double rmax = 0.0;
   for (int m = m_first; m <= m_last; ++m) {
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();  // X of term m complete; every thread is done with the previous term's work buffer
@@ -268,7 +392,7 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int q = i + r * T;
-          a[r] = c2r_pre(X[q], X[H - q], q, H, master);
+          a[r] = c2r_pre_w(X[q], X[H - q], q == 0, twpre[q]);
         }
         Dft<R, +1>::run(a);
 #pragma unroll
@@ -283,7 +407,7 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
         double2 a[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) a[r] = Wk[PL::p1(i, r)];
-        bfly<H, 1, +1>(a, i, master);
+        bfly_s<H, 1, +1>(a, i, tw1);
 #pragma unroll
         for (int r = 0; r < R; ++r) Wk[PL::p1(i, r)] = a[r];
       }
@@ -291,35 +415,45 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
     }
     {  // last pass -> outputs z_q, q = i + r TL: reals x[2q], x[2q+1]
       constexpr int LAST = PL::P - 1;
-      if (i < TL) {
-        double2 a[RL];
+      double2 a[RL];
 #pragma unroll
-        for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * TL)];
-        bfly<H, LAST, +1>(a, i, master);
+      for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * TL)];
+      bfly_s<H, LAST, +1>(a, i, LAST == 1 ? tw1 : tw2);
+      if (m == 0 || !d1row) {
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
-          const int q = i + r * TL;
+          double p0 = 0.0, p1 = 0.0;
+          p0 += a[r].x;
+          p1 += a[r].y;
+          acc[2 * r] += p0;
+          acc[2 * r + 1] += p1;
+        }
+      } else {
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const double x = c ? a[r].y : a[r].x;
-            double v;
-            if (m == 0 || !d1row) {
-              v = x;
-            } else {
-              const int j = 2 * q + c;
-              const double d = (m == 1) ? __ldg(&d1row[j]) : devm[j] * __ldg(&d1row[j]);
-              devm[j] = d;
-              v = d * x;
-            }
+        for (int c4 = 0; c4 < RL / 4; ++c4) {
+          unsigned dv[16], pv[16];
+          tm_ld16(tdev + 16 * c4, dv);
+          if (m > 1) tm_ld16(tpow + 16 * c4, pv);
+          tm_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {  // element e of the chunk: output r = 4 c4 + e / 2, real part e % 2
+            const int r = 4 * c4 + e / 2;
+            const double x = (e & 1) ? a[r].y : a[r].x;
+            double d = tm_get(dv, e);
+            if (m > 1) d = tm_get(pv, e) * d;  // (s-s0)^m = (s-s0)^{m-1} (s-s0)
+            tm_set(pv, e, d);
+            const double v = d * x;
             double p = 0.0;
             p += v;
-            acc[2 * r + c] += p;
+            acc[2 * r + (e & 1)] += p;
           }
+          tm_st16(tpow + 16 * c4, pv);
         }
+        tm_wait_st();
       }
     }
   }
-  if (live && i < TL) {
+  if (live) {
 #pragma unroll
     for (int r = 0; r < RL; ++r) {
       const int q = i + r * TL;
@@ -328,7 +462,25 @@ __global__ void __launch_bounds__(256) k_rows_c2r(const double2* __restrict__ sr
   }
   if (residue && live && i == 0 && rmax > 0.0)
     atomicMax(reinterpret_cast<unsigned long long*>(residue), (unsigned long long)__double_as_longlong(rmax));
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase_sh), "n"(RP::TMALLOC)
+                 : "memory");
 }
+
+// row plan of the R2C kernel (the block shape of the earlier shared-memory C2R)
+template <int H>
+struct RowPlan {
+  using P = Plan<H>;
+  static constexpr int TM = P::TMAX;
+  static constexpr int RL = radix(H, P::P - 1);
+  static constexpr int TL = H / RL;
+  static constexpr size_t ROWB = (size_t)(((H + 1) | 1) + P::LS) * sizeof(double2) + (size_t)2 * H * sizeof(double);
+  static constexpr int RPB = (256 / TM) * ROWB <= 112640 ? 256 / TM : (int)(112640 / ROWB);
+  static constexpr int NT = RPB * TM;
+};
 
 // Per row of the last axis: R2C of NL = 2H reals (z_j = x_2j + i x_2j+1, H-point C2C,
 // split X_k = f(Z_k, Z_{H-k})) into H+1 bins, x scale when do_scale.  Same plan/threads as
@@ -423,7 +575,7 @@ template <int H>
 bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m_first, int m_last,
                  const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
                  const BatchLine* bl) {
-  using RP = RowPlan<H>;
+  using RP = C2RPlan<H>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_rows_c2r<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RP::SMEM);

@@ -161,8 +161,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef FW_S2D_TWTM
 #define FW_S2D_TWTM 1
 #endif
+// seismic update inputs prefetched into L2 this many terms before the step's last term (0 = off)
+#ifndef FW_S2D_UPF
+#define FW_S2D_UPF 0
+#endif
 #if FW_STEP2D_TRACE
-#define FW_TRACE(t, slot)                                                                              \
+#define FW_TRACE(t, slot)                                                                            \
   do {                                                                                                 \
     if (prm.trace && (threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 100))               \
       prm.trace[(((size_t)(blockIdx.x == 0 ? 0 : 1) * 32 + (threadIdx.x >> 5)) * 136 + (t)) * 8 + (slot)] = \
@@ -929,6 +933,14 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       if (l_ == 0 && t + 1 < ntot) {  // the next term's (s-s0)^m row_ -> L2
         const double2* d = dev_row(t + 1, row_);
         if (d) prefetch_l2_hint(d, J1 * sizeof(double), pol_evict_first());
+      }
+      if (FW_S2D_UPF > 0 && prm.seismic && t == ntot - FW_S2D_UPF && l_ >= 1 && l_ <= 7) {
+        // the update's seven input rows (seismic.cpp:116-129) -> L2 while the last terms run:
+        // the update sits on the step's critical path and is otherwise HBM-latency bound
+        const bool ms = prm.nsteps > 1;
+        const double* src[7] = {ms ? lvl_u(s, 0) : prm.u, ms ? lvl_u(s, 2) : prm.prev, ms ? lvl_a(s, 1) : prm.ap,
+                                prm.out[0], prm.c, prm.eta, prm.tc};
+        prefetch_l2(src[l_ - 1] + (size_t)row_ * J1, J1 * sizeof(double));
       }
       mbar_wait(&tile_full, (unsigned)(s * ntot + t) & 1u);
       FW_TRACE(t, 2);
