@@ -157,43 +157,6 @@ __global__ void __launch_bounds__(256) k_lines(const double2* __restrict__ src, 
   }
 }
 
-template <int N>
-bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
-              long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
-              int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
-  constexpr int LPB = Plan<N>::L;
-  constexpr size_t SMEM = (size_t)LPB * Plan<N>::LS * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_lines<N, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(k_lines<N, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(k_lines<N, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(k_lines<N, +1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    attr = true;
-  }
-  const long long bpo = (inner + LPB - 1) / LPB;
-  const dim3 grid((unsigned)(outer * bpo), (unsigned)nterms, (unsigned)nfields);
-  const Scatter none{};
-  const Scatter& sc_ = scatter ? *scatter : none;
-  const int f = scale ? 1 : 0;
-  if (dir < 0) {
-    if (scatter)
-      k_lines<N, -1, true><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
-                                                           bl, sc_);
-    else
-      k_lines<N, -1, false><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
-                                                            L.master, bl, sc_);
-  } else {
-    if (scatter)
-      k_lines<N, +1, true><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
-                                                           bl, sc_);
-    else
-      k_lines<N, +1, false><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
-                                                            L.master, bl, sc_);
-  }
-  if (L.launches) *L.launches += 1;
-  return true;
-}
 
 // ---------------------------------------------------------------- tensor memory (per-thread state)
 // A warp reaches the 32 TMEM lanes of its quadrant (warp % 4); thread = lane, 32-bit columns.
@@ -470,6 +433,176 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
                  : "memory");
 }
 
+// All terms of an inverse along a strided axis in one pass over the spectrum: out_m =
+// C2C(w_m .* uhat) for m in the launch's term range (flap.cpp:64-71 weights fused into
+// pass 0).  Same thread mapping and arithmetic as k_lines<N, +1> with grid.y = terms, but a
+// block loops over the terms itself: its lines of uhat are read from HBM ONCE and parked in
+// tensor memory (pass-0 inputs of each thread), so a launch streams uhat once, w_m once and
+// writes the M+1 outputs (instead of re-reading uhat per term).  The next term's weights
+// are loaded while the current term's passes run.
+#ifndef FW_LT_PREFETCH
+#define FW_LT_PREFETCH 1  // next term's weights loaded during the current term's passes
+#endif
+template <int N>
+struct TermPlan {
+  using P = Plan<N>;
+  static constexpr int TW1 = P::P > 2 ? P::R0 * (P::R1 - 1) : 0;  // pass-1 twiddles of a 3-pass plan
+  static constexpr int TWL = pprod(N, P::P - 1) * (radix(N, P::P - 1) - 1);  // last pass
+  static constexpr int TWN = TW1 + TWL;
+  static constexpr size_t SMEM = (size_t)(TWN + P::L * P::LS) * sizeof(double2);
+  static constexpr int TMC = 4 * P::R0;  // columns per warp: R0 complex pass-0 inputs
+  static constexpr int TMALLOC = pow2ceil(2 * TMC < 32 ? 32 : 2 * TMC);  // 8 warps = 2 per quadrant
+};
+
+template <int N, bool SCAT>
+__global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                        const double* __restrict__ w, long long S, long long inner,
+                                                        long long dst_ts, long long w_ts, int nterms, double sc,
+                                                        int do_scale, const double2* __restrict__ master,
+                                                        const BatchLine* __restrict__ bl, const Scatter scat) {
+  using PL = Plan<N>;
+  using TP = TermPlan<N>;
+  constexpr int L = PL::L, R0 = PL::R0, T0 = PL::T0, LAST = PL::P - 1;
+  constexpr int RLST = radix(N, LAST), TLST = N / RLST;
+  extern __shared__ double2 sm[];
+  __shared__ unsigned tbase_sh;
+  if (bl) {
+    src = static_cast<const double2*>(bl[blockIdx.z].src);
+    if constexpr (!SCAT) dst = static_cast<double2*>(bl[blockIdx.z].dst);
+    w = bl[blockIdx.z].w;
+  }
+  double2* tw1 = sm;
+  double2* twl = sm + TP::TW1;
+  double2* lines_sm = sm + TP::TWN;
+  const int tid = threadIdx.x;
+  const long long bpo = (inner + L - 1) / L;
+  const long long o = blockIdx.x / bpo;
+  const long long in0 = (blockIdx.x - o * bpo) * L;
+  const int l = tid % L, i = tid / L;
+  const bool live = in0 + l < inner;
+  const long long base = o * (long long)N * S + in0 + l;
+  double2* line = lines_sm + l * PL::LS;
+
+  if constexpr (PL::P > 2) {
+    for (int e = tid; e < TP::TW1; e += 256) {
+      constexpr int R = PL::R1, p = PL::R0;
+      const int k = e / (R - 1), r = e % (R - 1) + 1;
+      tw1[e] = master[(r * k) * (kTwMaster / (p * R))];
+    }
+  }
+  for (int e = tid; e < TP::TWL; e += 256) {
+    constexpr int R = RLST, p = pprod(N, LAST);
+    const int k = e / (R - 1), r = e % (R - 1) + 1;
+    twl[e] = master[(r * k) * (kTwMaster / (p * R))];
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tbase_sh)),
+                 "n"(TP::TMALLOC)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int warp = tid >> 5;
+  const unsigned tu = tbase_sh + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * TP::TMC);
+  // pass-0 holders: i < T0 (warp-uniform: i = tid / L and T0 L is a multiple of 32)
+  static_assert((T0 * L) % 32 == 0, "warp-uniform pass-0 threads");
+  const bool p0 = i < T0;
+  double wk[R0];  // this term's weights (loaded one term ahead)
+  if (p0) {
+#pragma unroll
+    for (int c = 0; c < R0 / 4; ++c) {  // uhat -> tensor memory, 4 complex (16 columns) per store
+      unsigned v[16];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const long long idx = base + (long long)(i + (4 * c + rr) * T0) * S;
+        const double2 x = live ? src[idx] : make_double2(0.0, 0.0);
+        tm_set(v, 2 * rr, x.x);
+        tm_set(v, 2 * rr + 1, x.y);
+      }
+      tm_st16(tu + 16 * c, v);
+    }
+    tm_wait_st();
+#pragma unroll
+    for (int r = 0; r < R0; ++r) wk[r] = live ? __ldg(&w[base + (long long)(i + r * T0) * S]) : 0.0;
+  }
+  for (int term = 0; term < nterms; ++term) {
+    if (p0) {  // pass 0: w_m .* uhat (no twiddles)
+      if (!FW_LT_PREFETCH && term > 0) {
+        const double* wn = w + (long long)term * w_ts;
+#pragma unroll
+        for (int r = 0; r < R0; ++r) wk[r] = live ? __ldg(&wn[base + (long long)(i + r * T0) * S]) : 0.0;
+      }
+      double2 a[R0];
+#pragma unroll
+      for (int c = 0; c < R0 / 4; ++c) {
+        unsigned v[16];
+        tm_ld16(tu + 16 * c, v);
+        tm_wait_ld();
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const int r = 4 * c + rr;
+          a[r] = live ? make_double2(wk[r] * tm_get(v, 2 * rr), wk[r] * tm_get(v, 2 * rr + 1)) : make_double2(0.0, 0.0);
+        }
+      }
+      if (FW_LT_PREFETCH && term + 1 < nterms) {
+        const double* wn = w + (long long)(term + 1) * w_ts;
+#pragma unroll
+        for (int r = 0; r < R0; ++r) wk[r] = live ? __ldg(&wn[base + (long long)(i + r * T0) * S]) : 0.0;
+      }
+      Dft<R0, +1>::run(a);
+#pragma unroll
+      for (int r = 0; r < R0; ++r) line[PL::p0out(i * R0 + r)] = a[r];
+    }
+    __syncthreads();
+    if constexpr (PL::P == 3) {
+      constexpr int R = PL::R1, T = PL::T1;
+      if (i < T) {
+        double2 a[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) a[r] = line[PL::p1(i, r)];
+        bfly_s<N, 1, +1>(a, i, tw1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) line[PL::p1(i, r)] = a[r];
+      }
+      __syncthreads();
+    }
+    if (i < TLST) {  // last pass: shared -> registers -> global (natural order q = i + r T)
+      double2 a[RLST];
+#pragma unroll
+      for (int r = 0; r < RLST; ++r) a[r] = line[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * TLST)];
+      bfly_s<N, LAST, +1>(a, i, twl);
+      if (live) {
+#pragma unroll
+        for (int r = 0; r < RLST; ++r) {
+          double2 v = a[r];
+          if (do_scale) {
+            v.x *= sc;
+            v.y *= sc;
+          }
+          const int j = i + r * TLST;
+          if constexpr (SCAT) {
+            const int q = (int)(j / scat.blk);
+            scat.dst[q][term * scat.tstride + (j - q * scat.blk) * scat.jstride + o * scat.ostride + in0 + l +
+                        scat.base] = v;
+          } else {
+            dst[(long long)term * dst_ts + base + (long long)j * S] = v;
+          }
+        }
+      }
+    }
+    __syncthreads();  // the line buffer takes the next term's pass 0
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase_sh), "n"(TP::TMALLOC)
+                 : "memory");
+}
+
 // row plan of the R2C kernel (the block shape of the earlier shared-memory C2R)
 template <int H>
 struct RowPlan {
@@ -553,6 +686,66 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
       X[k] = v;
     }
   }
+}
+
+#ifndef FW_LINES_TERMS
+#define FW_LINES_TERMS 1  // 0: one block per (lines, term), uhat re-read per term
+#endif
+template <int N>
+bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
+              long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
+              int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
+  constexpr int LPB = Plan<N>::L;
+  constexpr size_t SMEM = (size_t)LPB * Plan<N>::LS * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lines<N, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, +1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    attr = true;
+  }
+  const long long bpo = (inner + LPB - 1) / LPB;
+  const Scatter none{};
+  const Scatter& sc_ = scatter ? *scatter : none;
+  const int f = scale ? 1 : 0;
+  if (FW_LINES_TERMS && dir > 0 && src_ts == 0 && nterms > 1 && (w || (bl && w_ts != 0))) {
+    // every term of an inverse from one uhat: one pass over the spectrum (k_lines_terms)
+    constexpr size_t TSM = TermPlan<N>::SMEM;
+    static bool tattr = false;
+    if (!tattr) {
+      cudaFuncSetAttribute(k_lines_terms<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
+      cudaFuncSetAttribute(k_lines_terms<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
+      tattr = true;
+    }
+    const dim3 tgrid((unsigned)(outer * bpo), 1, (unsigned)nfields);
+    if (scatter)
+      k_lines_terms<N, true><<<tgrid, 256, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, sc, f,
+                                                             L.master, bl, sc_);
+    else
+      k_lines_terms<N, false><<<tgrid, 256, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, sc, f,
+                                                              L.master, bl, sc_);
+    if (L.launches) *L.launches += 1;
+    return true;
+  }
+  const dim3 grid((unsigned)(outer * bpo), (unsigned)nterms, (unsigned)nfields);
+  if (dir < 0) {
+    if (scatter)
+      k_lines<N, -1, true><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
+                                                           bl, sc_);
+    else
+      k_lines<N, -1, false><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
+                                                            L.master, bl, sc_);
+  } else {
+    if (scatter)
+      k_lines<N, +1, true><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
+                                                           bl, sc_);
+    else
+      k_lines<N, +1, false><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
+                                                            L.master, bl, sc_);
+  }
+  if (L.launches) *L.launches += 1;
+  return true;
 }
 
 template <int H>
