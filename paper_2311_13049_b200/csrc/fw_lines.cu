@@ -66,10 +66,17 @@ __device__ __forceinline__ void bfly(double2* a, int i, const double2* __restric
   Dft<R, DIR>::run(a);
 }
 
+// blocks per SM the register allocation of k_lines<N> is bounded for (shared memory allows 3
+// at N = 256, 6 at N = 512 / 1024)
+#ifndef FW_LINES_MINB256
+#define FW_LINES_MINB256 3
+#endif
+__host__ __device__ constexpr int lines_minb(int n) { return n == 256 ? FW_LINES_MINB256 : 1; }
+
 // C2C of lines of length N along an axis of stride S (line (o, in): o*N*S + in + j*S).
 // blockIdx.y = term (src/dst/w advance by their term strides), blockIdx.z = field (bl).
 template <int N, int DIR, bool SCAT>
-__global__ void __launch_bounds__(256) k_lines(const double2* __restrict__ src, double2* __restrict__ dst,
+__global__ void __launch_bounds__(256, lines_minb(N)) k_lines(const double2* __restrict__ src, double2* __restrict__ dst,
                                                const double* __restrict__ w, long long S, long long inner,
                                                long long src_ts, long long dst_ts, long long w_ts, double sc,
                                                int do_scale, const double2* __restrict__ master,
@@ -223,6 +230,9 @@ __device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, do
 // the running power (s-s0)^{m-1} of the thread's outputs live in TENSOR MEMORY (loaded
 // once per launch), the twiddles in one shared-memory table per block; the next term's
 // row lands by cp.async while the current term's passes run.
+#ifndef FW_C2R_XB2
+#define FW_C2R_XB2 0  // measured: no gain at C3 (the kernel is not fetch-latency bound)
+#endif
 #ifndef FW_C2R_MINB
 #define FW_C2R_MINB 2  // blocks per SM the register allocation is bounded for
 #endif
@@ -243,7 +253,9 @@ struct C2RPlan {
                                  ? 256 / TM
                                  : (int)((CAP - TWN * sizeof(double2)) / ROWB);
   static constexpr int NT = RPB * TM;
-  static constexpr size_t SMEM = (size_t)TWN * sizeof(double2) + (size_t)RPB * ROWB;
+  // X rows double-buffered (next term and the one after in flight) when that keeps RPB
+  static constexpr int NXB = FW_C2R_XB2 && (size_t)TWN * sizeof(double2) + (size_t)RPB * (ROWB + XS * sizeof(double2)) <= CAP ? 2 : 1;
+  static constexpr size_t SMEM = (size_t)TWN * sizeof(double2) + (size_t)RPB * (ROWB + (NXB - 1) * XS * sizeof(double2));
   // tensor memory per warp: (s-s0) at [0, 4 RL), (s-s0)^{m-1} at [4 RL, 8 RL) (two columns per double)
   static constexpr int TMC = 8 * RL;
   static constexpr int NSLOT = (NT / 32 + 3) / 4;
@@ -279,15 +291,17 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
   const int rl = tid / TM, i = tid % TM;
   const long long row = (long long)blockIdx.x * RPB + rl;
   const bool live = row < rows;
-  double2* X = rsm + rl * RP::XS;                  // natural-order X of this row
-  double2* Wk = rsm + RPB * RP::XS + rl * PL::LS;  // FFT work (in-place layout)
+  constexpr int NXB = RP::NXB;
+  double2* Xb = rsm + rl * RP::XS;                       // natural-order X of this row (NXB buffers)
+  double2* Wk = rsm + NXB * RPB * RP::XS + rl * PL::LS;  // FFT work (in-place layout)
 
   const double* d1row = dev1 ? dev1 + (live ? row : 0) * NL : nullptr;
-  // X rows arrive by cp.async one term ahead: the next term's copy is issued as soon as
-  // pass 0 of this term has read the buffer, and lands during the remaining passes
+  // X rows arrive by cp.async NXB terms ahead: a buffer is refilled as soon as pass 0 of its
+  // term has read it, and lands during the following terms' passes (one commit group per term)
   auto fetch = [&](int m) {
     if (live && m <= m_last) {
       const double2* S = src + (long long)(m - m_first) * src_ts + row * (H + 1);
+      double2* X = Xb + ((m - m_first) % NXB) * RPB * RP::XS;
       for (int k = i; k <= H; k += TM)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(&X[k])),
                      "l"(S + k)
@@ -296,6 +310,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   fetch(m_first);
+  if (NXB > 1) fetch(m_first + 1);
 
   // twiddle tables (values = master entries, as twiddle() / bfly() read them)
   for (int e = tid; e <= H; e += NT) twpre[e] = master[e * (kTwMaster / (2 * H))];
@@ -345,8 +360,12 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
   for (int e = 0; e < 2 * RL; ++e) acc[e] = 0.0;
   double rmax = 0.0;
   for (int m = m_first; m <= m_last; ++m) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (NXB > 1)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // term m landed (m + 1 may be in flight)
+    else
+      asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();  // X of term m complete; every thread is done with the previous term's work buffer
+    const double2* X = Xb + ((m - m_first) % NXB) * RPB * RP::XS;
     if (residue && live && i == 0) rmax = fmax(rmax, fabs(X[0].y) + fabs(X[H].y));
     {  // C2R pre-processing + pass 0 (no twiddles) -> work
       constexpr int R = PL::R0, T = PL::T0;
@@ -363,7 +382,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
       }
     }
     __syncthreads();
-    fetch(m + 1);  // X is free again
+    fetch(m + NXB);  // X is free again
     if constexpr (PL::P == 3) {
       constexpr int R = PL::R1, T = PL::T1;
       if (i < T) {
