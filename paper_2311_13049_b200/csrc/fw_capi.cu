@@ -703,6 +703,11 @@ struct fw_seis_s {
   double* abuf[2] = {nullptr, nullptr};
   double* l1 = nullptr;
   int* flag = nullptr;
+  // multi-pass step: both operators' inverses batched (grid.z = operator); device tables for the
+  // two parities of the L2 output buffer, rebuilt when the scratch they point into moves
+  fw::BatchLine* btab = nullptr;
+  const void* btab_uh = nullptr;
+  const void* btab_T = nullptr;
   long n = 0;    // reported step count (SeismicStepper::n)
   long lvl = 0;  // index of the current level for buffer rotation
   double* cur() { return ubuf[lvl % 3]; }
@@ -719,6 +724,7 @@ void seis_free(fw_seis s) {
   for (double* p : {s->c, s->eta, s->tc, s->ubuf[0], s->ubuf[1], s->ubuf[2], s->abuf[0], s->abuf[1], s->l1})
     if (p) cudaFree(p);
   if (s->flag) cudaFree(s->flag);
+  if (s->btab) cudaFree(s->btab);
   delete s;
 }
 
@@ -784,8 +790,35 @@ int seis_enqueue_step(fw_seis s) {
   FW_TRY(ctx->get_scratch(SLOT_UH2, g.Nh * sizeof(double2), &uh));
   // shared forward transform of cur for both operators
   fw::launch_forward(L, g, cur, (double2*)uh, true);
-  FW_TRY(apply_device(s->A1, cur, s->l1, 0, nullptr, nullptr, (const double2*)uh));
-  FW_TRY(apply_device(s->A2, cur, l2, 0, nullptr, s->flag, (const double2*)uh));
+  if (g.d >= 2 && s->A1->M == s->A2->M && s->A1->constant_order == s->A2->constant_order) {
+    // both inverses in one batched pipeline (grid.z = operator): twice the blocks per launch
+    const int m_last = s->A1->constant_order ? 0 : s->A1->M;
+    const size_t per_op = (size_t)(m_last + 1) * g.Nh * sizeof(double2);
+    void* T = nullptr;
+    FW_TRY(ctx->get_scratch(SLOT_BT, 2 * per_op, &T));
+    if (!s->btab) FW_TRY(dalloc(&s->btab, 12));
+    if (s->btab_uh != uh || s->btab_T != T) {
+      std::vector<fw::BatchLine> h(12);
+      fw_op ops[2] = {s->A1, s->A2};
+      for (int par = 0; par < 2; ++par)
+        for (int o = 0; o < 2; ++o) {
+          double2* To = reinterpret_cast<double2*>(static_cast<char*>(T) + (size_t)o * per_op);
+          double* out = o == 0 ? s->l1 : s->abuf[par];
+          h[par * 6 + 0 + o] = {uh, To, ops[o]->w, nullptr, nullptr};        // inverse axis 0 (x w_m)
+          h[par * 6 + 2 + o] = {To, To, nullptr, nullptr, nullptr};          // axes 1..d-2
+          h[par * 6 + 4 + o] = {To, nullptr, nullptr, ops[o]->dev1, out};   // C2R + recombination
+        }
+      FW_CUDA(cudaMemcpyAsync(s->btab, h.data(), h.size() * sizeof(fw::BatchLine), cudaMemcpyHostToDevice,
+                              ctx->stream));
+      s->btab_uh = uh;
+      s->btab_T = T;
+    }
+    const fw::BatchLine* t = s->btab + (s->lvl % 2) * 6;
+    fw::launch_inverse_batch(L, g, 2, 0, m_last, t, t + 2, t + 4, s->flag);
+  } else {
+    FW_TRY(apply_device(s->A1, cur, s->l1, 0, nullptr, nullptr, (const double2*)uh));
+    FW_TRY(apply_device(s->A2, cur, l2, 0, nullptr, s->flag, (const double2*)uh));
+  }
   fw::launch_seis_update(L, g.N, s->tau, cur, s->prev(), s->ap(), s->l1, l2, s->c, s->eta, s->tc, next, s->thr,
                          (int)(s->n + 1), s->flag);
   s->n += 1;

@@ -108,7 +108,8 @@ void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const Ba
 // inverse + recombination for F fields of one grid and term range:
 // tab0[f] = {Uh_f, T_f, w_f + m_first Nh}, tab1[f] = {T_f, T_f} (axes 1..d-2), tab2[f] = {T_f, -, -, dev1_f, out_f}
 void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_first, int m_last,
-                          const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2);
+                          const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2,
+                          const int* guard = nullptr);
 
 // fused transpose: the last pass of a line C2C writes output element j of line (o, in), term t
 // to dst[q] + t tstride + (j - q blk) jstride + o ostride + in + base, q = j / blk -- the

@@ -525,7 +525,7 @@ void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const Ba
 }
 
 void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_first, int m_last,
-                          const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2) {
+                          const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2, const int* guard) {
   const int nterms = m_last - m_first + 1;
   for (int a = 0; a <= g.d - 2; ++a) {
     const int n = g.J[a];
@@ -545,14 +545,14 @@ void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_fi
     count(L);
   }
   if (!L.generic_lines && launch_rows_c2r(L, g.nl, nullptr, (long long)g.Nh, m_first, m_last, nullptr, nullptr,
-                                         (long long)g.rows, F, nullptr, nullptr, tab2))
+                                         (long long)g.rows, F, nullptr, guard, tab2))
     return;
   const int h = g.nl / 2;
   const int lpb = std::max(1, std::min(8, 4096 / g.nl));
   const unsigned nb = (unsigned)((g.rows + lpb - 1) / lpb);
   k_c2r_accum<<<dim3(nb, 1, F), kThreads, smem_bytes(h + 1, lpb), L.stream>>>(
       nullptr, (long long)g.Nh, nullptr, 0, m_first, m_last, nullptr, nullptr, g.nl, (long long)g.rows, lpb, nullptr,
-      nullptr, L.master, tab2);
+      guard, L.master, tab2);
   count(L);
 }
 

@@ -13,6 +13,8 @@
 // fma placement).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "fw_fft.cuh"
 #include "fw_internal.h"
 
@@ -476,8 +478,8 @@ struct TermPlan {
 template <int N, bool SCAT>
 __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
                                                         const double* __restrict__ w, long long S, long long inner,
-                                                        long long dst_ts, long long w_ts, int nterms, double sc,
-                                                        int do_scale, const double2* __restrict__ master,
+                                                        long long dst_ts, long long w_ts, int nterms, int tchunk,
+                                                        double sc, int do_scale, const double2* __restrict__ master,
                                                         const BatchLine* __restrict__ bl, const Scatter scat) {
   using PL = Plan<N>;
   using TP = TermPlan<N>;
@@ -490,6 +492,9 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
     if constexpr (!SCAT) dst = static_cast<double2*>(bl[blockIdx.z].dst);
     w = bl[blockIdx.z].w;
   }
+  // this block's terms [t0, t1) (blockIdx.y = chunk: small grids split the term range)
+  const int t0 = blockIdx.y * tchunk, t1 = min(nterms, t0 + tchunk);
+  w += (long long)t0 * w_ts;
   double2* tw1 = sm;
   double2* twl = sm + TP::TW1;
   double2* lines_sm = sm + TP::TWN;
@@ -547,10 +552,10 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
 #pragma unroll
     for (int r = 0; r < R0; ++r) wk[r] = live ? __ldg(&w[base + (long long)(i + r * T0) * S]) : 0.0;
   }
-  for (int term = 0; term < nterms; ++term) {
+  for (int term = t0; term < t1; ++term) {
     if (p0) {  // pass 0: w_m .* uhat (no twiddles)
-      if (!FW_LT_PREFETCH && term > 0) {
-        const double* wn = w + (long long)term * w_ts;
+      if (!FW_LT_PREFETCH && term > t0) {
+        const double* wn = w + (long long)(term - t0) * w_ts;
 #pragma unroll
         for (int r = 0; r < R0; ++r) wk[r] = live ? __ldg(&wn[base + (long long)(i + r * T0) * S]) : 0.0;
       }
@@ -566,8 +571,8 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
           a[r] = live ? make_double2(wk[r] * tm_get(v, 2 * rr), wk[r] * tm_get(v, 2 * rr + 1)) : make_double2(0.0, 0.0);
         }
       }
-      if (FW_LT_PREFETCH && term + 1 < nterms) {
-        const double* wn = w + (long long)(term + 1) * w_ts;
+      if (FW_LT_PREFETCH && term + 1 < t1) {
+        const double* wn = w + (long long)(term + 1 - t0) * w_ts;
 #pragma unroll
         for (int r = 0; r < R0; ++r) wk[r] = live ? __ldg(&wn[base + (long long)(i + r * T0) * S]) : 0.0;
       }
@@ -707,6 +712,9 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
   }
 }
 
+#ifndef FW_LT_TARGET
+#define FW_LT_TARGET 1184  // blocks the all-terms inverse aims for (4 waves x 2 blocks x 148 SMs)
+#endif
 #ifndef FW_LINES_TERMS
 #define FW_LINES_TERMS 1  // 0: one block per (lines, term), uhat re-read per term
 #endif
@@ -737,13 +745,18 @@ bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, con
       cudaFuncSetAttribute(k_lines_terms<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
       tattr = true;
     }
-    const dim3 tgrid((unsigned)(outer * bpo), 1, (unsigned)nfields);
+    // enough blocks to fill the GPU: split the term range when the lines alone give fewer than
+    // ~4 waves of two blocks per SM (uhat is then read once per chunk)
+    const long long nb = outer * bpo * nfields;
+    const int nchunk = (int)std::min<long long>(nterms, std::max<long long>(1, (FW_LT_TARGET + nb - 1) / nb));
+    const int tchunk = (nterms + nchunk - 1) / nchunk;
+    const dim3 tgrid((unsigned)(outer * bpo), (unsigned)((nterms + tchunk - 1) / tchunk), (unsigned)nfields);
     if (scatter)
-      k_lines_terms<N, true><<<tgrid, 256, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, sc, f,
-                                                             L.master, bl, sc_);
+      k_lines_terms<N, true><<<tgrid, 256, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, tchunk, sc,
+                                                             f, L.master, bl, sc_);
     else
-      k_lines_terms<N, false><<<tgrid, 256, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, sc, f,
-                                                              L.master, bl, sc_);
+      k_lines_terms<N, false><<<tgrid, 256, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, tchunk,
+                                                              sc, f, L.master, bl, sc_);
     if (L.launches) *L.launches += 1;
     return true;
   }
