@@ -587,3 +587,38 @@ def test_slab_seismic_stepper_equals_single_gpu(P):
     assert sts[0].n == n_r
     for a, b in zip(got, (cur_r, prev_r, ap_r)):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("J", [(32, 64), (16, 32, 16)])
+def test_multipass_batched_step_blowup_matches_restatement(J):
+    """2D/3D multi-pass seismic step (both operators' inverses batched, grid.z = operator,
+    the C2R guarded by the blow-up flag): same offending step and pre-step state as the
+    restatement of seismic.cpp:111-133, and bit-identical states before the blow-up."""
+    m = fw()
+    d = len(J)
+    lo, hi = (-4.0,) * d, (4.0,) * d
+    axes = [lo[a] + np.arange(J[a]) * (8.0 / J[a]) for a in range(d)]
+    r2 = sum(np.meshgrid(*[x**2 for x in axes], indexing="ij"))
+    phi = np.exp(-r2)
+    rng = np.random.default_rng(7)
+    gamma = 0.02 + 0.06 * rng.random(J)
+    ctx = generic_context()
+    med = m.build_medium(grid_of(J, lo, hi), gamma, np.ones(J), 1.0, 5)
+    # stable run: bitwise after 12 steps
+    cur_r, prev_r, ap_r, n_r = O.port_seismic(J, lo, hi, gamma, np.ones(J), 1.0, 5, phi, np.zeros(J), 1e-3, 12)
+    st = m.SeismicStepper(med, phi, np.zeros(J), 1e-3, ctx=ctx)
+    st.advance(12)
+    cur, prev, ap, n = st.state()
+    assert n == n_r == 13  # SeismicStepper::n counts the start step
+    assert np.array_equal(cur, cur_r) and np.array_equal(prev, prev_r) and np.array_equal(ap, ap_r)
+    # unstable run: the same offending step and pre-step state
+    tau = 0.35
+    cur_r, prev_r, ap_r, n_r, rc = O.port_seismic(J, lo, hi, gamma, np.ones(J), 1.0, 5, phi, np.zeros(J), tau, 400,
+                                                  allow_blowup=True)
+    assert rc == 7
+    st = m.SeismicStepper(med, phi, np.zeros(J), tau, ctx=ctx)
+    with pytest.raises(m.BlowupDetected):
+        st.advance(400)
+    cur, prev, ap, n = st.state()
+    assert n == n_r
+    assert np.array_equal(cur, cur_r) and np.array_equal(prev, prev_r) and np.array_equal(ap, ap_r)
