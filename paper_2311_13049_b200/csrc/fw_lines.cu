@@ -73,7 +73,15 @@ __device__ __forceinline__ void bfly(double2* a, int i, const double2* __restric
 #ifndef FW_LINES_MINB256
 #define FW_LINES_MINB256 3
 #endif
-__host__ __device__ constexpr int lines_minb(int n) { return n == 256 ? FW_LINES_MINB256 : 1; }
+#ifndef FW_LINES_MINB512
+#define FW_LINES_MINB512 4
+#endif
+#ifndef FW_LINES_MINB1024
+#define FW_LINES_MINB1024 2
+#endif
+__host__ __device__ constexpr int lines_minb(int n) {
+  return n == 256 ? FW_LINES_MINB256 : n == 512 ? FW_LINES_MINB512 : FW_LINES_MINB1024;
+}
 
 // C2C of lines of length N along an axis of stride S (line (o, in): o*N*S + in + j*S).
 // blockIdx.y = term (src/dst/w advance by their term strides), blockIdx.z = field (bl).
