@@ -200,6 +200,15 @@ __device__ __forceinline__ void tm_set(unsigned* v, int k, double x) {
   v[2 * k + 1] = (unsigned)__double2hiint(x);
 }
 
+// the reference's per-term partial 0.0 + v (flap.cpp:83-89: partials start from a zeroed
+// vector; differs from v only for v = -0.0).  An integer form that keeps the fp64 pipe free
+// measured no faster.
+__device__ __forceinline__ double zero_plus(double v) {
+  double p = 0.0;
+  p += v;
+  return p;
+}
+
 // twiddled butterfly of pass PASS with the twiddles from a shared-memory table [k][r-1]
 // (values = master entries: bit-identical to bfly())
 template <int N, int PASS, int DIR>
@@ -414,11 +423,8 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
       if (m == 0 || !d1row) {
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
-          double p0 = 0.0, p1 = 0.0;
-          p0 += a[r].x;
-          p1 += a[r].y;
-          acc[2 * r] += p0;
-          acc[2 * r + 1] += p1;
+          acc[2 * r] += zero_plus(a[r].x);
+          acc[2 * r + 1] += zero_plus(a[r].y);
         }
       } else {
 #pragma unroll
@@ -434,10 +440,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
             double d = tm_get(dv, e);
             if (m > 1) d = tm_get(pv, e) * d;  // (s-s0)^m = (s-s0)^{m-1} (s-s0)
             tm_set(pv, e, d);
-            const double v = d * x;
-            double p = 0.0;
-            p += v;
-            acc[2 * r + (e & 1)] += p;
+            acc[2 * r + (e & 1)] += zero_plus(d * x);
           }
           tm_st16(tpow + 16 * c4, pv);
         }
