@@ -249,6 +249,9 @@ __device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, do
 // the running power (s-s0)^{m-1} of the thread's outputs live in TENSOR MEMORY (loaded
 // once per launch), the twiddles in one shared-memory table per block; the next term's
 // row lands by cp.async while the current term's passes run.
+#ifndef FW_C2R_PAD
+#define FW_C2R_PAD 1  // 0: Plan<H>'s line padding in the row C2R (A/B)
+#endif
 #ifndef FW_C2R_XB2
 #define FW_C2R_XB2 0  // measured: no gain at C3 (the kernel is not fetch-latency bound)
 #endif
@@ -266,7 +269,21 @@ struct C2RPlan {
   static constexpr int TW1 = P::R0 * (P::R1 - 1);
   static constexpr int TW2 = P::P > 2 ? P::R0 * P::R1 * (P::R2 - 1) : 0;
   static constexpr int TWN = (H + 1) + TW1 + TW2;
-  static constexpr size_t ROWB = (size_t)(XS + P::LS) * sizeof(double2);
+  // work layout: the in-place-per-butterfly positions of Plan<H> with a padding chosen for this
+  // kernel's row-major thread mapping (Plan's padding suits the line-fastest mapping of k_lines
+  // and gives 2-way conflicts in the last pass here): one pad term p >> PADA makes every pass
+  // bank-conflict-free at h = 128 / 256 (checked by enumerating the quarter-warp bank groups of
+  // each access); h = 512 keeps Plan's padding (already conflict-free)
+  static constexpr int PADA = !FW_C2R_PAD ? 0 : H == 128 ? 3 : H == 256 ? 4 : 0;
+  __device__ static __forceinline__ int pad(int p) { return PADA ? p + (p >> PADA) : P::pad(p); }
+  static constexpr int LS = PADA ? (((H - 1) + ((H - 1) >> PADA) + 1) | 1) : P::LS;
+  __device__ static __forceinline__ int p0out(int e) { return pad((e % P::T1) * P::R1 + e / P::T1); }
+  __device__ static __forceinline__ int p1(int i, int r) { return pad(i * P::R1 + r); }
+  __device__ static __forceinline__ int p2in(int e) {
+    const int i1 = (e / (P::R0 * P::R1)) * P::R0 + e % P::R0, r1 = (e / P::R0) % P::R1;
+    return pad(i1 * P::R1 + r1);
+  }
+  static constexpr size_t ROWB = (size_t)(XS + LS) * sizeof(double2);
   static constexpr size_t CAP = 112640;  // two blocks per SM
   static constexpr int RPB = (size_t)(256 / TM) * ROWB + TWN * sizeof(double2) <= CAP
                                  ? 256 / TM
@@ -312,7 +329,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
   const bool live = row < rows;
   constexpr int NXB = RP::NXB;
   double2* Xb = rsm + rl * RP::XS;                       // natural-order X of this row (NXB buffers)
-  double2* Wk = rsm + NXB * RPB * RP::XS + rl * PL::LS;  // FFT work (in-place layout)
+  double2* Wk = rsm + NXB * RPB * RP::XS + rl * RP::LS;  // FFT work (in-place layout)
 
   const double* d1row = dev1 ? dev1 + (live ? row : 0) * NL : nullptr;
   // X rows arrive by cp.async NXB terms ahead: a buffer is refilled as soon as pass 0 of its
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
         }
         Dft<R, +1>::run(a);
 #pragma unroll
-        for (int r = 0; r < R; ++r) Wk[PL::p0out(i * R + r)] = a[r];
+        for (int r = 0; r < R; ++r) Wk[RP::p0out(i * R + r)] = a[r];
       }
     }
     __syncthreads();
@@ -407,10 +424,10 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
       if (i < T) {
         double2 a[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) a[r] = Wk[PL::p1(i, r)];
+        for (int r = 0; r < R; ++r) a[r] = Wk[RP::p1(i, r)];
         bfly_s<H, 1, +1>(a, i, tw1);
 #pragma unroll
-        for (int r = 0; r < R; ++r) Wk[PL::p1(i, r)] = a[r];
+        for (int r = 0; r < R; ++r) Wk[RP::p1(i, r)] = a[r];
       }
       __syncthreads();
     }
@@ -418,7 +435,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const 
       constexpr int LAST = PL::P - 1;
       double2 a[RL];
 #pragma unroll
-      for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * TL)];
+      for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? RP::p1(i, r) : RP::p2in(i + r * TL)];
       bfly_s<H, LAST, +1>(a, i, LAST == 1 ? tw1 : tw2);
       if (m == 0 || !d1row) {
 #pragma unroll

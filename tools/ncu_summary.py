@@ -10,8 +10,11 @@ import sys
 rep = sys.argv[1]
 
 
+KF = ["-k", "regex:" + sys.argv[2]] if len(sys.argv) > 2 else []
+
+
 def ncu(*args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *KF, *args], capture_output=True, text=True).stdout
 
 
 raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
