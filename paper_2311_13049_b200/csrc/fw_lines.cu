@@ -29,6 +29,9 @@ __host__ __device__ constexpr int radix(int n, int i) {
 __host__ __device__ constexpr int pprod(int n, int i) { return i == 0 ? 1 : pprod(n, i - 1) * radix(n, i - 1); }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
+#ifndef FW_LINES_SWZ
+#define FW_LINES_SWZ 1
+#endif
 template <int N>
 struct Plan {
   static constexpr int P = npass(N);
@@ -47,6 +50,27 @@ struct Plan {
   __device__ static __forceinline__ int p2in(int e) {
     const int i1 = (e / (R0 * R1)) * R0 + e % R0, r1 = (e / R0) % R1;
     return pad(i1 * R1 + r1);
+  }
+  // line kernels (line-fastest thread mapping, L lines per block): logical in-place slot p of
+  // line l at lpos(l, p).  n = 512 / 1024: unpadded lines with an XOR swizzle of the 16-B slot
+  // within its 128-B group (every pass bank-conflict-free, checked by enumerating the
+  // quarter-warp bank groups of each access; the padding above gives 2-way conflicts there);
+  // n = 256: the padding above (already conflict-free)
+  // (the XOR term reads only bits >= 3 of p, so it permutes slots within their 8-slot group)
+  static constexpr int SWA = N == 512 || N == 1024 ? 3 : 0, SWB = N == 512 ? 6 : N == 1024 ? 7 : 0;
+  static constexpr int SWL = N == 512 ? 2 : 4;
+  static constexpr int LLS = (FW_LINES_SWZ && SWA) ? N : LS;
+  __device__ static __forceinline__ int lpos(int l, int p) {
+    if constexpr (FW_LINES_SWZ && SWA != 0)
+      return l * N + (p ^ ((((p >> SWA) ^ (p >> SWB)) + SWL * l) & 7));
+    else
+      return l * LS + pad(p);
+  }
+  __device__ static __forceinline__ int q0out(int e) { return (e % T1) * R1 + e / T1; }
+  __device__ static __forceinline__ int q1(int i, int r) { return i * R1 + r; }
+  __device__ static __forceinline__ int q2in(int e) {
+    const int i1 = (e / (R0 * R1)) * R0 + e % R0, r1 = (e / R0) % R1;
+    return i1 * R1 + r1;
   }
   static_assert(P == 2 || P == 3, "2- or 3-pass plans");
   static_assert(L >= 1 && L * TMAX == 256, "256 threads");
@@ -109,7 +133,7 @@ __global__ void __launch_bounds__(256, lines_minb(N)) k_lines(const double2* __r
   const int l = threadIdx.x % L, i = threadIdx.x / L;
   const bool live = in0 + l < inner;
   const long long base = o * (long long)N * S + in0 + l;
-  double2* line = sm + l * PL::LS;
+  double2* line = sm;  // slot p of this thread's line at PL::lpos(l, p)
 
   {  // pass 0 (no twiddles): global -> registers -> shared
     constexpr int R = PL::R0, T = PL::T0;
@@ -128,7 +152,7 @@ __global__ void __launch_bounds__(256, lines_minb(N)) k_lines(const double2* __r
       }
       Dft<R, DIR>::run(a);
 #pragma unroll
-      for (int r = 0; r < R; ++r) line[PL::p0out(i * R + r)] = a[r];
+      for (int r = 0; r < R; ++r) line[PL::lpos(l, PL::q0out(i * R + r))] = a[r];
     }
   }
   __syncthreads();
@@ -137,10 +161,10 @@ __global__ void __launch_bounds__(256, lines_minb(N)) k_lines(const double2* __r
     if (i < T) {
       double2 a[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[r] = line[PL::p1(i, r)];
+      for (int r = 0; r < R; ++r) a[r] = line[PL::lpos(l, PL::q1(i, r))];
       bfly<N, 1, DIR>(a, i, master);
 #pragma unroll
-      for (int r = 0; r < R; ++r) line[PL::p1(i, r)] = a[r];
+      for (int r = 0; r < R; ++r) line[PL::lpos(l, PL::q1(i, r))] = a[r];
     }
     __syncthreads();
   }
@@ -150,7 +174,7 @@ __global__ void __launch_bounds__(256, lines_minb(N)) k_lines(const double2* __r
     if (i < T) {
       double2 a[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[r] = line[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * T)];
+      for (int r = 0; r < R; ++r) a[r] = line[PL::lpos(l, LAST == 1 ? PL::q1(i, r) : PL::q2in(i + r * T))];
       bfly<N, LAST, DIR>(a, i, master);
       if (live) {
 #pragma unroll
@@ -498,7 +522,7 @@ struct TermPlan {
   static constexpr int TW1 = P::P > 2 ? P::R0 * (P::R1 - 1) : 0;  // pass-1 twiddles of a 3-pass plan
   static constexpr int TWL = pprod(N, P::P - 1) * (radix(N, P::P - 1) - 1);  // last pass
   static constexpr int TWN = TW1 + TWL;
-  static constexpr size_t SMEM = (size_t)(TWN + P::L * P::LS) * sizeof(double2);
+  static constexpr size_t SMEM = (size_t)(TWN + P::L * P::LLS) * sizeof(double2);
   static constexpr int TMC = 4 * P::R0;  // columns per warp: R0 complex pass-0 inputs
   static constexpr int TMALLOC = pow2ceil(2 * TMC < 32 ? 32 : 2 * TMC);  // 8 warps = 2 per quadrant
 };
@@ -533,7 +557,7 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
   const int l = tid % L, i = tid / L;
   const bool live = in0 + l < inner;
   const long long base = o * (long long)N * S + in0 + l;
-  double2* line = lines_sm + l * PL::LS;
+  double2* line = lines_sm;  // slot p of this thread's line at PL::lpos(l, p)
 
   if constexpr (PL::P > 2) {
     for (int e = tid; e < TP::TW1; e += 256) {
@@ -606,7 +630,7 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
       }
       Dft<R0, +1>::run(a);
 #pragma unroll
-      for (int r = 0; r < R0; ++r) line[PL::p0out(i * R0 + r)] = a[r];
+      for (int r = 0; r < R0; ++r) line[PL::lpos(l, PL::q0out(i * R0 + r))] = a[r];
     }
     __syncthreads();
     if constexpr (PL::P == 3) {
@@ -614,17 +638,17 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
       if (i < T) {
         double2 a[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) a[r] = line[PL::p1(i, r)];
+        for (int r = 0; r < R; ++r) a[r] = line[PL::lpos(l, PL::q1(i, r))];
         bfly_s<N, 1, +1>(a, i, tw1);
 #pragma unroll
-        for (int r = 0; r < R; ++r) line[PL::p1(i, r)] = a[r];
+        for (int r = 0; r < R; ++r) line[PL::lpos(l, PL::q1(i, r))] = a[r];
       }
       __syncthreads();
     }
     if (i < TLST) {  // last pass: shared -> registers -> global (natural order q = i + r T)
       double2 a[RLST];
 #pragma unroll
-      for (int r = 0; r < RLST; ++r) a[r] = line[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * TLST)];
+      for (int r = 0; r < RLST; ++r) a[r] = line[PL::lpos(l, LAST == 1 ? PL::q1(i, r) : PL::q2in(i + r * TLST))];
       bfly_s<N, LAST, +1>(a, i, twl);
       if (live) {
 #pragma unroll
@@ -751,7 +775,7 @@ bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, con
               long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
               int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
   constexpr int LPB = Plan<N>::L;
-  constexpr size_t SMEM = (size_t)LPB * Plan<N>::LS * sizeof(double2);
+  constexpr size_t SMEM = (size_t)LPB * Plan<N>::LLS * sizeof(double2);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_lines<N, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
