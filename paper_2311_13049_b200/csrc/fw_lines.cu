@@ -701,6 +701,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
                                                   const BatchLine* __restrict__ bl) {
   using RP = RowPlan<H>;
   using PL = Plan<H>;
+  using XP = C2RPlan<H>;  // work layout of the row-major mapping (conflict-free padding)
   constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL;
   if (bl) {
     u = static_cast<const double*>(bl[blockIdx.z].src);
@@ -710,7 +711,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
   const int rl = threadIdx.x / TM, i = threadIdx.x % TM;
   const long long row = (long long)blockIdx.x * RPB + rl;
   const bool live = row < rows;
-  double2* Wk = sm + rl * PL::LS;  // FFT work, then the natural-order result
+  double2* Wk = sm + rl * XP::LS;  // FFT work, then the natural-order result
   const double2* z = reinterpret_cast<const double2*>(u) + row * H;
   {  // pass 0 straight from global
     constexpr int R = PL::R0, T = PL::T0;
@@ -720,7 +721,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
       for (int r = 0; r < R; ++r) a[r] = live ? z[i + r * T] : make_double2(0.0, 0.0);
       Dft<R, -1>::run(a);
 #pragma unroll
-      for (int r = 0; r < R; ++r) Wk[PL::p0out(i * R + r)] = a[r];
+      for (int r = 0; r < R; ++r) Wk[XP::p0out(i * R + r)] = a[r];
     }
   }
   __syncthreads();
@@ -729,10 +730,10 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
     if (i < T) {
       double2 a[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[r] = Wk[PL::p1(i, r)];
+      for (int r = 0; r < R; ++r) a[r] = Wk[XP::p1(i, r)];
       bfly<H, 1, -1>(a, i, master);
 #pragma unroll
-      for (int r = 0; r < R; ++r) Wk[PL::p1(i, r)] = a[r];
+      for (int r = 0; r < R; ++r) Wk[XP::p1(i, r)] = a[r];
     }
     __syncthreads();
   }
@@ -741,7 +742,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
     double2 a[RL];
     if (i < TL) {
 #pragma unroll
-      for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? PL::p1(i, r) : PL::p2in(i + r * TL)];
+      for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? XP::p1(i, r) : XP::p2in(i + r * TL)];
       bfly<H, LAST, -1>(a, i, master);
     }
     __syncthreads();  // every read of the work layout is done: store the natural-order result
@@ -836,7 +837,7 @@ template <int H>
 bool launch_rows_r2c_t(const LaunchCtx& L, const double* u, double2* Uh, long long rows, int nfields, double sc,
                        bool scale, const BatchLine* bl) {
   using RP = RowPlan<H>;
-  constexpr size_t SMEM = (size_t)RP::RPB * Plan<H>::LS * sizeof(double2);
+  constexpr size_t SMEM = (size_t)RP::RPB * C2RPlan<H>::LS * sizeof(double2);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_rows_r2c<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
