@@ -276,8 +276,11 @@ __device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, do
 #ifndef FW_C2R_PAD
 #define FW_C2R_PAD 1  // 0: Plan<H>'s line padding in the row C2R (A/B)
 #endif
+#ifndef FW_C2R_RPB128
+#define FW_C2R_RPB128 8  // rows per block of the h = 128 row C2R
+#endif
 #ifndef FW_C2R_XB2
-#define FW_C2R_XB2 0  // measured: no gain at C3 (the kernel is not fetch-latency bound)
+#define FW_C2R_XB2 0  // h = 256 / 512 (h = 128 always double-buffers; at 16 rows per block it gained nothing)
 #endif
 #ifndef FW_C2R_MINB
 #define FW_C2R_MINB 2  // blocks per SM the register allocation is bounded for
@@ -309,12 +312,16 @@ struct C2RPlan {
   }
   static constexpr size_t ROWB = (size_t)(XS + LS) * sizeof(double2);
   static constexpr size_t CAP = 112640;  // two blocks per SM
-  static constexpr int RPB = (size_t)(256 / TM) * ROWB + TWN * sizeof(double2) <= CAP
-                                 ? 256 / TM
-                                 : (int)((CAP - TWN * sizeof(double2)) / ROWB);
+  static constexpr int RPB0 = (size_t)(256 / TM) * ROWB + TWN * sizeof(double2) <= CAP
+                                  ? 256 / TM
+                                  : (int)((CAP - TWN * sizeof(double2)) / ROWB);
+  // h = 128: half-size blocks (8 rows, 4 warps), four per SM, X double-buffered (measured at C3:
+  // 6.34 -> ~6.0 ms per step against 16-row blocks, two per SM)
+  static constexpr int RPB = H == 128 ? FW_C2R_RPB128 : RPB0;
+  static constexpr int MINB = H == 128 ? 4 : FW_C2R_MINB;
   static constexpr int NT = RPB * TM;
   // X rows double-buffered (next term and the one after in flight) when that keeps RPB
-  static constexpr int NXB = FW_C2R_XB2 && (size_t)TWN * sizeof(double2) + (size_t)RPB * (ROWB + XS * sizeof(double2)) <= CAP ? 2 : 1;
+  static constexpr int NXB = (FW_C2R_XB2 || H == 128) && (size_t)TWN * sizeof(double2) + (size_t)RPB * (ROWB + XS * sizeof(double2)) <= CAP ? 2 : 1;
   static constexpr size_t SMEM = (size_t)TWN * sizeof(double2) + (size_t)RPB * (ROWB + (NXB - 1) * XS * sizeof(double2));
   // tensor memory per warp: (s-s0) at [0, 4 RL), (s-s0)^{m-1} at [4 RL, 8 RL) (two columns per double)
   static constexpr int TMC = 8 * RL;
@@ -327,7 +334,7 @@ struct C2RPlan {
 };
 
 template <int H>
-__global__ void __launch_bounds__(C2RPlan<H>::NT, FW_C2R_MINB) k_rows_c2r(const double2* __restrict__ src, long long src_ts,
+__global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(const double2* __restrict__ src, long long src_ts,
                                                             int m_first, int m_last, const double* __restrict__ dev1,
                                                             double* __restrict__ out, long long rows, double* residue,
                                                             const int* guard, const double2* __restrict__ master,
