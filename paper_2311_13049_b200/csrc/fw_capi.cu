@@ -1491,6 +1491,10 @@ int fw_stage_c2c_scatter(fw_ctx ctx, int dim, const int* J, int axis, int dir, c
   }
   sc.nq = nq;
   sc.blk = blk;
+  sc.lgblk = -1;
+  if (blk > 0 && (blk & (blk - 1)) == 0 && blk < (1ll << 30))
+    for (sc.lgblk = 0; (1ll << sc.lgblk) < blk; ++sc.lgblk) {
+    }
   sc.jstride = jstride;
   sc.ostride = ostride;
   sc.tstride = tstride;

@@ -119,6 +119,7 @@ struct Scatter {
   double2* dst[kMaxScatter];
   long long blk, jstride, ostride, tstride, base;
   int nq;
+  int lgblk;  // log2(blk) when blk is a power of two (32-bit shift / mask in the epilogue), else -1
 };
 
 // register-resident line FFTs (fw_lines.cu) for n in {256, 512, 1024}; false = not served

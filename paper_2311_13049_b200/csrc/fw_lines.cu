@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256, lines_minb(N)) k_lines(const double2* __r
                                                const double* __restrict__ w, long long S, long long inner,
                                                long long src_ts, long long dst_ts, long long w_ts, double sc,
                                                int do_scale, const double2* __restrict__ master,
-                                               const BatchLine* __restrict__ bl, const Scatter scat) {
+                                               const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat) {
   using PL = Plan<N>;
   constexpr int L = PL::L;
   extern __shared__ double2 sm[];  // L lines x LS
@@ -186,9 +186,16 @@ __global__ void __launch_bounds__(256, lines_minb(N)) k_lines(const double2* __r
           }
           const int j = i + r * T;
           if constexpr (SCAT) {  // fused transpose: straight into the destination rank's buffer
-            const int q = (int)(j / scat.blk);
-            scat.dst[q][term * scat.tstride + (j - q * scat.blk) * scat.jstride + o * scat.ostride + in0 + l +
-                        scat.base] = v;
+            int q, jr;
+            if (scat.lgblk >= 0) {  // power-of-two block: 32-bit shift and mask
+              q = j >> scat.lgblk;
+              jr = j & ((1 << scat.lgblk) - 1);
+            } else {
+              q = (int)(j / scat.blk);
+              jr = (int)(j - q * scat.blk);
+            }
+            scat.dst[q][term * scat.tstride + (long long)jr * scat.jstride + o * scat.ostride + in0 + l + scat.base] =
+                v;
           } else {
             dst[base + (long long)j * S] = v;
           }
@@ -539,7 +546,7 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
                                                         const double* __restrict__ w, long long S, long long inner,
                                                         long long dst_ts, long long w_ts, int nterms, int tchunk,
                                                         double sc, int do_scale, const double2* __restrict__ master,
-                                                        const BatchLine* __restrict__ bl, const Scatter scat) {
+                                                        const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat) {
   using PL = Plan<N>;
   using TP = TermPlan<N>;
   constexpr int L = PL::L, R0 = PL::R0, T0 = PL::T0, LAST = PL::P - 1;
@@ -667,9 +674,16 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
           }
           const int j = i + r * TLST;
           if constexpr (SCAT) {
-            const int q = (int)(j / scat.blk);
-            scat.dst[q][term * scat.tstride + (j - q * scat.blk) * scat.jstride + o * scat.ostride + in0 + l +
-                        scat.base] = v;
+            int q, jr;
+            if (scat.lgblk >= 0) {  // power-of-two block: 32-bit shift and mask
+              q = j >> scat.lgblk;
+              jr = j & ((1 << scat.lgblk) - 1);
+            } else {
+              q = (int)(j / scat.blk);
+              jr = (int)(j - q * scat.blk);
+            }
+            scat.dst[q][term * scat.tstride + (long long)jr * scat.jstride + o * scat.ostride + in0 + l + scat.base] =
+                v;
           } else {
             dst[(long long)term * dst_ts + base + (long long)j * S] = v;
           }
