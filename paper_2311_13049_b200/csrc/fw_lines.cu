@@ -32,13 +32,22 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 #ifndef FW_LINES_SWZ
 #define FW_LINES_SWZ 1
 #endif
-template <int N>
+#ifndef FW_LINES_WIDE
+#define FW_LINES_WIDE 1
+#endif
+#ifndef FW_WIDE_STRIDE
+#define FW_WIDE_STRIDE (512 << 10)  // bytes
+#endif
+template <int N, int NTH = 256>
 struct Plan {
   static constexpr int P = npass(N);
   static constexpr int R0 = radix(N, 0), R1 = radix(N, 1), R2 = P > 2 ? radix(N, 2) : 1;
   static constexpr int T0 = N / R0, T1 = N / R1, T2 = N / R2;
   static constexpr int TMAX = cmax(T0, cmax(T1, P > 2 ? T2 : 0));
-  static constexpr int L = 256 / TMAX;  // lines per block (256 threads)
+  // threads per block of the line kernels (launch_n picks 512 for long strides: 8 / 4 lines of
+  // n = 512 / 1024 give 128 / 64 B contiguous per global access)
+  static constexpr int NTHR = NTH;
+  static constexpr int L = NTHR / TMAX;  // lines per block
   static constexpr int S1 = ilog2c(R1), ST = ilog2c(T1);
   // padded position; the line stride is odd so the L lines of a quarter warp hit distinct banks
   __device__ static __forceinline__ int pad(int p) { return p + (p >> S1) + (p >> ST); }
@@ -57,12 +66,14 @@ struct Plan {
   // quarter-warp bank groups of each access; the padding above gives 2-way conflicts there);
   // n = 256: the padding above (already conflict-free)
   // (the XOR term reads only bits >= 3 of p, so it permutes slots within their 8-slot group)
-  static constexpr int SWA = N == 512 || N == 1024 ? 3 : 0, SWB = N == 512 ? 6 : N == 1024 ? 7 : 0;
-  static constexpr int SWL = N == 512 ? 2 : 4;
+  // (searched per (n, L): tools/layouts/search_line_swizzle.py)
+  static constexpr int SWA = N == 512 || N == 1024 ? 3 : 0;
+  static constexpr int SWB = N == 512 ? (L == 8 ? 0 : 6) : N == 1024 ? 7 : 0;  // 0: single term
+  static constexpr int SWL = N == 512 ? (L == 8 ? 1 : 2) : (L == 4 ? 2 : 4);
   static constexpr int LLS = (FW_LINES_SWZ && SWA) ? N : LS;
   __device__ static __forceinline__ int lpos(int l, int p) {
     if constexpr (FW_LINES_SWZ && SWA != 0)
-      return l * N + (p ^ ((((p >> SWA) ^ (p >> SWB)) + SWL * l) & 7));
+      return l * N + (p ^ ((((p >> SWA) ^ (SWB ? (p >> SWB) : 0)) + SWL * l) & 7));
     else
       return l * LS + pad(p);
   }
@@ -73,7 +84,7 @@ struct Plan {
     return i1 * R1 + r1;
   }
   static_assert(P == 2 || P == 3, "2- or 3-pass plans");
-  static_assert(L >= 1 && L * TMAX == 256, "256 threads");
+  static_assert(L >= 1 && L * TMAX == NTHR, "whole lines per block");
 };
 
 // twiddled radix-R butterfly of pass PASS (p = pprod > 1): twiddles = master entries
@@ -103,19 +114,21 @@ __device__ __forceinline__ void bfly(double2* a, int i, const double2* __restric
 #ifndef FW_LINES_MINB1024
 #define FW_LINES_MINB1024 2
 #endif
-__host__ __device__ constexpr int lines_minb(int n) {
-  return n == 256 ? FW_LINES_MINB256 : n == 512 ? FW_LINES_MINB512 : FW_LINES_MINB1024;
+// (the 512 / 1024 bounds are for 256-thread blocks; 512-thread blocks get half)
+template <int N, int NTH>
+__host__ __device__ constexpr int lines_minb() {
+  return N == 256 ? FW_LINES_MINB256 : (N == 512 ? FW_LINES_MINB512 : FW_LINES_MINB1024) * 256 / NTH;
 }
 
 // C2C of lines of length N along an axis of stride S (line (o, in): o*N*S + in + j*S).
 // blockIdx.y = term (src/dst/w advance by their term strides), blockIdx.z = field (bl).
-template <int N, int DIR, bool SCAT>
-__global__ void __launch_bounds__(256, lines_minb(N)) k_lines(const double2* __restrict__ src, double2* __restrict__ dst,
+template <int N, int DIR, bool SCAT, int NTH>
+__global__ void __launch_bounds__(NTH, (lines_minb<N, NTH>())) k_lines(const double2* __restrict__ src, double2* __restrict__ dst,
                                                const double* __restrict__ w, long long S, long long inner,
                                                long long src_ts, long long dst_ts, long long w_ts, double sc,
                                                int do_scale, const double2* __restrict__ master,
                                                const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat) {
-  using PL = Plan<N>;
+  using PL = Plan<N, NTH>;
   constexpr int L = PL::L;
   extern __shared__ double2 sm[];  // L lines x LS
   if (bl) {
@@ -530,25 +543,26 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
 #ifndef FW_LT_PREFETCH
 #define FW_LT_PREFETCH 1  // next term's weights loaded during the current term's passes
 #endif
-template <int N>
+template <int N, int NTH>
 struct TermPlan {
-  using P = Plan<N>;
+  using P = Plan<N, NTH>;
   static constexpr int TW1 = P::P > 2 ? P::R0 * (P::R1 - 1) : 0;  // pass-1 twiddles of a 3-pass plan
   static constexpr int TWL = pprod(N, P::P - 1) * (radix(N, P::P - 1) - 1);  // last pass
   static constexpr int TWN = TW1 + TWL;
   static constexpr size_t SMEM = (size_t)(TWN + P::L * P::LLS) * sizeof(double2);
   static constexpr int TMC = 4 * P::R0;  // columns per warp: R0 complex pass-0 inputs
-  static constexpr int TMALLOC = pow2ceil(2 * TMC < 32 ? 32 : 2 * TMC);  // 8 warps = 2 per quadrant
+  static constexpr int NSLOT = P::NTHR / 128;  // warps per TMEM lane quadrant
+  static constexpr int TMALLOC = pow2ceil(NSLOT * TMC < 32 ? 32 : NSLOT * TMC);
 };
 
-template <int N, bool SCAT>
-__global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
+template <int N, bool SCAT, int NTH>
+__global__ void __launch_bounds__(NTH, 512 / NTH) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
                                                         const double* __restrict__ w, long long S, long long inner,
                                                         long long dst_ts, long long w_ts, int nterms, int tchunk,
                                                         double sc, int do_scale, const double2* __restrict__ master,
                                                         const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat) {
-  using PL = Plan<N>;
-  using TP = TermPlan<N>;
+  using PL = Plan<N, NTH>;
+  using TP = TermPlan<N, NTH>;
   constexpr int L = PL::L, R0 = PL::R0, T0 = PL::T0, LAST = PL::P - 1;
   constexpr int RLST = radix(N, LAST), TLST = N / RLST;
   extern __shared__ double2 sm[];
@@ -574,13 +588,13 @@ __global__ void __launch_bounds__(256, 2) k_lines_terms(const double2* __restric
   double2* line = lines_sm;  // slot p of this thread's line at PL::lpos(l, p)
 
   if constexpr (PL::P > 2) {
-    for (int e = tid; e < TP::TW1; e += 256) {
+    for (int e = tid; e < TP::TW1; e += PL::NTHR) {
       constexpr int R = PL::R1, p = PL::R0;
       const int k = e / (R - 1), r = e % (R - 1) + 1;
       tw1[e] = master[(r * k) * (kTwMaster / (p * R))];
     }
   }
-  for (int e = tid; e < TP::TWL; e += 256) {
+  for (int e = tid; e < TP::TWL; e += PL::NTHR) {
     constexpr int R = RLST, p = pprod(N, LAST);
     const int k = e / (R - 1), r = e % (R - 1) + 1;
     twl[e] = master[(r * k) * (kTwMaster / (p * R))];
@@ -792,31 +806,31 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
 #ifndef FW_LINES_TERMS
 #define FW_LINES_TERMS 1  // 0: one block per (lines, term), uhat re-read per term
 #endif
-template <int N>
-bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
+template <int N, int NTH>
+bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
               long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
               int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
-  constexpr int LPB = Plan<N>::L;
-  constexpr size_t SMEM = (size_t)LPB * Plan<N>::LLS * sizeof(double2);
+  constexpr int LPB = Plan<N, NTH>::L;
+  constexpr size_t SMEM = (size_t)LPB * Plan<N, NTH>::LLS * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_lines<N, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(k_lines<N, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(k_lines<N, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    cudaFuncSetAttribute(k_lines<N, +1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, -1, false, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, +1, false, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, -1, true, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    cudaFuncSetAttribute(k_lines<N, +1, true, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     attr = true;
   }
   const long long bpo = (inner + LPB - 1) / LPB;
   const Scatter none{};
   const Scatter& sc_ = scatter ? *scatter : none;
   const int f = scale ? 1 : 0;
-  if (FW_LINES_TERMS && dir > 0 && src_ts == 0 && nterms > 1 && (w || (bl && w_ts != 0))) {
+  if (FW_LINES_TERMS && dir > 0 && src_ts == 0 && nterms > 1 && (w || (bl && w_ts != 0))) {  // (launch_n's `terms`)
     // every term of an inverse from one uhat: one pass over the spectrum (k_lines_terms)
-    constexpr size_t TSM = TermPlan<N>::SMEM;
+    constexpr size_t TSM = TermPlan<N, NTH>::SMEM;
     static bool tattr = false;
     if (!tattr) {
-      cudaFuncSetAttribute(k_lines_terms<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
-      cudaFuncSetAttribute(k_lines_terms<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
+      cudaFuncSetAttribute(k_lines_terms<N, false, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
+      cudaFuncSetAttribute(k_lines_terms<N, true, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
       tattr = true;
     }
     // enough blocks to fill the GPU: split the term range when the lines alone give fewer than
@@ -826,10 +840,10 @@ bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, con
     const int tchunk = (nterms + nchunk - 1) / nchunk;
     const dim3 tgrid((unsigned)(outer * bpo), (unsigned)((nterms + tchunk - 1) / tchunk), (unsigned)nfields);
     if (scatter)
-      k_lines_terms<N, true><<<tgrid, 256, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, tchunk, sc,
+      k_lines_terms<N, true, NTH><<<tgrid, Plan<N, NTH>::NTHR, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, tchunk, sc,
                                                              f, L.master, bl, sc_);
     else
-      k_lines_terms<N, false><<<tgrid, 256, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, tchunk,
+      k_lines_terms<N, false, NTH><<<tgrid, Plan<N, NTH>::NTHR, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, tchunk,
                                                               sc, f, L.master, bl, sc_);
     if (L.launches) *L.launches += 1;
     return true;
@@ -837,21 +851,36 @@ bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, con
   const dim3 grid((unsigned)(outer * bpo), (unsigned)nterms, (unsigned)nfields);
   if (dir < 0) {
     if (scatter)
-      k_lines<N, -1, true><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
+      k_lines<N, -1, true, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
                                                            bl, sc_);
     else
-      k_lines<N, -1, false><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
+      k_lines<N, -1, false, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
                                                             L.master, bl, sc_);
   } else {
     if (scatter)
-      k_lines<N, +1, true><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
+      k_lines<N, +1, true, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
                                                            bl, sc_);
     else
-      k_lines<N, +1, false><<<grid, 256, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
+      k_lines<N, +1, false, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
                                                             L.master, bl, sc_);
   }
   if (L.launches) *L.launches += 1;
   return true;
+}
+
+// 512-thread blocks (8 / 4 lines per block: 128 / 64 B contiguous per global access) for every
+// 512 / 1024-point line pass, except the all-terms inverse on short strides, which keeps
+// 256-thread blocks (measured: C4 step 97.6 -> 83 ms, C5 unchanged; tools/lt_stride.py)
+template <int N>
+bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
+              long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
+              int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
+  const bool terms = dir > 0 && src_ts == 0 && nterms > 1 && (w || (bl && w_ts != 0));
+  const bool wide = FW_LINES_WIDE && (N == 1024 || !terms || S * (long long)sizeof(double2) >= FW_WIDE_STRIDE);
+  if constexpr (N == 256)
+    return launch_nt<N, 256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter);
+  else
+    return wide ? launch_nt<N, 512>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter) : launch_nt<N, 256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter);
 }
 
 template <int H>
