@@ -311,7 +311,8 @@ struct C2RPlan {
   static constexpr int TM = P::TMAX;                 // threads per row
   static constexpr int RL = radix(H, P::P - 1);      // last-pass radix
   static constexpr int TL = H / RL;
-  static constexpr int XS = (H + 1) | 1;             // X row stride (natural order, odd)
+  // X row stride (natural order, odd; 128-B aligned rows measured 1-3 % slower)
+  static constexpr int XS = (H + 1) | 1;
   // twiddles: pre-processing W_{2H}^k (k <= H), pass 1 [k < R0][R1 - 1], pass 2 [k < R0 R1][R2 - 1]
   static constexpr int TW1 = P::R0 * (P::R1 - 1);
   static constexpr int TW2 = P::P > 2 ? P::R0 * P::R1 * (P::R2 - 1) : 0;
@@ -368,19 +369,19 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
     dev1 = bl[blockIdx.z].aux;
     out = bl[blockIdx.z].out;
   }
-  extern __shared__ double2 sm[];
+  // [X rows: NXB x RPB x XS][twiddles: TWN][work: RPB x LS]
+  extern __shared__ __align__(128) double2 sm[];
   __shared__ unsigned tbase_sh;
-  double2* twpre = sm;
-  double2* tw1 = sm + (H + 1);
-  double2* tw2 = tw1 + RP::TW1;
-  double2* rsm = sm + RP::TWN;
   const int tid = threadIdx.x;
   const int rl = tid / TM, i = tid % TM;
   const long long row = (long long)blockIdx.x * RPB + rl;
   const bool live = row < rows;
   constexpr int NXB = RP::NXB;
-  double2* Xb = rsm + rl * RP::XS;                       // natural-order X of this row (NXB buffers)
-  double2* Wk = rsm + NXB * RPB * RP::XS + rl * RP::LS;  // FFT work (in-place layout)
+  double2* Xb = sm + rl * RP::XS;  // natural-order X of this row (NXB buffers)
+  double2* twpre = sm + NXB * RPB * RP::XS;
+  double2* tw1 = twpre + (H + 1);
+  double2* tw2 = tw1 + RP::TW1;
+  double2* Wk = twpre + RP::TWN + rl * RP::LS;  // FFT work (in-place layout)
 
   const double* d1row = dev1 ? dev1 + (live ? row : 0) * NL : nullptr;
   // X rows arrive by cp.async NXB terms ahead: a buffer is refilled as soon as pass 0 of its
