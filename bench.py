@@ -513,17 +513,14 @@ def main():
     check = fw._capi.check
     check(lib.fw_seis_get(st._h, hp, None, None, None))
     e2e_steps = max(3, min(args.steps, 50))
+    # one public call per step: host wavefield in, one step, host wavefield out (fw_seis_step_io)
     for _ in range(2):
-        check(lib.fw_seis_set_current(st._h, hp))
-        check(lib.fw_seis_step(st._h, 1))
-        check(lib.fw_seis_get(st._h, hp, None, None, None))
+        check(lib.fw_seis_step_io(st._h, hp, 1, hp))
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for _ in range(e2e_steps):
-        check(lib.fw_seis_set_current(st._h, hp))
-        check(lib.fw_seis_step(st._h, 1))
-        check(lib.fw_seis_get(st._h, hp, None, None, None))
+        check(lib.fw_seis_step_io(st._h, hp, 1, hp))
     e3.record(stream)
     e3.synchronize()
     ms_e2e = e2.elapsed_time(e3) / e2e_steps
@@ -558,7 +555,7 @@ def main():
                          "algorithmic_bytes_per_step": B_step, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * cfg.N,
                     "d2h_bytes_per_step": 8 * cfg.N, "ms_per_step": float(t2.item()),
-                    "path": "fw_seis_set_current (pinned H2D) + fw_seis_step + fw_seis_get (D2H)"},
+                    "path": "fw_seis_step_io: pinned H2D of the wavefield, one step, D2H of the new wavefield, one host sync"},
             "gpu_launches": int(launches),
             "launches_per_step": launches / args.steps,
             "clocks": clk.summary(),

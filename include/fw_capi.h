@@ -19,6 +19,7 @@
  *   fw_seis_create          derive_medium + SeismicStepper ctor           seismic.cpp:11-44, 85-109
  *   fw_seis_step            SeismicStepper::step / advance               seismic.cpp:111-137
  *   fw_seis_get             SeismicStepper::current / n                  seismic.hpp:44-46
+ *   fw_seis_step_io         current() = u; step(); u = current()         seismic.cpp:111-133, seismic.hpp:44
  *   fw_tsfp2_*              Stepper (Method::TSFP2) ctor / step            stepping.cpp:119-138, 266-304
  *   fw_wave_*               Stepper (Method::LFFP / CNFP) ctor / step      stepping.cpp:88-104, 119-138, 170-264
  *                           (the Laplacian seam stepping.hpp:52-60 served by the device apply)
@@ -141,6 +142,10 @@ int fw_seis_get(fw_seis s, double* cur_host, double* prev_host, double* atten_pr
 /* overwrite the current wavefield from host memory (host-owned state between
  * steps: source injection / receivers), then the caller steps on. */
 int fw_seis_set_current(fw_seis s, const double* cur_host);
+/* set_current + step(nsteps) + current() in one call with one host synchronisation
+ * (both host buffers nullable, may alias; pinned memory for full PCIe speed).  On
+ * FW_E_BLOWUP cur_out_host holds the pre-step state, as fw_seis_get would return. */
+int fw_seis_step_io(fw_seis s, const double* cur_in_host, int nsteps, double* cur_out_host);
 /* device pointer of the current wavefield (valid until the next step) */
 const double* fw_seis_current_device(fw_seis s);
 /* the two operators, for diagnostics */

@@ -333,6 +333,18 @@ class SeismicStepper:
         cur = _f64(cur, self.grid.total())
         check(load_library().fw_seis_set_current(self._h, _ptr(cur)))
 
+    def step_io(self, cur_in=None, cur_out=None, steps: int = 1):
+        """Host-owned wavefield exchange in one call (fw_seis_step_io): the current field is
+        overwritten from cur_in (if given), `steps` steps run, the new current field lands in
+        cur_out (a float64 array of the grid's size, if given).  BlowupDetected as step()."""
+        pin = None if cur_in is None else _f64(cur_in, self.grid.total())
+        if cur_out is not None and (cur_out.dtype != np.float64 or not cur_out.flags.c_contiguous
+                                    or cur_out.size != self.grid.total()):
+            raise ValueError("cur_out must be a C-contiguous float64 array of the grid's size")
+        check(load_library().fw_seis_step_io(self._h, None if pin is None else _ptr(pin), int(steps),
+                                             None if cur_out is None else _ptr(cur_out)))
+        return cur_out
+
     def n(self) -> int:
         n = C.c_long(0)
         check(load_library().fw_seis_get(self._h, None, None, None, C.byref(n)))

@@ -973,6 +973,22 @@ int fw_seis_set_current(fw_seis s, const double* cur_host) {
   return FW_OK;
 }
 
+int fw_seis_step_io(fw_seis s, const double* cur_in_host, int nsteps, double* cur_out_host) {
+  if (!s) return set_err(FW_E_ARG, "null stepper");
+  const size_t N = s->g.N;
+  cudaStream_t st = s->ctx->stream;
+  if (cur_in_host) FW_CUDA(cudaMemcpyAsync(s->cur(), cur_in_host, N * 8, cudaMemcpyHostToDevice, st));
+  FW_TRY(fw_seis_enqueue(s, nsteps));
+  // the new wavefield and the blow-up flag come back behind the steps: one host synchronisation
+  if (cur_out_host) FW_CUDA(cudaMemcpyAsync(cur_out_host, s->cur(), N * 8, cudaMemcpyDeviceToHost, st));
+  const int rc = seis_check(s);
+  if (rc == FW_E_BLOWUP && cur_out_host) {  // the state was rolled back to before the offending step
+    FW_CUDA(cudaMemcpyAsync(cur_out_host, s->cur(), N * 8, cudaMemcpyDeviceToHost, st));
+    FW_CUDA(cudaStreamSynchronize(st));
+  }
+  return rc;
+}
+
 const double* fw_seis_current_device(fw_seis s) { return s ? s->cur() : nullptr; }
 
 int fw_seis_ops(fw_seis s, fw_op* disp, fw_op* atten) {

@@ -622,3 +622,37 @@ def test_multipass_batched_step_blowup_matches_restatement(J):
     cur, prev, ap, n = st.state()
     assert n == n_r
     assert np.array_equal(cur, cur_r) and np.array_equal(prev, prev_r) and np.array_equal(ap, ap_r)
+
+
+@pytest.mark.parametrize("J", [(1024, 1024), (64, 32)])
+def test_seis_step_io_equals_set_step_get(J):
+    """fw_seis_step_io (host wavefield in, steps, host wavefield out, one sync) is
+    set_current + step + current: identical bits, also on the persistent 1024^2 path,
+    and on a blow-up it returns the pre-step state like fw_seis_get."""
+    m = fw()
+    lo, hi = (-16.0, -16.0), (16.0, 16.0)
+    g = grid_of(J, lo, hi)
+    x0 = np.linspace(-16, 16, J[0], endpoint=False)[:, None]
+    x1 = np.linspace(-16, 16, J[1], endpoint=False)[None, :]
+    phi = np.exp(-(x0**2 + x1**2) / 0.5)
+    gamma = 0.02 + 0.01 * np.tanh(x1) + 0.0 * x0
+    med = m.build_medium(g, gamma, np.ones(J), 1.0, 6)
+    a = m.SeismicStepper(med, phi, np.zeros(J), 5e-4)
+    b = m.SeismicStepper(med, phi, np.zeros(J), 5e-4)
+    u = phi * 0.5
+    out = np.empty(J)
+    for k in range(3):
+        a.set_current(u)
+        a.advance(2)
+        ref = a.current()
+        b.step_io(u, out, steps=2)
+        assert np.array_equal(out, ref)
+        u = ref * 0.9
+    assert a.n() == b.n()
+    # blow-up: both report the same offending step and state
+    big = m.SeismicStepper(med, phi, np.zeros(J), 0.08 if J[0] == 1024 else 4.0)  # far beyond stability
+    with pytest.raises(m.BlowupDetected):
+        for _ in range(400):
+            big.step_io(None, out)
+    cur, _, _, n = big.state()
+    assert np.array_equal(out, cur) and n > 1
