@@ -11,6 +11,15 @@
 // fw_fft.cuh, only the storage order differs), one barrier per pass boundary.
 // Bit-identical to k_c2c_axis / the CPU oracle (same radix plan, twiddles,
 // fma placement).
+//
+// Kernels: k_lines<n, dir> (one term per blockIdx.y), k_lines_terms<n> (every term of the
+// first inverse axis per block, uhat parked in tensor memory), k_rows_r2c<h> / k_rows_c2r<h>
+// (per row of the last axis; the C2R keeps (s-s0) and (s-s0)^{m-1} in tensor memory and
+// recombines the terms in registers).  Shared-memory layouts are bank-conflict-free for each
+// kernel's thread mapping (tools/layouts/).  Build switches (-D..., A/B only; defaults are the
+// measured best): FW_LINES_TERMS, FW_LT_PREFETCH, FW_LT_TARGET, FW_LINES_SWZ,
+// FW_LINES_WIDE, FW_WIDE_STRIDE, FW_LINES_MINB{256,512,1024}, FW_C2R_PAD, FW_C2R_XB2,
+// FW_C2R_RPB128, FW_C2R_MINB.
 #include <cuda_runtime.h>
 
 #include <algorithm>
