@@ -418,6 +418,7 @@ def run_c5(args):
         ms16 = per_m[16]["ms_per_sweep"]
         # generic 2D path: (s-s0)^m regenerated on chip (k_rows_c2r) -> table term 8N
         B = configs.C5_FIELDS * configs.bytes_per_apply(n, nh, 16, table_model=False)
+        Bp = configs.C5_FIELDS * (8 * n + 16 * nh + 32 * nh + 16 * nh + 17 * (8 + 16 + 16) * nh + 8 * n + 8 * n)
         line = {"metric": METRIC, "value": per_m[16]["Gpoint_term_per_s"], "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms16, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -426,7 +427,12 @@ def run_c5(args):
                            "parallelism": f"data-parallel over {world} GPU(s), no collective"},
                 "roofline": {"bound": "hbm", "achieved": B / (ms16 * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                              "frac": B / (ms16 * 1e-3) / 1e9 / hbm, "traffic": None,
-                             "kernel": "64 applies (multi-pass kernels)", "peak_source": peak_src},
+                             "kernel": "64 applies (multi-pass kernels)", "peak_source": peak_src,
+                             "bytes_model": "table model, (s-s0)^m regenerated on chip (SURVEY 8(d))",
+                             # the 2D pass model: forward R2C + column C2C, all-terms column inverse
+                             # (uhat once, w_m, M+1 spectra out), row C2R (M+1 spectra in, dev1, out)
+                             "pass_model": {"bytes": Bp, "achieved": Bp / (ms16 * 1e-3) / 1e9,
+                                            "frac": Bp / (ms16 * 1e-3) / 1e9 / hbm}},
                 "e2e": None, "gpu_launches": None}
         print(json.dumps(line), flush=True)
     if world > 1:

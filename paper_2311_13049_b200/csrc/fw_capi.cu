@@ -632,7 +632,12 @@ int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_
   const fw::GridGeom& g = o0->g;
   const int m_last = o0->constant_order ? 0 : o0->M;
   const size_t per_field = (size_t)(m_last + 1) * g.Nh * sizeof(double2);
-  const int Fc = (int)std::max<size_t>(1, std::min<size_t>((size_t)nfields, ((size_t)2 << 30) / per_field));
+  // fields per batched pipeline: the all-terms spectra of a chunk live in scratch (up to 16 GiB of
+  // the 180 GB HBM); chunks are balanced (64 fields at M = 16 fit in one chunk; an unbalanced
+  // 59 + 5 split under a 2 GiB cap left the GPU idle in the small chunk)
+  const size_t cap = std::max<size_t>(1, std::min<size_t>((size_t)nfields, ((size_t)16 << 30) / per_field));
+  const size_t nchunk = ((size_t)nfields + cap - 1) / cap;
+  const int Fc = (int)(((size_t)nfields + nchunk - 1) / nchunk);
   void *uh = nullptr, *T = nullptr, *tab = nullptr;
   FW_TRY(ctx->get_scratch(SLOT_BUH, (size_t)Fc * g.Nh * sizeof(double2), &uh));
   FW_TRY(ctx->get_scratch(SLOT_BT, (size_t)Fc * per_field, &T));

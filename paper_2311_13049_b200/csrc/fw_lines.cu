@@ -550,6 +550,9 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
 // tensor memory (pass-0 inputs of each thread), so a launch streams uhat once, w_m once and
 // writes the M+1 outputs (instead of re-reading uhat per term).  The next term's weights
 // are loaded while the current term's passes run.
+#ifndef FW_LT_MINB512
+#define FW_LT_MINB512 2  // blocks per SM of the 256-thread 512-point all-terms inverse
+#endif
 #ifndef FW_LT_PREFETCH
 #define FW_LT_PREFETCH 1  // next term's weights loaded during the current term's passes
 #endif
@@ -566,7 +569,7 @@ struct TermPlan {
 };
 
 template <int N, bool SCAT, int NTH>
-__global__ void __launch_bounds__(NTH, 512 / NTH) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
+__global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 : 512 / NTH) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
                                                         const double* __restrict__ w, long long S, long long inner,
                                                         long long dst_ts, long long w_ts, int nterms, int tchunk,
                                                         double sc, int do_scale, const double2* __restrict__ master,
