@@ -45,7 +45,11 @@ bool step2d_supported(int J0, int J1, int nsm);
 int step2d_col_groups(int J1);
 int step2d_wcols(int J1);
 constexpr int kStep2dCG = 4;
-constexpr int kStep2dRing = 6;  // term slots of the global ring
+#ifndef FW_S2D_RING
+#define FW_S2D_RING 4  // measured: 4 -> 243.8, 3 -> 244.4, 5 -> 244.9, 6 -> 245.0, 7 -> 245.4 us/step; 2 deadlocks
+#endif
+constexpr int kStep2dRing = FW_S2D_RING;  // term slots of the global ring (8 / 12 measured slower)
+static_assert(kStep2dRing >= 3, "the columns publish term t after pass 0 of t + 1: two slots deadlock");
 cudaError_t launch_step2d(const Step2DParams& p, cudaStream_t st, int nsm);
 
 // table relayouts for the persistent kernel
