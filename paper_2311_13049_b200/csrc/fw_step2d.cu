@@ -118,9 +118,17 @@ __device__ __forceinline__ double2 ld_stream2(const double2* p, unsigned long lo
                : "l"(p), "l"(pol));
   return v;
 }
+#ifndef FW_S2D_ZKEEP
+#define FW_S2D_ZKEEP 1  // term-ring stores with the evict-last hint (0: plain stores, A/B)
+#endif
 __device__ __forceinline__ void st_keep(double2* p, double2 v, unsigned long long pol) {
+#if FW_S2D_ZKEEP
   asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
                : "memory");
+#else
+  (void)pol;
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+#endif
 }
 __device__ __forceinline__ void prefetch_l2_hint(const void* p, unsigned bytes, unsigned long long pol) {
   asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
@@ -160,6 +168,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // being re-read from shared memory every term
 #ifndef FW_S2D_TWTM
 #define FW_S2D_TWTM 1
+#endif
+// L2 promotion of the tile TMA loads (A/B)
+#ifndef FW_S2D_L2PROMO
+#define FW_S2D_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_NONE  // measured 0.2 % faster than L2_256B
 #endif
 // seismic update inputs prefetched into L2 this many terms before the step's last term (0 = off)
 #ifndef FW_S2D_UPF
@@ -1091,7 +1103,7 @@ cudaError_t launch_t(const Step2DParams& p, cudaStream_t st, int nblk) {
   const cuuint32_t box[3] = {16, 256, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   if (encode(&zmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)p.T, dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, FW_S2D_L2PROMO,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   void* args[] = {(void*)&p, (void*)&zmap};
