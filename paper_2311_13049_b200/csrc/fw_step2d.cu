@@ -96,9 +96,16 @@ __device__ __forceinline__ void setmaxnreg_inc() {
 // L2 residency: the streamed tables (weights, deviation powers) are read once per step and
 // marked evict-first, the term ring Z (re-read a term later, rewritten 6 terms later)
 // evict-last, so that most of the ring is overwritten in L2 instead of written back.
+#ifndef FW_S2D_STREAM_EF
+#define FW_S2D_STREAM_EF 1  // streamed tables evict-first (0: evict-normal, A/B)
+#endif
 __device__ __forceinline__ unsigned long long pol_evict_first() {
   unsigned long long p;
+#if FW_S2D_STREAM_EF
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#endif
   return p;
 }
 __device__ __forceinline__ unsigned long long pol_evict_last() {
