@@ -124,61 +124,121 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def cpu_baseline(cfg, steps: int):
+def cpu_model() -> str:
+    """lscpu's model name (falls back to /proc/cpuinfo)."""
+    import subprocess
+
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.lower().startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _omp_set_threads(n: int) -> None:
+    """omp_set_num_threads in this process's OpenMP runtime (the reference's parallel region,
+    flap.cpp:75-77, reads it at every apply)."""
+    import ctypes as C
+
+    for name in ("libgomp.so.1", "libgomp.so"):
+        try:
+            C.CDLL(name).omp_set_num_threads(int(n))
+            return
+        except OSError:
+            continue
+
+
+def cpu_baseline(cfg, steps: int, warmup: int = 1, single_thread_steps: int = 2):
     """Time the reference (oracle/_ref) — or, if it is not built, the C restatement —
-    on `steps` C2 steps on this host.  Checker code: only this leg imports oracle/."""
+    on `steps` C2 steps (after `warmup`) on this host with all cores, then again with one
+    thread (OMP_NUM_THREADS = nproc and = 1).  Checker code: only this leg
+    (and the reference arm) imports oracle/."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import ctypes as C
 
     import oracle_lib as O
 
     cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     units = 2 * cfg.N * (cfg.M + 1)
-    if O.ref_available():
-        lib = O.reference()
-        lib.ref_time_seismic.argtypes = [C.c_int, O._ip, O._dp, O._dp, O._dp, O._dp, C.c_double, C.c_int,
-                                         O._dp, O._dp, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_double),
-                                         C.c_void_p]
-        per = C.c_double(0.0)
-        rc = lib.ref_time_seismic(len(cfg.J), O._i32(cfg.J), O._f64(cfg.lo), O._f64(cfg.hi),
-                                  O._f64(cfg.gamma).ravel(), O._f64(cfg.c0).ravel(), cfg.omega0, cfg.M,
-                                  O._f64(cfg.phi).ravel(), O._f64(cfg.psi).ravel(), cfg.tau, 1, steps,
-                                  C.byref(per), None)
-        if rc != 0:
-            raise RuntimeError(lib.ref_last_error())
-        t = per.value
-        kind = "reference"
-        how = ("reference sources (proj/src, unmodified) + FFTW-API shim (FFTW absent in image), "
-               "OpenMP over the M+1 terms (flap.cpp:75-77)")
-    else:
+
+    def time_steps(nthreads, nsteps, nwarm):
+        _omp_set_threads(nthreads)
+        if O.ref_available():
+            lib = O.reference()
+            lib.ref_time_seismic.argtypes = [C.c_int, O._ip, O._dp, O._dp, O._dp, O._dp, C.c_double, C.c_int,
+                                             O._dp, O._dp, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                             C.c_void_p]
+            per = C.c_double(0.0)
+            rc = lib.ref_time_seismic(len(cfg.J), O._i32(cfg.J), O._f64(cfg.lo), O._f64(cfg.hi),
+                                      O._f64(cfg.gamma).ravel(), O._f64(cfg.c0).ravel(), cfg.omega0, cfg.M,
+                                      O._f64(cfg.phi).ravel(), O._f64(cfg.psi).ravel(), cfg.tau, int(nwarm),
+                                      int(nsteps), C.byref(per), None)
+            if rc != 0:
+                raise RuntimeError(lib.ref_last_error())
+            return per.value
         t0 = time.perf_counter()
         O.port_seismic(cfg.J, cfg.lo, cfg.hi, cfg.gamma, cfg.c0, cfg.omega0, cfg.M, cfg.phi, cfg.psi, cfg.tau,
-                       steps)
-        t = (time.perf_counter() - t0) / (steps + 1.5)  # construction = 3 applies ~ 1.5 steps
+                       nsteps)
+        return (time.perf_counter() - t0) / (nsteps + 1.5)  # construction = 3 applies ~ 1.5 steps
+
+    t = time_steps(cores, steps, warmup)
+    t1 = time_steps(1, single_thread_steps, 0) if single_thread_steps > 0 else None
+    _omp_set_threads(cores)
+    if O.ref_available():
+        kind = "reference"
+        how = ("reference sources (proj/src, unmodified) + FFTW-API shim (FFT backend = builder shim; FFTW absent "
+               "in image), OpenMP over the M+1 terms (flap.cpp:75-77)")
+    else:
         kind = "port"
         how = "C restatement (oracle/fw_oracle.c), OpenMP over FFT lines"
-    return {"value": units / t / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{steps} SeismicStepper steps of C2 (1024^2, M=16) after 1 warm-up step; {how}",
-            "sec_per_step": t}
+    out = {"value": units / t / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
+           "sample": f"{steps} SeismicStepper steps of C2 (1024^2, M=16) after {warmup} warm-up step(s), "
+                     f"steady_clock around step() (seismic.cpp:111-133); {how}",
+           "cpu_model": cpu_model(), "sec_per_step": t}
+    if t1 is not None:
+        out["single_thread"] = {"value": units / t1 / 1e9, "unit": UNIT, "cores": 1,
+                                "sample": f"{single_thread_steps} steps, omp_set_num_threads(1)",
+                                "sec_per_step": t1}
+    return out
+
+
+def c2_config(cfg, size: int, world: int) -> dict:
+    """The `config` object of the C2 line, shared by both arms (the driver compares them)."""
+    return {"workload": f"C2 seismic step ({size}^2, M=16, dt=5e-4; BASELINE configs[1])",
+            "grid": list(cfg.J), "M": cfg.M, "tau": cfg.tau,
+            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+            "l2": "working set (2 ops x 17 w-tables + term scratch + state) ~0.45 GB > 126 MB L2; no flush"}
 
 
 def run_reference_arm(args):
+    """The reference's own CPU implementation of the same step (SeismicStepper::step on the
+    reference sources) on this host's cores, --steps timed steps after --warmup, same metric,
+    unit and config as our arm.  Under torchrun only rank 0 runs it."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from paper_2311_13049_b200 import configs
 
     cfg = configs.c2(args.size)
-    steps = max(1, min(args.steps, args.cpu_baseline_steps))
-    cb = cpu_baseline(cfg, steps)
+    cb = cpu_baseline(cfg, args.steps, args.warmup)
     v = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": steps, "warmup": 1, "ms_per_step": cb["sec_per_step"] * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2 seismic step ({args.size}^2, M=16, dt=5e-4)", "grid": [args.size] * 2,
-                       "M": cfg.M, "parallelism": "cpu (host cores)"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["sec_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": c2_config(cfg, args.size, world),
+            "time_steps_per_s": 1.0 / cb["sec_per_step"],
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                "single_thread") if k in cb},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -549,10 +609,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2 seismic step ({args.size}^2, M=16, dt=5e-4; BASELINE configs[1])",
-                       "grid": list(cfg.J), "M": cfg.M, "tau": cfg.tau,
-                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
-                       "l2": "working set (2 ops x 17 w-tables + term scratch + state) ~0.45 GB > 126 MB L2; no flush"},
+            "config": c2_config(cfg, args.size, world),
             "time_steps_per_s": world * 1e3 / ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
@@ -569,7 +626,8 @@ def main():
         if not args.no_cpu_baseline and world == 1:
             try:
                 cb = cpu_baseline(cfg, args.cpu_baseline_steps)
-                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                           "single_thread") if k in cb}
             except Exception as e:  # reported, never fatal
                 line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
         print(json.dumps(line), flush=True)

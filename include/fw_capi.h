@@ -104,6 +104,11 @@ typedef struct {
   size_t device_bytes;     /* resident table bytes */
 } fw_op_info_t;
 int fw_op_info(fw_op op, fw_op_info_t* info);
+/* which device pipeline serves this operator's applies (diagnostics / tests):
+ * FW_PATH_PERSISTENT_2D = the single-launch persistent 2D kernel (fw_step2d.cu),
+ * FW_PATH_MULTIPASS = the per-axis line kernels (fw_lines.cu / fw_kernels.cu) */
+enum fw_path { FW_PATH_MULTIPASS = 0, FW_PATH_PERSISTENT_2D = 1 };
+int fw_op_path(fw_op op);
 
 /* Host buffers in/out (the reference call: Field in, new Field out).
  * m_first: 0 = apply_matrix_free, 1 = apply_perturbation.
@@ -153,10 +158,14 @@ int fw_seis_ops(fw_seis s, fw_op* disp, fw_op* atten);
 int fw_seis_medium(fw_seis s, double* c, double* eta, double* tau_coef);
 
 /* ---- TSFP2 time-splitting stepper (Stepper, Method::TSFP2) ----
- * f: 0 = none, 1 = cubic u^3. */
+ * f: 0 = none, 1 = cubic u^3.  blowup_factor: StepperConfig::blowup_factor (threshold =
+ * factor * max(sup|phi|, 1e-300), stepping.cpp:121).  fw_tsfp2_step(t, k) runs k steps and
+ * stops at the first one whose sup|u| exceeds the threshold: FW_E_BLOWUP, n = that step,
+ * (u, v) = the state right after it (the reference's throw from step_tsfp2, stepping.cpp:302-303). */
 int fw_tsfp2_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
                     const double* order_values, int M, double kappa, int f_kind,
-                    const double* phi, const double* psi, double tau, fw_tsfp2* out);
+                    const double* phi, const double* psi, double tau, double blowup_factor,
+                    fw_tsfp2* out);
 void fw_tsfp2_destroy(fw_tsfp2 t);
 int fw_tsfp2_step(fw_tsfp2 t, int nsteps);
 int fw_tsfp2_get(fw_tsfp2 t, double* u_host, double* v_host, long* n);

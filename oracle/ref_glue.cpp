@@ -221,7 +221,7 @@ int ref_lffp(int d, const int* J, const double* lo, const double* hi, const doub
   });
 }
 
-// Stepper with Method::LFFP (0) / CNFP (1) (stepping.cpp:119-138, 170-264), f none (0) or
+// Stepper with Method::LFFP (0) / CNFP (1) / TSFP2 (2) (stepping.cpp:119-138, 170-304), f none (0) or
 // cubic (1), the StepperConfig fields as given.  After `nsteps` step() calls (or the one
 // that threw) cur_out = current(), *n_out = n(), *picard_out = total_picard_iterations().
 int ref_wave(int method, int d, const int* J, const double* lo, const double* hi, const double* s, int M,
@@ -240,7 +240,7 @@ int ref_wave(int method, int d, const int* J, const double* lo, const double* hi
     p.psi = Field(g, vec(psi, N));
     p.M = M;
     StepperConfig cfg;
-    cfg.method = method == 0 ? Method::LFFP : Method::CNFP;
+    cfg.method = method == 0 ? Method::LFFP : (method == 1 ? Method::CNFP : Method::TSFP2);
     cfg.tau = tau;
     cfg.picard_tol = picard_tol;
     cfg.picard_max_iters = picard_max_iters;

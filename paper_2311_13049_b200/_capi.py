@@ -127,6 +127,7 @@ def load_library():
     lib.fw_op_destroy.argtypes = [_vp]
     lib.fw_op_destroy.restype = None
     lib.fw_op_info.argtypes = [_vp, C.POINTER(OpInfo)]
+    lib.fw_op_path.argtypes = [_vp]
     lib.fw_apply.argtypes = [_vp, _dp, _dp, C.c_int, _dp]
     lib.fw_apply_device.argtypes = [_vp, _vp, _vp, C.c_int, _vp]
     lib.fw_apply_batch_device.argtypes = [C.POINTER(_vp), C.c_int, C.POINTER(_vp), C.POINTER(_vp)]
@@ -144,7 +145,7 @@ def load_library():
     lib.fw_seis_ops.argtypes = [_vp, C.POINTER(_vp), C.POINTER(_vp)]
     lib.fw_seis_medium.argtypes = [_vp, _dp, _dp, _dp]
     lib.fw_tsfp2_create.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp, C.c_int, C.c_double, C.c_int,
-                                    _dp, _dp, C.c_double, C.POINTER(_vp)]
+                                    _dp, _dp, C.c_double, C.c_double, C.POINTER(_vp)]
     lib.fw_tsfp2_destroy.argtypes = [_vp]
     lib.fw_tsfp2_destroy.restype = None
     lib.fw_tsfp2_step.argtypes = [_vp, C.c_int]

@@ -158,6 +158,11 @@ class ExpansionOperator:
     def handle(self):
         return self._h
 
+    @property
+    def persistent(self) -> bool:
+        """True when applies run on the single-launch persistent 2D kernel (fw_op_path)."""
+        return load_library().fw_op_path(self._h) == 1
+
     @classmethod
     def from_tables(cls, grid: Grid, M: int, s0: float, constant_order: bool, base_symbol,
                     log_weights, deviation_powers, ctx: Optional[Context] = None):
@@ -358,6 +363,13 @@ class SeismicStepper:
         check(load_library().fw_seis_medium(self._h, _ptr(c), _ptr(eta), _ptr(tc)))
         return c, eta, tc
 
+    @property
+    def persistent(self) -> bool:
+        """True when every step runs on the single-launch persistent 2D kernel."""
+        d, a = C.c_void_p(), C.c_void_p()
+        check(load_library().fw_seis_ops(self._h, C.byref(d), C.byref(a)))
+        return load_library().fw_op_path(d) == 1 and load_library().fw_op_path(a) == 1
+
     def operators(self):
         d, a = C.c_void_p(), C.c_void_p()
         check(load_library().fw_seis_ops(self._h, C.byref(d), C.byref(a)))
@@ -382,7 +394,7 @@ class TSFP2Stepper:
     u_tt = -kappa (-Delta)^{s(x)} u + f(u), f in {none, cubic}."""
 
     def __init__(self, order: OrderField, M: int, kappa: float, phi, psi, tau: float, f: str = "none",
-                 ctx: Optional[Context] = None):
+                 ctx: Optional[Context] = None, blowup_factor: float = 1e8):
         self.ctx = ctx or default_context()
         g = order.grid
         self.grid = g
@@ -391,7 +403,7 @@ class TSFP2Stepper:
         h = C.c_void_p()
         check(load_library().fw_tsfp2_create(self.ctx.handle, g.dim, J, lo, hi, _ptr(order.values), int(M),
                                              float(kappa), 1 if f == "cubic" else 0, _ptr(_f64(phi, N)),
-                                             _ptr(_f64(psi, N)), float(tau), C.byref(h)))
+                                             _ptr(_f64(psi, N)), float(tau), float(blowup_factor), C.byref(h)))
         self._h = h
         self.tau = float(tau)
 
@@ -463,10 +475,8 @@ class Stepper:
         self.grid = g
         self.method = config.method.upper()
         if self.method == "TSFP2":
-            if config.blowup_factor != 1e8:
-                raise ArgumentError("TSFP2 uses the reference's default blow-up factor 1e8")
             self._ts = TSFP2Stepper(problem.order, problem.M, problem.kappa, problem.phi, problem.psi, config.tau,
-                                    f=problem.f, ctx=self.ctx)
+                                    f=problem.f, ctx=self.ctx, blowup_factor=config.blowup_factor)
             return
         if self.method not in self._METHODS:
             raise ArgumentError(f"unknown method {config.method!r}")

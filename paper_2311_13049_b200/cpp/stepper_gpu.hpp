@@ -38,7 +38,7 @@ class Stepper {
     const int f = p.f.kind == Nonlinearity::Kind::Cubic ? 1 : 0;
     if (method_ == Method::TSFP2) {
       check(fw_tsfp2_create(ctx_, g.dim(), J, lo, hi, p.order.values().data(), p.M, p.kappa, f,
-                            p.phi.values().data(), p.psi.values().data(), cfg.tau, &ts_));
+                            p.phi.values().data(), p.psi.values().data(), cfg.tau, cfg.blowup_factor, &ts_));
     } else {
       check(fw_wave_create(ctx_, method_ == Method::LFFP ? 0 : 1, g.dim(), J, lo, hi, p.order.values().data(),
                            p.M, p.kappa, f, p.phi.values().data(), p.psi.values().data(), cfg.tau, cfg.picard_tol,

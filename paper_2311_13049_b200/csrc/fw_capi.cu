@@ -41,6 +41,13 @@ int set_err(int code, const std::string& msg) {
     }                                                                                   \
   } while (0)
 
+// every entry point that allocates or launches first makes its context's device current
+// (another context on another device may have switched it in this thread)
+#define FW_SETDEV(ctxp)                                      \
+  do {                                                       \
+    if (ctxp) FW_CUDA(cudaSetDevice((ctxp)->device));        \
+  } while (0)
+
 #define FW_TRY(expr)               \
   do {                             \
     int rc_ = (expr);              \
@@ -312,6 +319,7 @@ void fw_ctx_destroy(fw_ctx c) {
 }
 
 int fw_ctx_sync(fw_ctx c) {
+  FW_SETDEV(c);
   if (!c) return set_err(FW_E_ARG, "null ctx");
   FW_CUDA(cudaStreamSynchronize(c->stream));
   FW_CUDA(cudaGetLastError());
@@ -323,6 +331,7 @@ void* fw_ctx_stream(fw_ctx c) { return c ? (void*)c->stream : nullptr; }
 /* diagnostics: copy the persistent-kernel trace (2 x 32 x 136 x 8 + 2 x 160 x 2 x 136 u64) to host; FW_E_ARG if
    tracing is off */
 int fw_ctx_trace(fw_ctx c, unsigned long long* out) {
+  FW_SETDEV(c);
   if (!c || !c->trace || !out) return set_err(FW_E_ARG, "tracing disabled (set FW_TRACE=1 before fw_ctx_create)");
   FW_CUDA(cudaStreamSynchronize(c->stream));
   FW_CUDA(cudaMemcpy(out, c->trace, (2 * 32 * 136 * 8 + 2 * 160 * 2 * 136) * sizeof(unsigned long long),
@@ -445,9 +454,15 @@ int launch_persistent(fw_ctx ctx, fw_op const* ops, int nops, int m_first, const
   p.dbg = ctx->dbg;
   p.cset = ctx->cset;
   p.cstride = fw::kStep2dCStride;
-  ctx->cset ^= 1;
   cudaError_t e = fw::launch_step2d(p, ctx->stream, ctx->nsm);
-  if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("persistent 2D launch: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) {
+    // only a running kernel zeroes the other counter set: after a failed launch both sets are
+    // reset so that the next launch cannot find its spin targets already met
+    cudaGetLastError();
+    cudaMemsetAsync(ctx->counters, 0, 2 * (size_t)fw::kStep2dCStride * sizeof(unsigned long long), ctx->stream);
+    return set_err(FW_E_CUDA, std::string("persistent 2D launch: ") + cudaGetErrorString(e));
+  }
+  ctx->cset ^= 1;  // the launched kernel zeroes the other set for the next launch
   ctx->launches += 1;
   return FW_OK;
 }
@@ -551,6 +566,7 @@ int fw_op_create_from_tables(fw_ctx ctx, int dim, const int* J, const double* lo
 }
 
 void fw_op_destroy(fw_op op) {
+  if (op && op->ctx) cudaSetDevice(op->ctx->device);
   if (!op) return;
   if (op->w) cudaFree(op->w);
   if (op->dev1) cudaFree(op->dev1);
@@ -577,6 +593,14 @@ int fw_op_info(fw_op op, fw_op_info_t* info) {
   info->N_half = op->g.Nh;
   info->device_bytes = op->bytes;
   return FW_OK;
+}
+
+int fw_op_path(fw_op op) {
+  if (!op) {
+    set_err(FW_E_ARG, "null op");
+    return -1;
+  }
+  return use_persistent(op) ? FW_PATH_PERSISTENT_2D : FW_PATH_MULTIPASS;
 }
 
 int fw_apply(fw_op op, const double* u_host, double* out_host, int m_first, double* imag_residue) {
@@ -609,6 +633,7 @@ int fw_apply_device(fw_op op, const double* u_dev, double* out_dev, int m_first,
 }
 
 int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_dev, double* const* out_dev) {
+  FW_SETDEV((ops && nfields > 0 && ops[0] ? ops[0]->ctx : nullptr));
   if (!ops || !u_dev || !out_dev || nfields < 0) return set_err(FW_E_ARG, "null argument");
   for (int f = 0; f < nfields; ++f)
     if (!ops[f]) return set_err(FW_E_ARG, "null op in batch");
@@ -666,6 +691,7 @@ int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_
 }
 
 int fw_rfftn(fw_ctx ctx, int dim, const int* J, const double* x_host, double* H_host) {
+  FW_SETDEV(ctx);
   if (!ctx || !x_host || !H_host) return set_err(FW_E_ARG, "null argument");
   fw::GridGeom g;
   FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
@@ -680,6 +706,7 @@ int fw_rfftn(fw_ctx ctx, int dim, const int* J, const double* x_host, double* H_
 }
 
 int fw_irfftn(fw_ctx ctx, int dim, const int* J, const double* H_host, double* x_host) {
+  FW_SETDEV(ctx);
   if (!ctx || !x_host || !H_host) return set_err(FW_E_ARG, "null argument");
   fw::GridGeom g;
   FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
@@ -933,11 +960,13 @@ int fw_seis_create(fw_ctx ctx, int dim, const int* J, const double* lo, const do
 }
 
 void fw_seis_destroy(fw_seis s) {
+  if (s && s->ctx) cudaSetDevice(s->ctx->device);
   if (s && s->ctx) cudaStreamSynchronize(s->ctx->stream);
   seis_free(s);
 }
 
 int fw_seis_enqueue(fw_seis s, int nsteps) {
+  FW_SETDEV((s ? s->ctx : nullptr));
   if (!s || nsteps < 0) return set_err(FW_E_ARG, "bad argument");
   if (seis_persistent(s) && nsteps > 0) {
     const int per = s->ctx->steps_per_launch > 0 ? s->ctx->steps_per_launch : nsteps;
@@ -955,11 +984,13 @@ int fw_seis_enqueue(fw_seis s, int nsteps) {
 }
 
 int fw_seis_step(fw_seis s, int nsteps) {
+  FW_SETDEV((s ? s->ctx : nullptr));
   FW_TRY(fw_seis_enqueue(s, nsteps));
   return seis_check(s);
 }
 
 int fw_seis_get(fw_seis s, double* cur_host, double* prev_host, double* atten_prev_host, long* n) {
+  FW_SETDEV((s ? s->ctx : nullptr));
   if (!s) return set_err(FW_E_ARG, "null stepper");
   FW_TRY(seis_check(s));
   const size_t N = s->g.N;
@@ -973,12 +1004,14 @@ int fw_seis_get(fw_seis s, double* cur_host, double* prev_host, double* atten_pr
 }
 
 int fw_seis_set_current(fw_seis s, const double* cur_host) {
+  FW_SETDEV((s ? s->ctx : nullptr));
   if (!s || !cur_host) return set_err(FW_E_ARG, "null argument");
   FW_CUDA(cudaMemcpyAsync(s->cur(), cur_host, s->g.N * 8, cudaMemcpyHostToDevice, s->ctx->stream));
   return FW_OK;
 }
 
 int fw_seis_step_io(fw_seis s, const double* cur_in_host, int nsteps, double* cur_out_host) {
+  FW_SETDEV((s ? s->ctx : nullptr));
   if (!s) return set_err(FW_E_ARG, "null stepper");
   const size_t N = s->g.N;
   cudaStream_t st = s->ctx->stream;
@@ -1004,6 +1037,7 @@ int fw_seis_ops(fw_seis s, fw_op* disp, fw_op* atten) {
 }
 
 int fw_seis_medium(fw_seis s, double* c, double* eta, double* tau_coef) {
+  FW_SETDEV((s ? s->ctx : nullptr));
   if (!s) return set_err(FW_E_ARG, "null stepper");
   const size_t N = s->g.N;
   cudaStream_t st = s->ctx->stream;
@@ -1050,8 +1084,9 @@ void osc_flow(fw_tsfp2 t) {  // oscillator_flow(tau/2), stepping.cpp:271-291
   fw::launch_forward(L, t->g, t->u, t->uh, true);
   fw::launch_forward(L, t->g, t->v, t->vh, true);
   fw::launch_osc_rotate(L, t->g.Nh, t->w, t->cw, t->sw, 0.5 * t->tau, t->uh, t->vh);
-  fw::launch_irfft(L, t->g, t->uh, t->u);
-  fw::launch_irfft(L, t->g, t->vh, t->v);
+  // guarded: after a flagged step the later steps of the same call leave (u, v) untouched
+  fw::launch_irfft(L, t->g, t->uh, t->u, t->flag);
+  fw::launch_irfft(L, t->g, t->vh, t->v, t->flag);
 }
 
 }  // namespace
@@ -1060,7 +1095,7 @@ extern "C" {
 
 int fw_tsfp2_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
                     const double* order_values, int M, double kappa, int f_kind, const double* phi,
-                    const double* psi, double tau, fw_tsfp2* out) {
+                    const double* psi, double tau, double blowup_factor, fw_tsfp2* out) {
   if (!ctx || !out || !lo || !hi || !phi || !psi) return set_err(FW_E_ARG, "null argument");
   fw::GridGeom g;
   FW_TRY(check_grid(dim, J, lo, hi, &g));
@@ -1094,7 +1129,7 @@ int fw_tsfp2_create(fw_ctx ctx, int dim, const int* J, const double* lo, const d
   }
   double sup = 0.0;
   for (size_t j = 0; j < g.N; ++j) sup = std::max(sup, std::fabs(phi[j]));
-  t->thr = 1e8 * std::max(sup, 1e-300);
+  t->thr = blowup_factor * std::max(sup, 1e-300);  // stepping.cpp:121
   cudaStream_t st = ctx->stream;
   cudaMemcpyAsync(t->w, w.data(), g.Nh * 8, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(t->cw, cw.data(), g.Nh * 8, cudaMemcpyHostToDevice, st);
@@ -1113,11 +1148,13 @@ int fw_tsfp2_create(fw_ctx ctx, int dim, const int* J, const double* lo, const d
 }
 
 void fw_tsfp2_destroy(fw_tsfp2 t) {
+  if (t && t->ctx) cudaSetDevice(t->ctx->device);
   if (t && t->ctx) cudaStreamSynchronize(t->ctx->stream);
   tsfp2_free(t);
 }
 
 int fw_tsfp2_step(fw_tsfp2 t, int nsteps) {
+  FW_SETDEV((t ? t->ctx : nullptr));
   if (!t || nsteps < 0) return set_err(FW_E_ARG, "bad argument");
   auto L = t->ctx->L();
   const bool kick = !(t->A->constant_order && !t->cubic);  // stepping.cpp:295
@@ -1125,7 +1162,7 @@ int fw_tsfp2_step(fw_tsfp2 t, int nsteps) {
     osc_flow(t);
     if (kick) {
       FW_TRY(apply_device(t->A, t->u, t->pert, 1, nullptr, nullptr));
-      fw::launch_tsfp2_kick(L, t->g.N, t->tau, t->kappa, t->cubic, t->u, t->pert, t->v);
+      fw::launch_tsfp2_kick(L, t->g.N, t->tau, t->kappa, t->cubic, t->u, t->pert, t->v, t->flag);
     }
     osc_flow(t);
     t->n += 1;
@@ -1136,6 +1173,12 @@ int fw_tsfp2_step(fw_tsfp2 t, int nsteps) {
   FW_CUDA(cudaStreamSynchronize(t->ctx->stream));
   FW_CUDA(cudaGetLastError());
   if (flag != fw::kNoBlowup) {
+    // as the reference's throw from step_tsfp2 (stepping.cpp:302-303): n is the offending step,
+    // (u, v) the state right after it (later steps of this call were no-ops on the device)
+    t->n = flag;
+    const int none = fw::kNoBlowup;
+    FW_CUDA(cudaMemcpyAsync(t->flag, &none, sizeof(int), cudaMemcpyHostToDevice, t->ctx->stream));
+    FW_CUDA(cudaStreamSynchronize(t->ctx->stream));
     char b[128];
     snprintf(b, sizeof b, "sup|u| > %g at step %d", t->thr, flag);
     return set_err(FW_E_BLOWUP, b);
@@ -1144,6 +1187,7 @@ int fw_tsfp2_step(fw_tsfp2 t, int nsteps) {
 }
 
 int fw_tsfp2_get(fw_tsfp2 t, double* u_host, double* v_host, long* n) {
+  FW_SETDEV((t ? t->ctx : nullptr));
   if (!t) return set_err(FW_E_ARG, "null stepper");
   cudaStream_t st = t->ctx->stream;
   if (u_host) FW_CUDA(cudaMemcpyAsync(u_host, t->u, t->g.N * 8, cudaMemcpyDeviceToHost, st));
@@ -1336,11 +1380,13 @@ int fw_wave_create(fw_ctx ctx, int method, int dim, const int* J, const double* 
 }
 
 void fw_wave_destroy(fw_wave t) {
+  if (t && t->ctx) cudaSetDevice(t->ctx->device);
   if (t && t->ctx) cudaStreamSynchronize(t->ctx->stream);
   wave_free(t);
 }
 
 int fw_wave_step(fw_wave t, int nsteps) {
+  FW_SETDEV((t ? t->ctx : nullptr));
   if (!t || nsteps < 0) return set_err(FW_E_ARG, "bad argument");
   auto L = t->ctx->L();
   const size_t N = t->g.N;
@@ -1390,6 +1436,7 @@ int fw_wave_step(fw_wave t, int nsteps) {
 }
 
 int fw_wave_get(fw_wave t, double* cur_host, double* prev_host, long* n, long* picard_total) {
+  FW_SETDEV((t ? t->ctx : nullptr));
   if (!t) return set_err(FW_E_ARG, "null stepper");
   cudaStream_t st = t->ctx->stream;
   if (cur_host) FW_CUDA(cudaMemcpyAsync(cur_host, t->ub[t->lvl % 3], t->g.N * 8, cudaMemcpyDeviceToHost, st));
@@ -1410,6 +1457,7 @@ int fw_wave_get(fw_wave t, double* cur_host, double* prev_host, long* n, long* p
 extern "C" {
 
 int fw_stage_r2c(fw_ctx ctx, int dim, const int* J, const double* x_dev, double* H_dev, double scale) {
+  FW_SETDEV(ctx);
   if (!ctx || !x_dev || !H_dev) return set_err(FW_E_ARG, "null argument");
   fw::GridGeom g;
   FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
@@ -1420,6 +1468,7 @@ int fw_stage_r2c(fw_ctx ctx, int dim, const int* J, const double* x_dev, double*
 
 int fw_stage_c2c(fw_ctx ctx, int dim, const int* J, int axis, int dir, const double* src_dev, double* dst_dev,
                  const double* w_dev, long long src_ts, long long dst_ts, long long w_ts, int nterms, double scale) {
+  FW_SETDEV(ctx);
   if (!ctx || !src_dev || !dst_dev || nterms < 1) return set_err(FW_E_ARG, "bad argument");
   fw::GridGeom g;
   FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));
@@ -1453,6 +1502,7 @@ int fw_medium_coefficients(long long n, const double* gamma, const double* c0, d
 int fw_stage_seis_start(fw_ctx ctx, long long n, double tau, const double* phi, const double* psi, const double* c,
                         const double* eta, const double* tau_coef, const double* l1phi, const double* l2psi,
                         double* cur) {
+  FW_SETDEV(ctx);
   if (!ctx || n < 0 || !phi || !psi || !c || !eta || !tau_coef || !l1phi || !l2psi || !cur)
     return set_err(FW_E_ARG, "null argument");
   fw::launch_seis_start(ctx->L(), (size_t)n, tau, phi, psi, c, eta, tau_coef, l1phi, l2psi, cur);
@@ -1463,6 +1513,7 @@ int fw_stage_seis_start(fw_ctx ctx, long long n, double tau, const double* phi, 
 int fw_stage_seis_update(fw_ctx ctx, long long n, double tau, const double* cur, const double* prev,
                          const double* l2prev, const double* l1, const double* l2, const double* c, const double* eta,
                          const double* tau_coef, double* next, double thr, int step, int* flag_dev) {
+  FW_SETDEV(ctx);
   if (!ctx || n < 0 || !cur || !prev || !l2prev || !l1 || !l2 || !c || !eta || !tau_coef || !next || !flag_dev)
     return set_err(FW_E_ARG, "null argument");
   fw::launch_seis_update(ctx->L(), (size_t)n, tau, cur, prev, l2prev, l1, l2, c, eta, tau_coef, next, thr, step,
@@ -1498,6 +1549,7 @@ int fw_stage_c2c_scatter(fw_ctx ctx, int dim, const int* J, int axis, int dir, c
                          const double* w_dev, long long src_ts, long long w_ts, int nterms, double scale, int nq,
                          double* const* dst_q, long long blk, long long jstride, long long ostride,
                          long long tstride, long long base) {
+  FW_SETDEV(ctx);
   if (!ctx || !src_dev || !dst_q || nterms < 1 || nq < 1 || nq > fw::kMaxScatter || blk < 1)
     return set_err(FW_E_ARG, "bad argument");
   fw::GridGeom g;
@@ -1533,6 +1585,7 @@ int fw_stage_c2c_scatter(fw_ctx ctx, int dim, const int* J, int axis, int dir, c
 
 int fw_stage_c2r_accum(fw_ctx ctx, int dim, const int* J, const double* src_dev, long long src_ts, int m_first,
                        int m_last, const double* dev1_dev, double* out_dev, double* residue_dev) {
+  FW_SETDEV(ctx);
   if (!ctx || !src_dev || !out_dev || m_last < m_first) return set_err(FW_E_ARG, "bad argument");
   fw::GridGeom g;
   FW_TRY(check_grid(dim, J, nullptr, nullptr, &g));

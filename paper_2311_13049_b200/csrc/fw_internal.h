@@ -5,7 +5,21 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include <atomic>
+
 namespace fw {
+
+// Kernel attributes (cudaFuncSetAttribute) are per device: run `f` once for every device
+// that becomes current here (a repeat by a racing thread is harmless).
+template <class F>
+inline void once_per_device(std::atomic<unsigned long long>& done, F f) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_release);
+}
 
 struct GridGeom {
   int d = 0;
@@ -71,9 +85,11 @@ void launch_osc_rotate(const LaunchCtx& L, size_t Nh, const double* w, const dou
 // raise the dynamic shared-memory limit of the FFT kernels on the current device
 void init_kernels();
 void launch_tsfp2_kick(const LaunchCtx& L, size_t N, double tau, double kappa, int cubic, const double* u,
-                       const double* pert, double* v);
+                       const double* pert, double* v, const int* guard = nullptr);
 // unscaled inverse of one spectrum to reals (C2C axes 0..d-2 + C2R), in place on H
-void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x);
+// guard (nullable): the final write of x is skipped when *guard != kNoBlowup (a blow-up was
+// flagged earlier in the same multi-step enqueue: the state stays at the offending step)
+void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x, const int* guard = nullptr);
 void launch_sup_check(const LaunchCtx& L, size_t N, const double* u, double thr, int step, int* flag);
 
 // two-level integrators LFFP / CNFP (stepping.cpp:88-104, 170-264), fw_wave.cu

@@ -300,7 +300,8 @@ __global__ void k_osc_rotate(long long Nh, const double* __restrict__ w, const d
 }
 
 __global__ void k_tsfp2_kick(long long N, double tau, double kappa, int cubic, const double* __restrict__ u,
-                             const double* __restrict__ pert, double* __restrict__ v) {
+                             const double* __restrict__ pert, double* __restrict__ v, const int* guard) {
+  if (guard && *guard != kNoBlowup) return;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
     const double fu = cubic ? u[j] * u[j] * u[j] : 0.0;
     v[j] += tau * (-kappa * pert[j] + fu);
@@ -413,9 +414,9 @@ void launch_inverse(const LaunchCtx& L, const GridGeom& g, const InverseArgs& a)
   c2r_accum(L, g, a.T, (long long)g.Nh, nullptr, 0, a.m_first, a.m_last, a.dev1, a.out, a.residue, a.guard);
 }
 
-void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x) {
+void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x, const int* guard) {
   for (int ax = 0; ax <= g.d - 2; ++ax) c2c_axis(L, g, ax, +1, H, H, nullptr, 0, 0, 0, 1, 1.0, false);
-  c2r_accum(L, g, H, 0, nullptr, 0, 0, 0, nullptr, x, nullptr, nullptr);
+  c2r_accum(L, g, H, 0, nullptr, 0, 0, 0, nullptr, x, nullptr, guard);
 }
 
 void launch_build_weights(const LaunchCtx& L, size_t Nh, int M, const double* mu2h, const double* base,
@@ -458,8 +459,8 @@ void launch_osc_rotate(const LaunchCtx& L, size_t Nh, const double* w, const dou
 }
 
 void launch_tsfp2_kick(const LaunchCtx& L, size_t N, double tau, double kappa, int cubic, const double* u,
-                       const double* pert, double* v) {
-  k_tsfp2_kick<<<elementwise_grid(N), kThreads, 0, L.stream>>>((long long)N, tau, kappa, cubic, u, pert, v);
+                       const double* pert, double* v, const int* guard) {
+  k_tsfp2_kick<<<elementwise_grid(N), kThreads, 0, L.stream>>>((long long)N, tau, kappa, cubic, u, pert, v, guard);
   count(L);
 }
 

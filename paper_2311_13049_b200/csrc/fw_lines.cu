@@ -825,14 +825,13 @@ bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, co
               int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
   constexpr int LPB = Plan<N, NTH>::L;
   constexpr size_t SMEM = (size_t)LPB * Plan<N, NTH>::LLS * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_lines<N, -1, false, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     cudaFuncSetAttribute(k_lines<N, +1, false, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     cudaFuncSetAttribute(k_lines<N, -1, true, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     cudaFuncSetAttribute(k_lines<N, +1, true, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    attr = true;
-  }
+  });
   const long long bpo = (inner + LPB - 1) / LPB;
   const Scatter none{};
   const Scatter& sc_ = scatter ? *scatter : none;
@@ -840,12 +839,11 @@ bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, co
   if (FW_LINES_TERMS && dir > 0 && src_ts == 0 && nterms > 1 && (w || (bl && w_ts != 0))) {  // (launch_n's `terms`)
     // every term of an inverse from one uhat: one pass over the spectrum (k_lines_terms)
     constexpr size_t TSM = TermPlan<N, NTH>::SMEM;
-    static bool tattr = false;
-    if (!tattr) {
+    static std::atomic<unsigned long long> tattr{0};
+    once_per_device(tattr, [] {
       cudaFuncSetAttribute(k_lines_terms<N, false, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
       cudaFuncSetAttribute(k_lines_terms<N, true, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSM);
-      tattr = true;
-    }
+    });
     // enough blocks to fill the GPU: split the term range when the lines alone give fewer than
     // ~4 waves of two blocks per SM (uhat is then read once per chunk)
     const long long nb = outer * bpo * nfields;
@@ -901,11 +899,10 @@ bool launch_rows_r2c_t(const LaunchCtx& L, const double* u, double2* Uh, long lo
                        bool scale, const BatchLine* bl) {
   using RP = RowPlan<H>;
   constexpr size_t SMEM = (size_t)RP::RPB * C2RPlan<H>::LS * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_rows_r2c<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    attr = true;
-  }
+  });
   const dim3 grid((unsigned)((rows + RP::RPB - 1) / RP::RPB), 1, (unsigned)nfields);
   k_rows_r2c<H><<<grid, RP::NT, SMEM, L.stream>>>(u, Uh, rows, sc, scale ? 1 : 0, L.master, bl);
   if (L.launches) *L.launches += 1;
@@ -917,11 +914,10 @@ bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m
                  const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
                  const BatchLine* bl) {
   using RP = C2RPlan<H>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_rows_c2r<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RP::SMEM);
-    attr = true;
-  }
+  });
   const dim3 grid((unsigned)((rows + RP::RPB - 1) / RP::RPB), 1, (unsigned)nfields);
   k_rows_c2r<H><<<grid, RP::NT, RP::SMEM, L.stream>>>(src, src_ts, m_first, m_last, dev1, out, rows, residue, guard,
                                                     L.master, bl);

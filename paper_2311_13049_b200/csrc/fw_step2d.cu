@@ -1090,11 +1090,10 @@ template <int J0, int J1, int RMAX>
 cudaError_t launch_t(const Step2DParams& p, cudaStream_t st, int nblk) {
   using G = Geo<J0, J1, RMAX>;
   if ((J0 + nblk - 1) / nblk > RMAX || 2 * nblk < G::NSLOT) return cudaErrorInvalidConfiguration;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_step2d<J0, J1, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-    attr = true;
-  }
+  });
   // the term ring as a 3D tensor of doubles [KRING][h][2 J0]; box = 8 rows (128 B) x 256 k
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {

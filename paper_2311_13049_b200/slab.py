@@ -373,7 +373,10 @@ class SlabSeismicStepper:
                                                  self.flag.data_ptr()))
 
     def blown(self):
-        """The offending step over all ranks (flag_reduce = a min all-reduce), or None."""
+        """The offending step over all ranks (flag_reduce = a min all-reduce), or None.
+        fw_stage_seis_update wrote the flag on the context's (non-blocking) stream: wait for
+        it before torch reads the flag on its own stream."""
+        self.ctx.sync()
         f = self.flag.clone()
         if self.flag_reduce is not None:
             f = self.flag_reduce(f)

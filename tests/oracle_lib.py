@@ -324,13 +324,14 @@ def ref_lffp(J, lo, hi, s, M, kappa, phi, psi, tau, nsteps):
 def ref_wave(method, J, lo, hi, s, M, kappa, cubic, phi, psi, tau, nsteps, picard_tol=1e-12,
              picard_max_iters=200, inner_cg_tol=1e-14, cg_max_iters=500, blowup_factor=1e8,
              allow_error=False):
-    """Stepper with Method::LFFP ("LFFP") / CNFP ("CNFP") (stepping.cpp:119-138, 170-264).
+    """Stepper with Method::LFFP ("LFFP") / CNFP ("CNFP") / TSFP2 ("TSFP2") (stepping.cpp:119-138,
+    170-304).
     Returns (current, n, total_picard_iterations[, rc])."""
     lib = reference()
     J = _i32(J)
     cur = np.empty(int(np.prod(J)))
     n, pt = C.c_long(), C.c_long()
-    rc = lib.ref_wave({"LFFP": 0, "CNFP": 1}[method], len(J), J, _f64(lo), _f64(hi), _f64(s).ravel(), int(M),
+    rc = lib.ref_wave({"LFFP": 0, "CNFP": 1, "TSFP2": 2}[method], len(J), J, _f64(lo), _f64(hi), _f64(s).ravel(), int(M),
                       float(kappa), int(bool(cubic)), _f64(phi).ravel(), _f64(psi).ravel(), float(tau),
                       float(picard_tol), int(picard_max_iters), float(inner_cg_tol), int(cg_max_iters),
                       float(blowup_factor), int(nsteps), cur, C.byref(n), C.byref(pt))

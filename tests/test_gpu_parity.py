@@ -266,10 +266,11 @@ def generic_context():
         del os.environ["FW_FORCE_GENERIC"]
 
 
-@pytest.mark.parametrize("J", [(256, 256), (512, 512), (512, 1024), (1024, 512), (1024, 1024)])
+@pytest.mark.parametrize("J", [(512, 1024), (1024, 1024)])
 def test_persistent_2d_apply_bitwise(J):
-    """The single-launch persistent kernel (fw_step2d.cu) and the multi-pass kernels
-    implement the same canonical arithmetic: identical bits, both m_first values."""
+    """The single-launch persistent kernel (fw_step2d.cu; asserted to serve these shapes)
+    and the multi-pass kernels implement the same canonical arithmetic: identical bits,
+    both m_first values, and both equal to the oracle."""
     m = fw()
     lo, hi = (-16.0, -16.0), (16.0, 16.0)
     g = grid_of(J, lo, hi)
@@ -280,33 +281,51 @@ def test_persistent_2d_apply_bitwise(J):
     gctx = generic_context()
     op_p = m.build_expansion(m.OrderField(g, s), 16)
     op_g = m.build_expansion(m.OrderField(g, s), 16, ctx=gctx)
+    assert op_p.persistent and not op_g.persistent
     for m_first in (0, 1):
         a, ra = op_p.apply(u, m_first, residue=True)
         b, rb = op_g.apply(u, m_first, residue=True)
         assert np.array_equal(a, b), rel_l2(a, b)
         assert ra == rb
-    if J == (256, 256):
-        ref, rres = O.port_apply(J, lo, hi, s, u, 16)
-        assert np.array_equal(op_p.apply(u), ref)
+        ref, rres = O.port_apply(J, lo, hi, s, u, 16, m_first=m_first)
+        assert np.array_equal(a, ref) and ra == rres
 
 
-@pytest.mark.parametrize("n", [256, 1024])
-def test_persistent_2d_seismic_bitwise(n):
+@pytest.mark.parametrize("J", [(256, 256), (512, 512), (1024, 512), (2048, 256)])
+def test_multipass_2d_apply_vs_oracle(J):
+    """2D shapes the persistent kernel does not serve run the multi-pass line kernels
+    (asserted): bitwise against the oracle, both m_first values."""
     m = fw()
-    cfg = cfgs.c2(n)
+    lo, hi = (-16.0, -16.0), (16.0, 16.0)
+    g = grid_of(J, lo, hi)
+    rng = np.random.default_rng(7 * J[0] + J[1])
+    s = np.clip(1.0 + 0.4 * cfgs.mode_sum(lo, hi, J, *cfgs.random_modes(rng, 6, 3, 2)) / 6.0, 0.6, 1.4)
+    u = rng.standard_normal(J)
+    op = m.build_expansion(m.OrderField(g, s), 16)
+    assert not op.persistent
+    for m_first in (0, 1):
+        a, ra = op.apply(u, m_first, residue=True)
+        ref, rres = O.port_apply(J, lo, hi, s, u, 16, m_first=m_first)
+        assert np.array_equal(a, ref) and ra == rres
+
+
+def test_persistent_2d_seismic_bitwise():
+    """7 seismic steps at 1024^2: persistent kernel (asserted) = multi-pass path = oracle."""
+    m = fw()
+    cfg = cfgs.c2(1024)
     g = grid_of(cfg.J, cfg.lo, cfg.hi)
     med = m.build_medium(g, cfg.gamma, cfg.c0, cfg.omega0, cfg.M)
     st_p = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau)
     st_g = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau, ctx=generic_context())
+    assert st_p.persistent and not st_g.persistent
     st_p.advance(7)
     st_g.advance(7)
     for a, b in zip(st_p.state(), st_g.state()):
         assert np.array_equal(a, b)
-    if n == 256:
-        rcur, rprev, rap, rn = O.port_seismic(cfg.J, cfg.lo, cfg.hi, cfg.gamma, cfg.c0, cfg.omega0, cfg.M,
-                                              cfg.phi, cfg.psi, cfg.tau, 7)
-        cur, prev, ap, n_ = st_p.state()
-        assert n_ == rn and np.array_equal(cur, rcur) and np.array_equal(ap, rap)
+    rcur, rprev, rap, rn = O.port_seismic(cfg.J, cfg.lo, cfg.hi, cfg.gamma, cfg.c0, cfg.omega0, cfg.M,
+                                          cfg.phi, cfg.psi, cfg.tau, 7)
+    cur, prev, ap, n_ = st_p.state()
+    assert n_ == rn and np.array_equal(cur, rcur) and np.array_equal(prev, rprev) and np.array_equal(ap, rap)
 
 
 def test_c2_200_steps_vs_multipass():
@@ -318,6 +337,7 @@ def test_c2_200_steps_vs_multipass():
     med = m.build_medium(g, cfg.gamma, cfg.c0, cfg.omega0, cfg.M)
     st_p = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau)
     st_g = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau, ctx=generic_context())
+    assert st_p.persistent and not st_g.persistent
     st_p.advance(cfg.steps)
     st_g.advance(cfg.steps)
     a, b = st_p.current(), st_g.current()
@@ -522,31 +542,32 @@ def test_fused_transpose_slab_equals_single_gpu_apply(P, J):
         assert np.array_equal(got, op.apply(u, m_first))
 
 
-@pytest.mark.parametrize("P", [1, 2])
-def test_slab_seismic_stepper_equals_single_gpu(P):
-    """The slab-decomposed SeismicStepper (fused transposes, shared forward transform, fused
-    update) with P virtual ranks on one device (phases interleaved by the host): cur, prev,
-    L2prev and n identical to the single-GPU SeismicStepper after 5 steps."""
-    import torch
-
-    m = fw()
-    from paper_2311_13049_b200.slab import LocalPeers, SlabGeometry, SlabSeismicStepper
-
-    # the fused transposes need axis lengths 256/512/1024 for the two transposed axes
+def _slab_case():
     J, lo, hi = (256, 256, 8), (-4.0, -4.0, -1.0), (4.0, 4.0, 1.0)
     x = [lo[a] + (hi[a] - lo[a]) * np.arange(J[a]) / J[a] for a in range(3)]
     X, Y, Z = np.meshgrid(*x, indexing="ij")
     gamma = 0.02 + 0.015 * np.sin(X) * np.cos(0.5 * Y)
     phi = np.exp(-(X**2 + Y**2 + Z**2) / 0.5)
+    return J, lo, hi, gamma, phi
 
-    class Cfg:
-        pass
 
-    cfg = Cfg()
-    cfg.gamma, cfg.c0, cfg.omega0, cfg.phi, cfg.psi, cfg.tau = gamma, np.ones(J), 1.0, phi, np.zeros(J), 1e-3
+def _slab_run(P, tau, blowup_factor, nsteps):
+    """P virtual ranks of SlabSeismicStepper on one device (phases interleaved by the host)
+    next to the single-GPU SeismicStepper.  Returns (ref stepper, ref exception or None,
+    slab states (cur, prev, L2prev) concatenated, slab n, slab offending step or None)."""
+    m = fw()
+    from paper_2311_13049_b200.slab import LocalPeers, SlabGeometry, SlabSeismicStepper
+
+    # the fused transposes need axis lengths 256/512/1024 for the two transposed axes
+    J, lo, hi, gamma, phi = _slab_case()
+    c0, psi = np.ones(J), np.zeros(J)
     g = m.Grid(list(zip(lo, hi)), list(J))
-    ref = m.SeismicStepper(m.build_medium(g, cfg.gamma, cfg.c0, cfg.omega0, 6), cfg.phi, cfg.psi, cfg.tau)
-    ref.advance(5)
+    ref = m.SeismicStepper(m.build_medium(g, gamma, c0, 1.0, 6), phi, psi, tau, blowup_factor=blowup_factor)
+    ref_exc = None
+    try:
+        ref.advance(nsteps)
+    except m.BlowupDetected as e:
+        ref_exc = e
     ctx = m.default_context()
     shared = {}
 
@@ -555,8 +576,8 @@ def test_slab_seismic_stepper_equals_single_gpu(P):
             shared[k] = LocalPeers(SlabGeometry(J, P, 0), nt, ctx_)
         return shared[k]
 
-    sts = [SlabSeismicStepper(g, cfg.gamma, cfg.c0, cfg.omega0, 6, cfg.phi, cfg.psi, cfg.tau, SlabGeometry(J, P, r),
-                              ctx, peers_factory, construct=False) for r in range(P)]
+    sts = [SlabSeismicStepper(g, gamma, c0, 1.0, 6, phi, psi, tau, SlabGeometry(J, P, r), ctx, peers_factory,
+                              blowup_factor=blowup_factor, construct=False) for r in range(P)]
     # constructor applies, phase by phase over the virtual ranks
     outs = {}
     for key, k, field in (("l1phi", 0, "phi_l"), ("l2psi", 1, "psi_l"), ("l2phi", 1, "phi_l")):
@@ -569,7 +590,8 @@ def test_slab_seismic_stepper_equals_single_gpu(P):
         outs[key] = [st.apps[k].phase_finish(0) for st in sts]
     for r, st in enumerate(sts):
         st.start(outs["l1phi"][r], outs["l2psi"][r], outs["l2phi"][r])
-    for _ in range(5):
+    bad = None
+    for _ in range(nsteps):
         for st in sts:
             st.phase_forward()
         ctx.sync()
@@ -578,13 +600,50 @@ def test_slab_seismic_stepper_equals_single_gpu(P):
         ctx.sync()
         for st in sts:
             st.phase_update()
-        assert all(st.blown() is None for st in sts)
+        flags = [st.blown() for st in sts]  # the min all-reduce of flag_reduce, by hand
+        flags = [f for f in flags if f is not None]
+        if flags:
+            bad = min(flags)
+            break
         for st in sts:
             st.commit()
     ctx.sync()
-    cur_r, prev_r, ap_r, n_r = ref.state()
     got = [np.concatenate([st.state()[i].cpu().numpy() for st in sts]) for i in range(3)]
-    assert sts[0].n == n_r
+    return ref, ref_exc, got, sts[0].n, bad
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_slab_seismic_stepper_equals_single_gpu(P):
+    """The slab-decomposed SeismicStepper (fused transposes, shared forward transform, fused
+    update) with P virtual ranks on one device: cur, prev, L2prev and n identical to the
+    single-GPU SeismicStepper after 5 steps."""
+    ref, ref_exc, got, n, bad = _slab_run(P, 1e-3, 1e8, 5)
+    assert ref_exc is None and bad is None
+    cur_r, prev_r, ap_r, n_r = ref.state()
+    assert n == n_r
+    for a, b in zip(got, (cur_r, prev_r, ap_r)):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_slab_seismic_stepper_blowup_matches_single_gpu(P):
+    """A blow-up inside the slab stepper: the flag written on the context stream is read
+    after that stream (blown() syncs it), the offending step equals the single-GPU
+    stepper's BlowupDetected step, and the slab state is the pre-step state (seismic.cpp:124-129)."""
+    m = fw()
+    J, lo, hi, gamma, phi = _slab_case()
+    tau = 0.05  # far above the explicit scheme's stability limit: sup|u| grows every step
+    probe = m.SeismicStepper(m.build_medium(m.Grid(list(zip(lo, hi)), list(J)), gamma, np.ones(J), 1.0, 6), phi,
+                             np.zeros(J), tau, blowup_factor=1e300)
+    sups = []
+    for _ in range(4):
+        probe.step()
+        sups.append(np.abs(probe.current()).max())
+    assert sups[3] > max(sups[:3]) > 0
+    factor = np.sqrt(max(max(sups[:3]), 1.0) * sups[3]) / np.abs(phi).max()  # first exceeded at n = 5
+    ref, ref_exc, got, n, bad = _slab_run(P, tau, factor, 6)
+    assert ref_exc is not None and ref.n() == 5 and bad == 5
+    cur_r, prev_r, ap_r, _ = ref.state()
     for a, b in zip(got, (cur_r, prev_r, ap_r)):
         assert np.array_equal(a, b)
 

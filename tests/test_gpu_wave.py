@@ -142,3 +142,24 @@ def test_stepper_facade_tsfp2_matches_golden(manifest):
     assert st.n() == c["steps"]
     assert np.array_equal(st.current(), load_golden(c, "u"))
     assert np.array_equal(st.velocity(), load_golden(c, "v"))
+
+
+@pytest.mark.parametrize("blowup_factor", [2.0, 5.0])
+def test_tsfp2_blowup_in_a_batch_matches_reference(blowup_factor):
+    """TSFP2 (stepping.cpp:266-304) blowing up inside one multi-step advance(): the device
+    leaves (u, v) at the offending step, n() is that step and u the state right after it,
+    as after the reference's throw; the StepperConfig blow-up factor is honoured."""
+    m = fw()
+    J, lo, hi = (256,), (-16.0,), (16.0,)
+    x = lo[0] + np.arange(256) * (32.0 / 256)
+    s = 1.0 + 0.3 * np.sin(np.pi * x / 8)
+    phi = 3.0 * np.exp(-x**2)
+    tau = 0.05
+    cur_r, n_r, _, rc = O.ref_wave("TSFP2", J, lo, hi, s, 15, 1.0, 1, phi, np.zeros(J), tau, 40,
+                                   blowup_factor=blowup_factor, allow_error=True)
+    assert rc == 7 and 1 < n_r < 40
+    st = stepper(J, lo, hi, s, 15, 1.0, "cubic", phi, np.zeros(J), "TSFP2", tau, blowup_factor=blowup_factor)
+    with pytest.raises(m.BlowupDetected):
+        st.advance(40)
+    assert st.n() == n_r
+    assert np.array_equal(st.current(), cur_r)
