@@ -73,8 +73,10 @@ int fw_ctx_sync(fw_ctx ctx);
 void* fw_ctx_stream(fw_ctx ctx);
 /* number of kernels this context has launched so far (diagnostics / bench) */
 long long fw_ctx_launches(fw_ctx ctx);
-/* diagnostics: persistent-kernel phase timestamps (needs FW_TRACE=1 at context creation);
- * out receives 2 x 32 x 136 x 8 unsigned 64-bit globaltimer values */
+/* diagnostics: the persistent 2D kernel's watchdog records (needs FW_TRACE=1 at context
+ * creation; mapped host memory, readable even after the kernel trapped): out receives
+ * 1024 x 16 unsigned 64-bit words, per CTA two records (producer, compute warps) of 8 words
+ * {wait site, thread, value seen, target, term, globaltimer} */
 int fw_ctx_trace(fw_ctx ctx, unsigned long long* out);
 
 /* ---- operator: ExpansionOperator resident on the device ----

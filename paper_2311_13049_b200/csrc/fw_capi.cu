@@ -210,8 +210,10 @@ struct fw_ctx_s {
   bool force_generic = false;                 // FW_FORCE_GENERIC=1: multi-pass kernels only
   int dbg = 0;                                // FW_STEP2D_DBG: timing experiments only (wrong results)
   int steps_per_launch = 0;                   // FW_STEPS_PER_LAUNCH: seismic steps per persistent launch (0 = all)
+  bool step2d_tm = false;                     // FW_STEP2D_TM=1: time-multiplexed persistent kernel (A/B)
   unsigned long long* counters = nullptr;     // persistent-kernel counters (2 sets)
-  unsigned long long* trace = nullptr;        // FW_TRACE=1: persistent-kernel phase timestamps
+  unsigned long long* trace = nullptr;        // FW_TRACE=1: persistent-kernel watchdog records (device view)
+  unsigned long long* trace_host = nullptr;   //   ... the same buffer, mapped host memory (survives a trap)
   int cset = 0;
   bool generic_lines = false;                 // FW_GENERIC_LINES=1: shared-memory line FFTs only (tests)
   fw::LaunchCtx L() { return fw::LaunchCtx{stream, master, &launches, generic_lines}; }
@@ -287,6 +289,8 @@ int fw_ctx_create(int device, fw_ctx* out) {
   c->generic_lines = gl && gl[0] == '1';
   const char* dg = getenv("FW_STEP2D_DBG");
   c->dbg = dg ? atoi(dg) : 0;
+  const char* tm = getenv("FW_STEP2D_TM");
+  c->step2d_tm = tm && tm[0] == '1';
   const char* spl = getenv("FW_STEPS_PER_LAUNCH");
   c->steps_per_launch = spl ? std::max(0, atoi(spl)) : 0;
   if (dalloc(&c->counters, 2 * (size_t)fw::kStep2dCStride)) {
@@ -296,8 +300,14 @@ int fw_ctx_create(int device, fw_ctx* out) {
   FW_CUDA(cudaMemset(c->counters, 0, 2 * (size_t)fw::kStep2dCStride * sizeof(unsigned long long)));
   const char* tr = getenv("FW_TRACE");
   if (tr && tr[0] == '1') {
-    const size_t n = 2 * 32 * 136 * 8 + 2 * 160 * 2 * 136;  // + per-CTA column-group term ends
-    if (dalloc(&c->trace, n) == FW_OK) cudaMemset(c->trace, 0, n * sizeof(unsigned long long));
+    const size_t n = (size_t)fw::kTraceWords;
+    if (cudaHostAlloc((void**)&c->trace_host, n * sizeof(unsigned long long), cudaHostAllocMapped) == cudaSuccess) {
+      memset(c->trace_host, 0, n * sizeof(unsigned long long));
+      if (cudaHostGetDevicePointer((void**)&c->trace, c->trace_host, 0) != cudaSuccess) c->trace = nullptr;
+    } else {
+      cudaGetLastError();
+      c->trace_host = nullptr;
+    }
   }
   fw::init_kernels();
   *out = c;
@@ -313,7 +323,7 @@ void fw_ctx_destroy(fw_ctx c) {
   if (c->master) cudaFree(c->master);
   if (c->residue) cudaFree(c->residue);
   if (c->counters) cudaFree(c->counters);
-  if (c->trace) cudaFree(c->trace);
+  if (c->trace_host) cudaFreeHost(c->trace_host);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -328,14 +338,13 @@ int fw_ctx_sync(fw_ctx c) {
 
 void* fw_ctx_stream(fw_ctx c) { return c ? (void*)c->stream : nullptr; }
 
-/* diagnostics: copy the persistent-kernel trace (2 x 32 x 136 x 8 + 2 x 160 x 2 x 136 u64) to host; FW_E_ARG if
-   tracing is off */
+/* diagnostics: the persistent kernel's watchdog records (kTraceWords u64: per CTA 8 words = site, thread,
+   counter value seen, target, term, globaltimer), readable even after the kernel trapped; FW_E_ARG if
+   FW_TRACE=1 was not set at context creation */
 int fw_ctx_trace(fw_ctx c, unsigned long long* out) {
-  FW_SETDEV(c);
-  if (!c || !c->trace || !out) return set_err(FW_E_ARG, "tracing disabled (set FW_TRACE=1 before fw_ctx_create)");
-  FW_CUDA(cudaStreamSynchronize(c->stream));
-  FW_CUDA(cudaMemcpy(out, c->trace, (2 * 32 * 136 * 8 + 2 * 160 * 2 * 136) * sizeof(unsigned long long),
-                     cudaMemcpyDeviceToHost));
+  if (!c || !c->trace_host || !out) return set_err(FW_E_ARG, "tracing disabled (set FW_TRACE=1 before fw_ctx_create)");
+  if (c->stream) cudaStreamSynchronize(c->stream);  // a trapped kernel leaves a sticky error: ignored here
+  memcpy(out, c->trace_host, (size_t)fw::kTraceWords * sizeof(unsigned long long));
   return FW_OK;
 }
 long long fw_ctx_launches(fw_ctx c) { return c ? c->launches : 0; }
@@ -454,7 +463,8 @@ int launch_persistent(fw_ctx ctx, fw_op const* ops, int nops, int m_first, const
   p.dbg = ctx->dbg;
   p.cset = ctx->cset;
   p.cstride = fw::kStep2dCStride;
-  cudaError_t e = fw::launch_step2d(p, ctx->stream, ctx->nsm);
+  cudaError_t e = ctx->step2d_tm ? fw::launch_step2d_tm(p, ctx->stream, ctx->nsm)
+                                 : fw::launch_step2d(p, ctx->stream, ctx->nsm);
   if (e != cudaSuccess) {
     // only a running kernel zeroes the other counter set: after a failed launch both sets are
     // reset so that the next launch cannot find its spin targets already met

@@ -8,6 +8,7 @@ namespace fw {
 
 constexpr int kStep2dMaxTerms = 2 * 65;                 // nops <= 2, M <= 64
 constexpr int kStep2dCStride = 1 + 2 * kStep2dMaxTerms;  // counters per set
+constexpr int kTraceWords = 1024 * 16;                  // watchdog records: 2 x 8 words per CTA
 
 struct Step2DParams {
   int J0, J1;
@@ -22,7 +23,7 @@ struct Step2DParams {
   double* residue;          // nullable, max-accumulated
   const double2* master;    // twiddle master table
   unsigned long long* counters;  // 2 sets x kStep2dCStride, zero-initialised
-  unsigned long long* trace;     // optional phase timestamps (CTAs 0 and 100), see fw_step2d.cu
+  unsigned long long* trace;     // optional watchdog records (mapped host memory), see fw_step2d.cu
   int cset, cstride;
   // seismic update
   int seismic;
@@ -51,6 +52,9 @@ constexpr int kStep2dCG = 4;
 constexpr int kStep2dRing = FW_S2D_RING;  // term slots of the global ring (8 / 12 measured slower)
 static_assert(kStep2dRing >= 3, "the columns publish term t after pass 0 of t + 1: two slots deadlock");
 cudaError_t launch_step2d(const Step2DParams& p, cudaStream_t st, int nsm);
+// the time-multiplexed variant (fw_step2d_tm.cu): same parameters, tables and results
+bool step2d_tm_supported(int J0, int J1, int nsm);
+cudaError_t launch_step2d_tm(const Step2DParams& p, cudaStream_t st, int nsm);
 
 // table relayouts for the persistent kernel
 void launch_w_to_2d(cudaStream_t st, int J0, int J1, int M, const double* w, double* w2d);
