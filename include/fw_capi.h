@@ -17,13 +17,18 @@
  *   fw_apply_device         same, device-resident buffers (no reference equivalent: the GPU-resident form)
  *   fw_apply_batch_device   a batch of independent applies (config 5 sweep; reference runs them serially)
  *   fw_seis_create          derive_medium + SeismicStepper ctor           seismic.cpp:11-44, 85-109
+ *                           (grids: every even J >= 4 up to the device transforms' reach; power-of-two
+ *                           axes take the real-transform pipeline, others the full-spectrum C2C one)
  *   fw_seis_step            SeismicStepper::step / advance               seismic.cpp:111-137
  *   fw_seis_get             SeismicStepper::current / n                  seismic.hpp:44-46
  *   fw_seis_step_io         current() = u; step(); u = current()         seismic.cpp:111-133, seismic.hpp:44
  *   fw_tsfp2_*              Stepper (Method::TSFP2) ctor / step            stepping.cpp:119-138, 266-304
  *   fw_wave_*               Stepper (Method::LFFP / CNFP) ctor / step      stepping.cpp:88-104, 119-138, 170-264
  *                           (the Laplacian seam stepping.hpp:52-60 served by the device apply)
- *   fw_grid_dft             Grid::dft on a real/Hermitian field           grid.cpp:134-137 (canonical FFT, test hook)
+ *   fw_ricker_initial       ricker_initial                               seismic.cpp:70-83
+ *   fw_grid_dft[_device]    Grid::dft (in-place unnormalised C2C)         grid.cpp:134-137, grid.hpp:49-51
+ *   fw_grid_forward/inverse Grid::forward / Grid::inverse                 grid.cpp:171-197
+ *   fw_apply_constant_order apply_constant_order(Field / Spectrum, s)     flap.cpp:137-149
  */
 #ifndef FW_CAPI_H
 #define FW_CAPI_H
@@ -50,7 +55,8 @@ enum fw_status {
   FW_E_DIM_RANGE = 10,      /* fwave::DimOutOfRange */
   FW_E_OOM = 11,            /* device allocation failed */
   FW_E_CUDA = 12,           /* CUDA runtime error / no device */
-  FW_E_UNSUPPORTED = 13,    /* valid for the reference but not for this backend (non-power-of-two axis) */
+  FW_E_UNSUPPORTED = 13,    /* valid for the reference but beyond this backend (axis length past the device
+                               transforms; TSFP2 / LFFP / CNFP and the rfftn hooks on non-power-of-two grids) */
   FW_E_NCCL = 14,           /* collective failure (slab-decomposed grids) */
   FW_E_PICARD_DIVERGED = 15,/* fwave::PicardDiverged */
   FW_E_CG_STAGNATED = 16    /* fwave::CgStagnated */
@@ -80,8 +86,9 @@ long long fw_ctx_launches(fw_ctx ctx);
 int fw_ctx_trace(fw_ctx ctx, unsigned long long* out);
 
 /* ---- operator: ExpansionOperator resident on the device ----
- * grid: dim in {1,2,3}, J[dim] points per axis (even, >= 4; this backend needs
- * powers of two), periodic [lo, hi) per axis, row-major with axis 0 slowest.
+ * grid: dim in {1,2,3}, J[dim] points per axis (even, >= 4: powers of two <= 4096 take the
+ * real-transform pipeline; other lengths <= 2048 the full-spectrum C2C form of flap.cpp:38-92
+ * through Bluestein transforms), periodic [lo, hi) per axis, row-major with axis 0 slowest.
  * order_values: s(x_j), N = prod(J) doubles.  s0_override: NULL -> serial mean
  * (or s exactly when constant), else the given value.  M >= 0 terms. */
 int fw_op_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
@@ -188,6 +195,27 @@ int fw_wave_step(fw_wave w, int nsteps);
 /* cur = u^n, prev = u^{n-1} (host, nullable); n; total Picard iterations (CNFP) */
 int fw_wave_get(fw_wave w, double* cur_host, double* prev_host, long* n, long* picard_total);
 
+/* ---- spectral utilities of the reference's Grid and the constant-order operator ----
+ * Every even axis length the reference Grid accepts up to the device transforms' reach: powers of
+ * two <= 4096 by the canonical Stockham plan, other lengths <= 2048 by Bluestein's chirp-z form
+ * through it (FW_E_UNSUPPORTED beyond).  Spectra are full (N complex, interleaved re, im),
+ * row-major, standard FFT order (grid.hpp:16-19).
+ *   fw_grid_dft            in-place unnormalised C2C of data[2N] (sign -1 = FFTW_FORWARD, +1 = FFTW_BACKWARD)
+ *   fw_grid_forward        spec = DFT(u) / N                                  (Grid::forward)
+ *   fw_grid_inverse        u = Re IDFT(spec), *imag_residue = max |Im|         (Grid::inverse)
+ *   fw_apply_constant_order  u -> (-Delta)^s u = inverse(|mu|^{2s} .* forward(u)); s in (0, 2)
+ *                          else FW_E_ORDER_RANGE (flap.cpp:13-16, 146-149)
+ *   fw_apply_constant_order_spectrum  spec .* |mu|^{2s}                        (flap.cpp:137-145) */
+int fw_grid_dft(fw_ctx ctx, int dim, const int* J, double* data_host, int sign);
+int fw_grid_dft_device(fw_ctx ctx, int dim, const int* J, double* data_dev, int sign);
+int fw_grid_forward(fw_ctx ctx, int dim, const int* J, const double* u_host, double* spec_host);
+int fw_grid_inverse(fw_ctx ctx, int dim, const int* J, const double* spec_host, double* u_host,
+                    double* imag_residue);
+int fw_apply_constant_order(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                            const double* u_host, double s, double* out_host, double* imag_residue);
+int fw_apply_constant_order_spectrum(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                                     const double* spec_host, double s, double* out_host);
+
 /* ---- canonical transforms (test hooks) ----
  * forward: real x[N] -> half spectrum H[N_half] (interleaved re,im), unscaled;
  * backward: H -> real x (unnormalized C2R). */
@@ -228,6 +256,11 @@ int fw_op_device_tables(fw_op op, const double** w_dev, const double** dev1_dev,
  *                           |next| > thr somewhere (the blow-up check of seismic.cpp:124-129) */
 int fw_medium_coefficients(long long n, const double* gamma, const double* c0, double omega0, double* c_out,
                            double* eta_out, double* tau_coef_out);
+/* ricker_initial(nu0, xc, grid) (seismic.cpp:70-83): out[j] = (1 - 2 a r^2) exp(-a r^2), a = pi^2 nu0^2,
+ * r = |x_j - xc| with x_j = Grid::point(j) (grid.cpp:107-116); host, glibc exp as the reference
+ * (bit-identical); grid validation as Grid::Grid (FW_E_ODD_SIZE, FW_E_EMPTY_INTERVAL, FW_E_DIM_RANGE) */
+int fw_ricker_initial(int dim, const int* J, const double* lo, const double* hi, double nu0, const double* xc,
+                      double* out);
 int fw_stage_seis_start(fw_ctx ctx, long long n, double tau, const double* phi, const double* psi, const double* c,
                         const double* eta, const double* tau_coef, const double* l1phi, const double* l2psi,
                         double* cur);

@@ -133,6 +133,16 @@ int ref_forward(int d, const int* J, const double* lo, const double* hi, const d
   });
 }
 
+// ricker_initial (seismic.cpp:70-83)
+int ref_ricker(int d, const int* J, const double* lo, const double* hi, double nu0, const double* xc,
+               double* out) {
+  return guard([&] {
+    Grid g = make_grid(d, J, lo, hi);
+    Field f = ricker_initial(nu0, std::vector<double>(xc, xc + d), g);
+    std::memcpy(out, f.values().data(), g.total() * sizeof(double));
+  });
+}
+
 // derive_medium (seismic.cpp:11-44)
 int ref_medium(int d, const int* J, const double* lo, const double* hi, const double* gamma,
                const double* c0, double omega0, int M, double* c, double* eta, double* tau_coef,

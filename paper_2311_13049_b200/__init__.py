@@ -54,8 +54,13 @@ from .api import (  # noqa: F401
     build_grid,
     build_medium,
     default_context,
+    apply_constant_order,
+    forward,
+    grid_dft,
+    inverse,
     irfftn,
     rfftn,
+    ricker_initial,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

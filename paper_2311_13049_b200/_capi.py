@@ -128,6 +128,13 @@ def load_library():
     lib.fw_op_destroy.restype = None
     lib.fw_op_info.argtypes = [_vp, C.POINTER(OpInfo)]
     lib.fw_op_path.argtypes = [_vp]
+    lib.fw_ricker_initial.argtypes = [C.c_int, _ip, _dp, _dp, C.c_double, _dp, _dp]
+    lib.fw_grid_dft.argtypes = [_vp, C.c_int, _ip, _dp, C.c_int]
+    lib.fw_grid_dft_device.argtypes = [_vp, C.c_int, _ip, _vp, C.c_int]
+    lib.fw_grid_forward.argtypes = [_vp, C.c_int, _ip, _dp, _dp]
+    lib.fw_grid_inverse.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp]
+    lib.fw_apply_constant_order.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp, C.c_double, _dp, _dp]
+    lib.fw_apply_constant_order_spectrum.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp, C.c_double, _dp]
     lib.fw_apply.argtypes = [_vp, _dp, _dp, C.c_int, _dp]
     lib.fw_apply_device.argtypes = [_vp, _vp, _vp, C.c_int, _vp]
     lib.fw_apply_batch_device.argtypes = [C.POINTER(_vp), C.c_int, C.POINTER(_vp), C.POINTER(_vp)]
@@ -177,5 +184,6 @@ EXPORTED_SYMBOLS = [
     "fw_seis_step", "fw_seis_enqueue", "fw_seis_get", "fw_seis_set_current", "fw_seis_step_io",
     "fw_seis_current_device", "fw_seis_ops", "fw_seis_medium", "fw_tsfp2_create",
     "fw_tsfp2_destroy", "fw_tsfp2_step", "fw_tsfp2_get", "fw_wave_create", "fw_wave_destroy", "fw_wave_step",
-    "fw_wave_get", "fw_rfftn", "fw_irfftn",
+    "fw_wave_get", "fw_rfftn", "fw_irfftn", "fw_op_path", "fw_ricker_initial", "fw_grid_dft", "fw_grid_dft_device",
+    "fw_grid_forward", "fw_grid_inverse", "fw_apply_constant_order", "fw_apply_constant_order_spectrum",
 ]

@@ -282,6 +282,18 @@ class SeismicMedium:
             raise GammaOutOfRange(f"gamma = {self.gamma[bad].flat[0]} outside [0, 0.5)")
 
 
+def ricker_initial(nu0: float, xc, grid: Grid) -> np.ndarray:
+    """ricker_initial (seismic.cpp:70-83): (1 - 2 a r^2) exp(-a r^2), a = pi^2 nu0^2, on the
+    reference's grid points (grid.cpp:107-116); bit-identical to the reference (fw_ricker_initial)."""
+    xc = _f64(xc)
+    if xc.size < grid.dim:
+        raise ArgumentError("xc needs one coordinate per grid axis")
+    J, lo, hi = grid._carrays()
+    out = np.empty(grid.shape)
+    check(load_library().fw_ricker_initial(grid.dim, J, lo, hi, float(nu0), _ptr(xc), _ptr(out)))
+    return out
+
+
 def build_medium(grid: Grid, gamma, c0, omega0: float, M: int) -> SeismicMedium:
     return SeismicMedium(grid, gamma, c0, omega0, M)
 
@@ -548,6 +560,66 @@ class Stepper:
                 self._h = None
         except Exception:
             pass
+
+
+def _cplx(a, n: int) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    if a.size != n:
+        raise GridMismatch("spectrum length does not match grid point count")
+    return a
+
+
+def grid_dft(grid: Grid, data, sign: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """Grid::dft (grid.cpp:134-137): unnormalised C2C of a complex array on the grid's shape,
+    sign -1 (FFTW_FORWARD) / +1 (FFTW_BACKWARD); returns the transformed array (the input is
+    not modified)."""
+    ctx = ctx or default_context()
+    x = _cplx(data, grid.total()).reshape(grid.shape).copy()
+    J, _, _ = grid._carrays()
+    check(load_library().fw_grid_dft(ctx.handle, grid.dim, J, x.view(np.float64).ctypes.data_as(_dp), int(sign)))
+    return x
+
+
+def forward(grid: Grid, u, ctx: Optional[Context] = None) -> np.ndarray:
+    """Grid::forward (grid.cpp:171-179): the full spectrum DFT(u) / N."""
+    ctx = ctx or default_context()
+    u = _f64(u, grid.total())
+    spec = np.empty(grid.shape, dtype=np.complex128)
+    J, _, _ = grid._carrays()
+    check(load_library().fw_grid_forward(ctx.handle, grid.dim, J, _ptr(u), spec.view(np.float64).ctypes.data_as(_dp)))
+    return spec
+
+
+def inverse(grid: Grid, spec, residue: bool = False, ctx: Optional[Context] = None):
+    """Grid::inverse (grid.cpp:181-197): Re IDFT(spec) [and max |Im|]."""
+    ctx = ctx or default_context()
+    sp = _cplx(spec, grid.total())
+    out = np.empty(grid.shape)
+    res = C.c_double(0.0)
+    J, _, _ = grid._carrays()
+    check(load_library().fw_grid_inverse(ctx.handle, grid.dim, J, sp.view(np.float64).ctypes.data_as(_dp), _ptr(out),
+                                         C.byref(res)))
+    return (out, res.value) if residue else out
+
+
+def apply_constant_order(grid: Grid, u, s: float, residue: bool = False, ctx: Optional[Context] = None):
+    """apply_constant_order (flap.cpp:137-149): (-Delta)^s of a real field (returns a field) or of a
+    full complex spectrum (returns the spectrum times |mu|^{2s}); s in (0, 2) else OrderOutOfRange."""
+    ctx = ctx or default_context()
+    J, lo, hi = grid._carrays()
+    if np.iscomplexobj(u):
+        sp = _cplx(u, grid.total())
+        out = np.empty(grid.shape, dtype=np.complex128)
+        check(load_library().fw_apply_constant_order_spectrum(ctx.handle, grid.dim, J, lo, hi,
+                                                              sp.view(np.float64).ctypes.data_as(_dp), float(s),
+                                                              out.view(np.float64).ctypes.data_as(_dp)))
+        return out
+    uu = _f64(u, grid.total())
+    out = np.empty(grid.shape)
+    res = C.c_double(0.0)
+    check(load_library().fw_apply_constant_order(ctx.handle, grid.dim, J, lo, hi, _ptr(uu), float(s), _ptr(out),
+                                                 C.byref(res)))
+    return (out, res.value) if residue else out
 
 
 def rfftn(x, ctx: Optional[Context] = None):

@@ -9,8 +9,10 @@
 // (flap.cpp:40-41), exact zeros for the perturbation of a constant order
 // (flap.cpp:163-166), the imaginary residue through the optional pointer.  C-ABI
 // status codes are re-thrown as the matching fwave exception type (errors.hpp).
-// Grids this backend does not support (non-power-of-two axes) raise fwave::Error:
-// there is no silent CPU fallback.
+// Every grid the reference accepts runs on the device (power-of-two axes on the real-transform
+// pipeline, other lengths on the full-spectrum C2C form); lengths past the device transforms'
+// reach raise fwave::Error: there is no silent CPU fallback.  The reference's own FFTW calls
+// (Grid::dft, apply_toeplitz) are served by the device too (fftw_gpu.cpp).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -20,6 +22,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "dropin_ctx.hpp"
 #include "fracwave/errors.hpp"
 #include "fracwave/flap.hpp"
 #include "fw_capi.h"
@@ -48,8 +51,6 @@ void check(int rc) {
   if (rc != FW_OK) rethrow(rc);
 }
 
-std::mutex g_mu;
-fw_ctx g_ctx = nullptr;
 long g_calls = 0;
 
 struct Entry {
@@ -85,10 +86,7 @@ std::uint64_t fingerprint(const ExpansionOperator& op) {
 }
 
 fw_op device_op(const ExpansionOperator& op) {
-  if (!g_ctx) {
-    const char* dev = std::getenv("FW_DEVICE");
-    check(fw_ctx_create(dev ? std::atoi(dev) : 0, &g_ctx));
-  }
+  fw_ctx ctx = gpu_dropin::context();
   const std::uint64_t h = fingerprint(op);
   auto it = g_cache.find(&op);
   if (it != g_cache.end()) {
@@ -110,7 +108,7 @@ fw_op device_op(const ExpansionOperator& op) {
     dv[m] = op.deviation_powers[m].data();
   }
   fw_op d = nullptr;
-  check(fw_op_create_from_tables(g_ctx, g.dim(), J, lo, hi, op.M, op.order.s0(), op.constant_order ? 1 : 0,
+  check(fw_op_create_from_tables(ctx, g.dim(), J, lo, hi, op.M, op.order.s0(), op.constant_order ? 1 : 0,
                                  op.base_symbol.data(), op.M ? lw.data() : nullptr, op.M ? dv.data() : nullptr,
                                  &d));
   g_cache[&op] = Entry{h, d};
@@ -119,7 +117,7 @@ fw_op device_op(const ExpansionOperator& op) {
 
 Field apply_gpu(const ExpansionOperator& op, const Field& u, int m_first, double* imag_residue) {
   if (!u.grid().same_as(op.grid)) throw GridMismatch("field defined on a different grid than the operator");
-  std::lock_guard<std::mutex> lock(g_mu);
+  std::lock_guard<std::mutex> lock(gpu_dropin::mutex());
   fw_op d = device_op(op);
   Field out(op.grid, 0.0);
   check(fw_apply(d, u.values().data(), out.values().data(), m_first, imag_residue));
@@ -135,6 +133,22 @@ struct Report {
 } g_report;
 
 }  // namespace
+
+namespace gpu_dropin {
+std::mutex& mutex() {
+  static std::mutex mu;
+  return mu;
+}
+fw_ctx context() {
+  static fw_ctx ctx = [] {
+    fw_ctx c = nullptr;
+    const char* dev = std::getenv("FW_DEVICE");
+    check(fw_ctx_create(dev ? std::atoi(dev) : 0, &c));
+    return c;
+  }();
+  return ctx;
+}
+}  // namespace gpu_dropin
 
 Field apply_matrix_free(const ExpansionOperator& op, const Field& u, double* imag_residue) {
   return apply_gpu(op, u, 0, imag_residue);

@@ -1,7 +1,11 @@
 // Reference-side check of fwave::gpu::Stepper against the reference's own Stepper
-// (stepping.cpp) on the same WaveProblem: LFFP and TSFP2 bit for bit, CNFP (device
-// CG with tree-order dot products) to relative L2 1e-10 with the same step and
-// Picard counts, and the reference's exceptions (BlowupDetected, PicardDiverged).
+// (stepping.cpp) on the same WaveProblem, both inside the drop-in build: LFFP bit for bit
+// (the same device apply on both sides), TSFP2 to relative L2 1e-12 (the reference's
+// oscillator flows call Grid::dft, which the drop-in serves with the device's full complex
+// DFT, while fw_tsfp2 uses the real transforms), CNFP (device CG with tree-order dot
+// products) to 1e-10, with the same step and Picard counts, and the reference's
+// exceptions (BlowupDetected, PicardDiverged).  Bitwise pins against the reference built
+// on the oracle's canonical FFT: tests/test_gpu_wave.py.
 #include <cmath>
 #include <cstdio>
 
@@ -61,8 +65,8 @@ int main() {
     ref.advance(c.steps);
     dev.advance(c.steps);
     const double e = rel(dev.current(), ref.current());
-    const bool exact = c.m != Method::CNFP;
-    const bool ok = (exact ? e == 0.0 : e <= 1e-10) && dev.n() == ref.n() &&
+    const double tol = c.m == Method::LFFP ? 0.0 : (c.m == Method::TSFP2 ? 1e-12 : 1e-10);
+    const bool ok = e <= tol && dev.n() == ref.n() &&
                     dev.total_picard_iterations() == ref.total_picard_iterations();
     std::printf("method %d f=%s: rel L2 %.3e, n %ld/%ld, picard %ld/%ld %s\n", (int)c.m, c.cubic ? "cubic" : "none",
                 e, dev.n(), ref.n(), dev.total_picard_iterations(), ref.total_picard_iterations(),

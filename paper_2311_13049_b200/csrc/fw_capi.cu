@@ -91,7 +91,8 @@ void twiddle(long t, long n, double* c, double* s) {
 bool is_pow2(long n) { return n >= 1 && (n & (n - 1)) == 0; }
 
 // Grid::Grid validation (grid.cpp:35-58) + this backend's size support
-int check_grid(int dim, const int* J, const double* lo, const double* hi, fw::GridGeom* g) {
+// Grid::Grid validation (grid.cpp:35-58) and the geometry
+int check_grid_ref(int dim, const int* J, const double* lo, const double* hi, fw::GridGeom* g) {
   if (!J) return set_err(FW_E_ARG, "null size array");
   if (dim < 1 || dim > 3) return set_err(FW_E_DIM_RANGE, "dimension must be 1, 2 or 3, got " + std::to_string(dim));
   for (int m = 0; m < dim; ++m) {
@@ -100,10 +101,6 @@ int check_grid(int dim, const int* J, const double* lo, const double* hi, fw::Gr
                                         " must be even and >= 4");
     if (lo && hi && !(hi[m] > lo[m])) return set_err(FW_E_EMPTY_INTERVAL, "axis " + std::to_string(m) + ": empty interval");
   }
-  for (int m = 0; m < dim; ++m)
-    if (!is_pow2(J[m]) || J[m] > 4096)
-      return set_err(FW_E_UNSUPPORTED, "axis " + std::to_string(m) + ": this backend needs a power of two in [4, 4096], got " +
-                                           std::to_string(J[m]));
   g->d = dim;
   g->N = 1;
   for (int m = 0; m < 3; ++m) g->J[m] = m < dim ? J[m] : 1;
@@ -112,6 +109,38 @@ int check_grid(int dim, const int* J, const double* lo, const double* hi, fw::Gr
   g->hp1 = g->nl / 2 + 1;
   g->rows = g->N / (size_t)g->nl;
   g->Nh = g->rows * (size_t)g->hp1;
+  return FW_OK;
+}
+
+// ... plus the device transforms: full = some axis is not a power of two (served by the
+// full-spectrum C2C path, fw_dft.cu); lengths past the device transforms' reach: FW_E_UNSUPPORTED
+int plan_grid(int dim, const int* J, const double* lo, const double* hi, fw::GridGeom* g, bool* full) {
+  FW_TRY(check_grid_ref(dim, J, lo, hi, g));
+  *full = false;
+  for (int m = 0; m < dim; ++m) {
+    if (!fw::dft_length_supported(J[m]))
+      return set_err(FW_E_UNSUPPORTED, "axis " + std::to_string(m) + ": length " + std::to_string(J[m]) +
+                                           " beyond the device transforms (powers of two <= 4096, other even "
+                                           "lengths <= 2048)");
+    if (!is_pow2(J[m])) *full = true;
+  }
+  return FW_OK;
+}
+
+// the table geometry of the full-spectrum path: every bin of the last axis
+fw::GridGeom full_geom(fw::GridGeom g) {
+  g.hp1 = g.nl;
+  g.Nh = g.N;
+  return g;
+}
+
+// ... plus what the canonical real-transform pipeline serves
+int check_grid(int dim, const int* J, const double* lo, const double* hi, fw::GridGeom* g) {
+  FW_TRY(check_grid_ref(dim, J, lo, hi, g));
+  for (int m = 0; m < dim; ++m)
+    if (!is_pow2(J[m]) || J[m] > 4096)
+      return set_err(FW_E_UNSUPPORTED, "axis " + std::to_string(m) + ": this backend needs a power of two in [4, 4096], got " +
+                                           std::to_string(J[m]));
   return FW_OK;
 }
 
@@ -211,11 +240,13 @@ struct fw_ctx_s {
   int dbg = 0;                                // FW_STEP2D_DBG: timing experiments only (wrong results)
   int steps_per_launch = 0;                   // FW_STEPS_PER_LAUNCH: seismic steps per persistent launch (0 = all)
   bool step2d_tm = false;                     // FW_STEP2D_TM=1: time-multiplexed persistent kernel (A/B)
+  int batch_fields = 0;                       // FW_BATCH_FIELDS: fields per batched pipeline (0 = all that fit)
   unsigned long long* counters = nullptr;     // persistent-kernel counters (2 sets)
   unsigned long long* trace = nullptr;        // FW_TRACE=1: persistent-kernel watchdog records (device view)
   unsigned long long* trace_host = nullptr;   //   ... the same buffer, mapped host memory (survives a trap)
   int cset = 0;
   bool generic_lines = false;                 // FW_GENERIC_LINES=1: shared-memory line FFTs only (tests)
+  fw::ChirpCache chirps;                      // Bluestein chirps of the non-power-of-two axes (fw_dft.cu)
   fw::LaunchCtx L() { return fw::LaunchCtx{stream, master, &launches, generic_lines}; }
   int get_scratch(int slot, size_t bytes, void** out) {
     if (scratch_bytes[slot] < bytes) {
@@ -252,6 +283,7 @@ struct fw_op_s {
   double* devt = nullptr;  // persistent 2D kernel: [M][N] deviation powers (s-s0)^m
   size_t bytes = 0;
   bool step2d = false;
+  bool full = false;       // non-power-of-two axes: full-spectrum tables, C2C apply (fw_dft.cu)
 };
 
 extern "C" {
@@ -289,6 +321,8 @@ int fw_ctx_create(int device, fw_ctx* out) {
   c->generic_lines = gl && gl[0] == '1';
   const char* dg = getenv("FW_STEP2D_DBG");
   c->dbg = dg ? atoi(dg) : 0;
+  const char* bf = getenv("FW_BATCH_FIELDS");
+  c->batch_fields = bf ? std::max(0, atoi(bf)) : 0;
   const char* tm = getenv("FW_STEP2D_TM");
   c->step2d_tm = tm && tm[0] == '1';
   const char* spl = getenv("FW_STEPS_PER_LAUNCH");
@@ -320,6 +354,7 @@ void fw_ctx_destroy(fw_ctx c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->scratch)
     if (p) cudaFree(p);
+  c->chirps.release();
   if (c->master) cudaFree(c->master);
   if (c->residue) cudaFree(c->residue);
   if (c->counters) cudaFree(c->counters);
@@ -354,22 +389,24 @@ long long fw_ctx_launches(fw_ctx c) { return c ? c->launches : 0; }
 namespace {
 
 int op_alloc_common(fw_ctx ctx, const fw::GridGeom& g, const double* lo, const double* hi, int M, fw_op* out,
-                    fw_op_s** o) {
+                    fw_op_s** o, bool full = false) {
   if (M < 0) return set_err(FW_E_NEGATIVE_M, "truncation count M must be >= 0");
   fw_op_s* op = new fw_op_s();
   op->ctx = ctx;
   op->g = g;
+  op->full = full;
+  const fw::GridGeom gw = full ? full_geom(g) : g;  // table geometry
   for (int m = 0; m < g.d; ++m) {
     op->lo[m] = lo[m];
     op->hi[m] = hi[m];
   }
   op->M = M;
-  if (dalloc(&op->w, (size_t)(M + 1) * g.Nh) || dalloc(&op->dev1, g.N)) {
+  if (dalloc(&op->w, (size_t)(M + 1) * gw.Nh) || dalloc(&op->dev1, g.N)) {
     fw_op_destroy(op);
     return FW_E_OOM;
   }
-  op->bytes = ((size_t)(M + 1) * g.Nh + g.N) * sizeof(double);
-  if (g.d == 2 && fw::step2d_supported(g.J[0], g.J[1], ctx->nsm) && M <= 64) {
+  op->bytes = ((size_t)(M + 1) * gw.Nh + g.N) * sizeof(double);
+  if (!full && g.d == 2 && fw::step2d_supported(g.J[0], g.J[1], ctx->nsm) && M <= 64) {
     const size_t nw = (size_t)(M + 1) * fw::step2d_col_groups(g.J[1]) * g.J[0] * fw::kStep2dCG;
     if (dalloc(&op->w2d, nw) || dalloc(&op->devt, (size_t)std::max(M, 1) * g.N)) {
       fw_op_destroy(op);
@@ -383,13 +420,14 @@ int op_alloc_common(fw_ctx ctx, const fw::GridGeom& g, const double* lo, const d
   return FW_OK;
 }
 
-int op_create_internal(fw_ctx ctx, const fw::GridGeom& g, const double* lo, const double* hi, const double* s,
-                       const double* s0_override, int M, fw_op* out) {
+int op_create_internal(fw_ctx ctx, const fw::GridGeom& g0, const double* lo, const double* hi, const double* s,
+                       const double* s0_override, int M, fw_op* out, bool full = false) {
   double s0, smin, smax;
   int constant;
-  FW_TRY(order_stats(s, g.N, s0_override, &s0, &smin, &smax, &constant));
+  FW_TRY(order_stats(s, g0.N, s0_override, &s0, &smin, &smax, &constant));
   fw_op_s* op = nullptr;
-  FW_TRY(op_alloc_common(ctx, g, lo, hi, M, out, &op));
+  FW_TRY(op_alloc_common(ctx, g0, lo, hi, M, out, &op, full));
+  const fw::GridGeom g = full ? full_geom(g0) : g0;  // table geometry (N bins when full)
   op->s0 = s0;
   op->smin = smin;
   op->smax = smax;
@@ -491,6 +529,20 @@ int apply_device(fw_op op, const double* u, double* out, int m_first, double* re
     FW_CUDA(cudaMemsetAsync(out, 0, g.N * sizeof(double), ctx->stream));
     return FW_OK;
   }
+  if (op->full) {  // non-power-of-two axes: the C2C form (fw_dft.cu)
+    void *uh = nullptr, *buf = nullptr, *devm = nullptr;
+    FW_TRY(ctx->get_scratch(SLOT_UH, g.N * sizeof(double2), &uh));
+    FW_TRY(ctx->get_scratch(SLOT_T, g.N * sizeof(double2), &buf));
+    FW_TRY(ctx->get_scratch(SLOT_TMP, g.N * sizeof(double), &devm));
+    cudaError_t e = fw::launch_full_forward(L, ctx->chirps, g.d, g.J, (long long)g.N, u, (double2*)uh, true);
+    if (e == cudaSuccess) {
+      fw::FullApplyArgs a{(const double2*)uh, op->w, op->dev1, (double*)devm, (double2*)buf, out, m_first, m_last,
+                          residue, guard};
+      e = fw::launch_full_apply(L, ctx->chirps, g.d, g.J, (long long)g.N, a);
+    }
+    if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("full-spectrum apply: ") + cudaGetErrorString(e));
+    return FW_OK;
+  }
   if (!Uh_pre && !guard && use_persistent(op)) {
     fw_op ops[1] = {op};
     double* outs[1] = {out};
@@ -518,9 +570,10 @@ int fw_op_create(fw_ctx ctx, int dim, const int* J, const double* lo, const doub
                  const double* order_values, const double* s0_override, int M, fw_op* out) {
   if (!ctx || !out || !lo || !hi) return set_err(FW_E_ARG, "null argument");
   fw::GridGeom g;
-  FW_TRY(check_grid(dim, J, lo, hi, &g));
+  bool full = false;
+  FW_TRY(plan_grid(dim, J, lo, hi, &g, &full));
   FW_CUDA(cudaSetDevice(ctx->device));
-  return op_create_internal(ctx, g, lo, hi, order_values, s0_override, M, out);
+  return op_create_internal(ctx, g, lo, hi, order_values, s0_override, M, out, full);
 }
 
 int fw_op_create_from_tables(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi, int M,
@@ -529,11 +582,13 @@ int fw_op_create_from_tables(fw_ctx ctx, int dim, const int* J, const double* lo
                              fw_op* out) {
   if (!ctx || !out || !lo || !hi || !base_symbol) return set_err(FW_E_ARG, "null argument");
   if (M > 0 && (!log_weights || !deviation_powers)) return set_err(FW_E_ARG, "null table rows");
-  fw::GridGeom g;
-  FW_TRY(check_grid(dim, J, lo, hi, &g));
+  fw::GridGeom g0;
+  bool full = false;
+  FW_TRY(plan_grid(dim, J, lo, hi, &g0, &full));
   FW_CUDA(cudaSetDevice(ctx->device));
   fw_op_s* op = nullptr;
-  FW_TRY(op_alloc_common(ctx, g, lo, hi, M, out, &op));
+  FW_TRY(op_alloc_common(ctx, g0, lo, hi, M, out, &op, full));
+  const fw::GridGeom g = full ? full_geom(g0) : g0;  // table geometry
   op->s0 = s0;
   op->constant_order = constant_order ? 1 : 0;
   // gather the Hermitian half of the spectral tables (row r, bin q -> full index r*nl + q)
@@ -651,11 +706,11 @@ int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_
   // one batched pipeline (grid.z = field) when every field shares grid, context and term range and
   // the grid is not served by the persistent single-launch kernel; else one apply per field
   const fw_op o0 = ops[0];
-  bool batch = nfields > 1 && o0->g.d >= 2 && !use_persistent(o0);
+  bool batch = nfields > 1 && o0->g.d >= 2 && !use_persistent(o0) && !o0->full;
   for (int f = 1; f < nfields && batch; ++f) {
     const fw_op o = ops[f];
     batch = o->ctx == o0->ctx && o->g.d == o0->g.d && o->g.N == o0->g.N && o->M == o0->M &&
-            o->constant_order == o0->constant_order && !use_persistent(o);
+            o->constant_order == o0->constant_order && !use_persistent(o) && !o->full;
     for (int a = 0; a < o0->g.d && batch; ++a) batch = o->g.J[a] == o0->g.J[a];
   }
   if (!batch) {
@@ -670,7 +725,8 @@ int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_
   // fields per batched pipeline: the all-terms spectra of a chunk live in scratch (up to 16 GiB of
   // the 180 GB HBM); chunks are balanced (64 fields at M = 16 fit in one chunk; an unbalanced
   // 59 + 5 split under a 2 GiB cap left the GPU idle in the small chunk)
-  const size_t cap = std::max<size_t>(1, std::min<size_t>((size_t)nfields, ((size_t)16 << 30) / per_field));
+  size_t cap = std::max<size_t>(1, std::min<size_t>((size_t)nfields, ((size_t)16 << 30) / per_field));
+  if (ctx->batch_fields > 0) cap = std::min<size_t>(cap, (size_t)ctx->batch_fields);  // FW_BATCH_FIELDS (A/B)
   const size_t nchunk = ((size_t)nfields + cap - 1) / cap;
   const int Fc = (int)(((size_t)nfields + nchunk - 1) / nchunk);
   void *uh = nullptr, *T = nullptr, *tab = nullptr;
@@ -697,6 +753,128 @@ int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_
     fw::launch_inverse_batch(L, g, F, 0, m_last, dt + 2 * Fc, dt + 3 * Fc, dt + 4 * Fc);
   }
   FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+// ---- Grid::dft / forward / inverse and apply_constant_order on the device (fw_dft.cu)
+namespace {
+int plan_dft(fw_ctx ctx, int dim, const int* J, fw::GridGeom* g) {
+  if (!ctx) return set_err(FW_E_ARG, "null ctx");
+  bool full = false;
+  return plan_grid(dim, J, nullptr, nullptr, g, &full);
+}
+}  // namespace
+
+int fw_grid_dft_device(fw_ctx ctx, int dim, const int* J, double* data_dev, int sign) {
+  FW_SETDEV(ctx);
+  fw::GridGeom g;
+  FW_TRY(plan_dft(ctx, dim, J, &g));
+  if (!data_dev || (sign != -1 && sign != 1)) return set_err(FW_E_ARG, "null data or sign not -1 / +1");
+  cudaError_t e = fw::launch_dft(ctx->L(), ctx->chirps, g.d, g.J, sign, (double2*)data_dev);
+  if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("grid dft: ") + cudaGetErrorString(e));
+  return FW_OK;
+}
+
+int fw_grid_dft(fw_ctx ctx, int dim, const int* J, double* data_host, int sign) {
+  FW_SETDEV(ctx);
+  fw::GridGeom g;
+  FW_TRY(plan_dft(ctx, dim, J, &g));
+  if (!data_host) return set_err(FW_E_ARG, "null data");
+  void* d = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_UH, g.N * sizeof(double2), &d));
+  FW_CUDA(cudaMemcpyAsync(d, data_host, g.N * 16, cudaMemcpyHostToDevice, ctx->stream));
+  FW_TRY(fw_grid_dft_device(ctx, dim, J, (double*)d, sign));
+  FW_CUDA(cudaMemcpyAsync(data_host, d, g.N * 16, cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FW_OK;
+}
+
+int fw_grid_forward(fw_ctx ctx, int dim, const int* J, const double* u_host, double* spec_host) {
+  FW_SETDEV(ctx);
+  fw::GridGeom g;
+  FW_TRY(plan_dft(ctx, dim, J, &g));
+  if (!u_host || !spec_host) return set_err(FW_E_ARG, "null argument");
+  void *du = nullptr, *ds = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_U, g.N * 8, &du));
+  FW_TRY(ctx->get_scratch(SLOT_UH, g.N * 16, &ds));
+  FW_CUDA(cudaMemcpyAsync(du, u_host, g.N * 8, cudaMemcpyHostToDevice, ctx->stream));
+  cudaError_t e = fw::launch_full_forward(ctx->L(), ctx->chirps, g.d, g.J, (long long)g.N, (const double*)du,
+                                          (double2*)ds, true);
+  if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("grid forward: ") + cudaGetErrorString(e));
+  FW_CUDA(cudaMemcpyAsync(spec_host, ds, g.N * 16, cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FW_OK;
+}
+
+int fw_grid_inverse(fw_ctx ctx, int dim, const int* J, const double* spec_host, double* u_host,
+                    double* imag_residue) {
+  FW_SETDEV(ctx);
+  fw::GridGeom g;
+  FW_TRY(plan_dft(ctx, dim, J, &g));
+  if (!u_host || !spec_host) return set_err(FW_E_ARG, "null argument");
+  void *du = nullptr, *ds = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_OUT, g.N * 8, &du));
+  FW_TRY(ctx->get_scratch(SLOT_UH, g.N * 16, &ds));
+  FW_CUDA(cudaMemcpyAsync(ds, spec_host, g.N * 16, cudaMemcpyHostToDevice, ctx->stream));
+  FW_CUDA(cudaMemsetAsync(ctx->residue, 0, sizeof(double), ctx->stream));
+  cudaError_t e = fw::launch_dft(ctx->L(), ctx->chirps, g.d, g.J, +1, (double2*)ds);
+  if (e == cudaSuccess) e = fw::launch_real_part(ctx->L(), (long long)g.N, (const double2*)ds, (double*)du, ctx->residue);
+  if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("grid inverse: ") + cudaGetErrorString(e));
+  FW_CUDA(cudaMemcpyAsync(u_host, du, g.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  double res = 0.0;
+  FW_CUDA(cudaMemcpyAsync(&res, ctx->residue, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (imag_residue) *imag_residue = res;
+  return FW_OK;
+}
+
+// flap.cpp:13-16
+static int check_order(double s) {
+  if (!(s > 0.0) || !(s < 2.0)) {
+    char b[96];
+    snprintf(b, sizeof b, "order s = %f outside (0, 2)", s);
+    return set_err(FW_E_ORDER_RANGE, b);
+  }
+  return FW_OK;
+}
+
+int fw_apply_constant_order(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                            const double* u_host, double s, double* out_host, double* imag_residue) {
+  FW_SETDEV(ctx);
+  if (!ctx || !lo || !hi || !u_host || !out_host) return set_err(FW_E_ARG, "null argument");
+  FW_TRY(check_order(s));
+  fw::GridGeom g;
+  bool full = false;
+  FW_TRY(plan_grid(dim, J, lo, hi, &g, &full));
+  // inverse(|mu|^{2s} .* forward(u)) (flap.cpp:146-149) is the m = 0 term of a constant-order
+  // operator: base symbol pow(mu2, s) on the device tables, the same forward / multiply / inverse
+  std::vector<double> sv(g.N, s);
+  fw_op op = nullptr;
+  FW_TRY(op_create_internal(ctx, g, lo, hi, sv.data(), nullptr, 0, &op, full));
+  const int rc = fw_apply(op, u_host, out_host, 0, imag_residue);
+  fw_op_destroy(op);
+  return rc;
+}
+
+int fw_apply_constant_order_spectrum(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                                     const double* spec_host, double s, double* out_host) {
+  FW_SETDEV(ctx);
+  if (!ctx || !lo || !hi || !spec_host || !out_host) return set_err(FW_E_ARG, "null argument");
+  FW_TRY(check_order(s));
+  fw::GridGeom g;
+  bool full = false;
+  FW_TRY(plan_grid(dim, J, lo, hi, &g, &full));
+  std::vector<double> f = half_mu2(full_geom(g), lo, hi);  // every bin (grid.cpp:60-80)
+  for (size_t k = 0; k < f.size(); ++k) f[k] = f[k] > 0.0 ? pow(f[k], s) : 0.0;  // flap.cpp:143-144
+  void *ds = nullptr, *df = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_UH, g.N * 16, &ds));
+  FW_TRY(ctx->get_scratch(SLOT_OUT, g.N * 8, &df));
+  FW_CUDA(cudaMemcpyAsync(ds, spec_host, g.N * 16, cudaMemcpyHostToDevice, ctx->stream));
+  FW_CUDA(cudaMemcpyAsync(df, f.data(), g.N * 8, cudaMemcpyHostToDevice, ctx->stream));
+  cudaError_t e = fw::launch_spectrum_mul(ctx->L(), (long long)g.N, (const double*)df, (double2*)ds);
+  if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("constant-order spectrum: ") + cudaGetErrorString(e));
+  FW_CUDA(cudaMemcpyAsync(out_host, ds, g.N * 16, cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
   return FW_OK;
 }
 
@@ -828,6 +1006,15 @@ int seis_enqueue_step(fw_seis s) {
     s->lvl += 1;
     return FW_OK;
   }
+  if (s->A1->full) {  // non-power-of-two axes: two C2C applies (each with its own forward DFT)
+    FW_TRY(apply_device(s->A1, cur, s->l1, 0, nullptr, nullptr));
+    FW_TRY(apply_device(s->A2, cur, l2, 0, nullptr, s->flag));
+    fw::launch_seis_update(L, g.N, s->tau, cur, s->prev(), s->ap(), s->l1, l2, s->c, s->eta, s->tc, next, s->thr,
+                           (int)(s->n + 1), s->flag);
+    s->n += 1;
+    s->lvl += 1;
+    return FW_OK;
+  }
   void* uh = nullptr;
   FW_TRY(ctx->get_scratch(SLOT_UH2, g.Nh * sizeof(double2), &uh));
   // shared forward transform of cur for both operators
@@ -900,7 +1087,8 @@ int fw_seis_create(fw_ctx ctx, int dim, const int* J, const double* lo, const do
                    double blowup_factor, fw_seis* out) {
   if (!ctx || !out || !lo || !hi || !gamma || !c0 || !phi || !psi) return set_err(FW_E_ARG, "null argument");
   fw::GridGeom g;
-  FW_TRY(check_grid(dim, J, lo, hi, &g));
+  bool full = false;
+  FW_TRY(plan_grid(dim, J, lo, hi, &g, &full));
   FW_CUDA(cudaSetDevice(ctx->device));
   const size_t N = g.N;
   for (size_t j = 0; j < N; ++j)  // seismic.cpp:14-19
@@ -924,8 +1112,8 @@ int fw_seis_create(fw_ctx ctx, int dim, const int* J, const double* lo, const do
   s->ctx = ctx;
   s->g = g;
   s->tau = tau;
-  int rc = op_create_internal(ctx, g, lo, hi, ord1.data(), nullptr, M, &s->A1);
-  if (rc == FW_OK) rc = op_create_internal(ctx, g, lo, hi, ord2.data(), nullptr, M, &s->A2);
+  int rc = op_create_internal(ctx, g, lo, hi, ord1.data(), nullptr, M, &s->A1, full);
+  if (rc == FW_OK) rc = op_create_internal(ctx, g, lo, hi, ord2.data(), nullptr, M, &s->A2, full);
   for (double** p : {&s->c, &s->eta, &s->tc, &s->ubuf[0], &s->ubuf[1], &s->ubuf[2], &s->abuf[0], &s->abuf[1], &s->l1})
     if (rc == FW_OK) rc = dalloc(p, N);
   if (rc == FW_OK) rc = dalloc(&s->flag, 1);
@@ -1505,6 +1693,32 @@ int fw_medium_coefficients(long long n, const double* gamma, const double* c0, d
     c_out[j] = cg * cos(0.5 * M_PI * gj);
     eta_out[j] = -scale * cos(M_PI * gj);
     tau_coef_out[j] = -(scale / cg) * sin(M_PI * gj);
+  }
+  return FW_OK;
+}
+
+int fw_ricker_initial(int dim, const int* J, const double* lo, const double* hi, double nu0, const double* xc,
+                      double* out) {
+  if (!J || !lo || !hi || !xc || !out) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid_ref(dim, J, lo, hi, &g));
+  double h[3] = {0, 0, 0};
+  for (int m = 0; m < dim; ++m) h[m] = (hi[m] - lo[m]) / J[m];  // grid.cpp:56
+  const double a = M_PI * M_PI * nu0 * nu0;                        // seismic.cpp:72
+  for (size_t j = 0; j < g.N; ++j) {
+    size_t rem = j;
+    double x[3] = {0, 0, 0};
+    for (int m = dim - 1; m >= 0; --m) {  // Grid::point (grid.cpp:107-116)
+      const size_t jm = rem % (size_t)J[m];
+      rem /= (size_t)J[m];
+      x[m] = lo[m] + jm * h[m];
+    }
+    double r2 = 0.0;
+    for (int m = 0; m < dim; ++m) {
+      const double d = x[m] - xc[m];
+      r2 += d * d;
+    }
+    out[j] = (1.0 - 2.0 * a * r2) * exp(-a * r2);  // seismic.cpp:80
   }
   return FW_OK;
 }

@@ -6,6 +6,7 @@
 #include <stddef.h>
 
 #include <atomic>
+#include <vector>
 
 namespace fw {
 
@@ -37,6 +38,46 @@ struct LaunchCtx {
   long long* launches = nullptr;    // host-side launch counter
   bool generic_lines = false;       // FW_GENERIC_LINES=1: shared-memory line FFTs only (tests)
 };
+
+// every line of length n (power of two <= 4096) along a strided axis of a complex array, in
+// place: element j of line (o, in) at o n S + j S + in (in < S); canonical plan; x sc if scale
+void launch_c2c_lines(const LaunchCtx& L, int n, long long S, long long outer, int dir, double2* x, double sc,
+                      bool scale);
+
+// ---- general-length complex DFTs (fw_dft.cu): Grid::dft of any supported axis lengths
+constexpr int kMaxBluestein = 2048;  // non-power-of-two axes: chirp-z through a pow2 FFT of <= 4096
+bool dft_length_supported(int n);
+struct ChirpCache {  // per (length, sign): chirp w_j and the transformed filter, device-resident
+  struct Entry {
+    int n = 0, sign = 0, m = 0;
+    double2* w = nullptr;
+    double2* bhat = nullptr;
+  };
+  std::vector<Entry> entries;
+  cudaError_t get(const LaunchCtx& L, int n, int sign, const Entry** out);
+  void release();
+};
+// in place, unnormalised C2C over every axis of x[J0]..[J_{d-1}] (sign -1 forward, +1 backward)
+cudaError_t launch_dft(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, int sign, double2* x);
+// uh = DFT(u) (x 1/N when scale): Grid::forward / flap.cpp:46-50 in the C2C form
+cudaError_t launch_full_forward(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, long long N,
+                                const double* u, double2* uh, bool scale);
+// flap.cpp:52-91 in the C2C form: out = sum_m (s-s0)^m Re IDFT(w_m .* uh), ascending m from 0
+struct FullApplyArgs {
+  const double2* uh;
+  const double* w;     // (M+1) x N weights on the full spectrum
+  const double* dev1;  // s - s0
+  double* devm;        // scratch N: (s-s0)^m by the reference recurrence
+  double2* buf;        // scratch N complex
+  double* out;
+  int m_first, m_last;
+  double* residue;
+  const int* guard;
+};
+cudaError_t launch_full_apply(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, long long N,
+                              const FullApplyArgs& a);
+cudaError_t launch_real_part(const LaunchCtx& L, long long N, const double2* x, double* out, double* residue);
+cudaError_t launch_spectrum_mul(const LaunchCtx& L, long long n, const double* f, double2* x);
 
 // u (N reals) -> Uh (Nh bins), scaled by 1/N (flap.cpp:46-50)
 void launch_forward(const LaunchCtx& L, const GridGeom& g, const double* u, double2* Uh, bool scale);

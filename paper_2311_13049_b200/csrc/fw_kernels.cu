@@ -358,6 +358,25 @@ void c2c_axis(const LaunchCtx& L, const GridGeom& g, int a, int dir, const doubl
 
 }  // namespace
 
+// every line of length n (power of two <= 4096) along a strided axis of a complex array, in place:
+// element j of line (o, in) at o n S + j S + in, in < S (canonical plan; x sc when scale)
+void launch_c2c_lines(const LaunchCtx& L, int n, long long S, long long outer, int dir, double2* x, double sc,
+                      bool scale) {
+  if (!L.generic_lines && launch_lines(L, n, dir, x, x, nullptr, S, outer, S, 0, 0, 0, 1, 1, sc, scale, nullptr))
+    return;
+  const int lpb = std::max(1, std::min(8, 4096 / n));
+  const long long bpo = (S + lpb - 1) / lpb;
+  dim3 grid((unsigned)(outer * bpo), 1);
+  const size_t sm = smem_bytes(n, lpb);
+  if (dir < 0)
+    k_c2c_axis<-1><<<grid, kThreads, sm, L.stream>>>(x, x, nullptr, n, S, S, 0, 0, 0, lpb, sc, scale ? 1 : 0, L.master,
+                                                      nullptr);
+  else
+    k_c2c_axis<+1><<<grid, kThreads, sm, L.stream>>>(x, x, nullptr, n, S, S, 0, 0, 0, lpb, sc, scale ? 1 : 0, L.master,
+                                                      nullptr);
+  count(L);
+}
+
 void init_kernels() {
   const int lim = 227 * 1024;
   cudaFuncSetAttribute(k_r2c_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);

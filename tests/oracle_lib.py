@@ -212,6 +212,7 @@ def reference():
                                C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
     lib.ref_constant_order.argtypes = [C.c_int, _ip, _dp, _dp, _dp, C.c_double, _dp]
     lib.ref_forward.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp]
+    lib.ref_ricker.argtypes = [C.c_int, _ip, _dp, _dp, C.c_double, _dp, _dp]
     lib.ref_medium.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                _dp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     lib.ref_seismic.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
@@ -269,6 +270,15 @@ def ref_forward(J, lo, hi, u):
     _chk(lib, lib.ref_forward(len(J), J, _f64(lo), _f64(hi), _f64(u).ravel(), out),
          lib.ref_last_error)
     return out.view(np.complex128).reshape(tuple(J))
+
+
+def ref_ricker(J, lo, hi, nu0, xc):
+    """ricker_initial (seismic.cpp:70-83) of the reference."""
+    lib = reference()
+    J = _i32(J)
+    out = np.empty(int(np.prod(J)))
+    _chk(lib, lib.ref_ricker(len(J), J, _f64(lo), _f64(hi), float(nu0), _f64(xc), out), lib.ref_last_error)
+    return out.reshape(tuple(J))
 
 
 def ref_medium(J, lo, hi, gamma, c0, omega0, M):

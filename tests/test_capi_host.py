@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 from conftest import ROOT
+import oracle_lib as O
 
 import paper_2311_13049_b200 as fw
 from paper_2311_13049_b200 import _capi, configs
@@ -104,3 +105,21 @@ def test_roofline_byte_model():
     bs = configs.bytes_per_seismic_step(cfg.N, cfg.N_half, cfg.M)
     assert abs(ba / 1e6 - 222.4) < 0.1
     assert abs(bs / 1e6 - 512.0) < 0.1
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference (oracle/_ref) not built")
+@pytest.mark.parametrize("J,lo,hi,nu0,xc", [
+    ((64,), (-8.0,), (8.0,), 2.0, (0.0,)),
+    ((32, 48), (-4.0, -2.0), (4.0, 6.0), 1.5, (0.25, 1.0)),
+    ((16, 16, 8), (-8.0, -8.0, -8.0), (8.0, 8.0, 8.0), 2.0, (0.0, 0.0, 0.0)),
+])
+def test_ricker_initial_bitwise_vs_reference(J, lo, hi, nu0, xc):
+    """fw_ricker_initial (host, glibc exp) reproduces the reference's ricker_initial (seismic.cpp:70-83)
+    bit for bit on the reference's Grid::point coordinates, including non-power-of-two axes."""
+    import paper_2311_13049_b200 as fw
+
+    g = fw.Grid(list(zip(lo, hi)), J)
+    got = fw.ricker_initial(nu0, xc, g)
+    ref = O.ref_ricker(J, lo, hi, nu0, xc)
+    assert np.array_equal(got, ref)
+    assert got.flat[int(np.argmin(np.abs(got - 1.0)))] <= 1.0  # value 1 at the centre (test_seismic.cpp:51-58)

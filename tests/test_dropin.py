@@ -24,6 +24,16 @@ def test_dropin_links_the_b200_library():
     assert "libfw_b200.so" in out and "not found" not in out
 
 
+@needs_build
+def test_dropin_links_no_oracle_code():
+    """The drop-in library carries no CPU FFT: the reference's FFTW calls resolve to the device-backed
+    entry points (cpp/fftw_gpu.cpp), nothing from oracle/ (fwcanon / fwshim) is linked."""
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(BUILD, "libfracwave_b200dropin.so")],
+                         capture_output=True, text=True).stdout
+    assert "fftw_execute_dft" in out and "fftw_plan_dft" in out
+    assert not re.search(r"\b(fwc_|fwshim)", out), [ln for ln in out.splitlines() if "fwc_" in ln or "fwshim" in ln][:5]
+
+
 def _run(cmd, tmp_path):
     env = dict(os.environ, FW_DROPIN_REPORT="1")
     r = subprocess.run(cmd, cwd=tmp_path, capture_output=True, text=True, timeout=900, env=env)
@@ -43,8 +53,10 @@ def test_reference_unit_suites_on_b200(suite, tmp_path):
 
 @pytest.mark.gpu
 @needs_build
-@pytest.mark.parametrize("criterion", [1, 2, 5, 9])
+@pytest.mark.parametrize("criterion", [1, 2, 5, 8, 9])
 def test_reference_acceptance_on_b200(criterion, tmp_path):
+    """The reference's acceptance criteria through the drop-in; 8 includes the two-layer 200^2 seismic
+    runs (acceptance.cpp:406-432): a non-power-of-two grid on the full-spectrum (Bluestein) path."""
     r, n = _run([ACC, "--criterion", str(criterion)], tmp_path)
     assert r.returncode == 0 and "[PASS]" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
     if criterion != 5:  # criterion 5 uses constant orders only: its perturbations are exact host zeros
