@@ -29,6 +29,8 @@
  *   fw_grid_dft[_device]    Grid::dft (in-place unnormalised C2C)         grid.cpp:134-137, grid.hpp:49-51
  *   fw_grid_forward/inverse Grid::forward / Grid::inverse                 grid.cpp:171-197
  *   fw_apply_constant_order apply_constant_order(Field / Spectrum, s)     flap.cpp:137-149
+ *   fw_dense_*              assemble_dense / apply_dense                  flap.cpp:170-243
+ *   fw_apply_toeplitz       apply_toeplitz                               flap.cpp:245-285
  */
 #ifndef FW_CAPI_H
 #define FW_CAPI_H
@@ -59,7 +61,10 @@ enum fw_status {
                                transforms; TSFP2 / LFFP / CNFP and the rfftn hooks on non-power-of-two grids) */
   FW_E_NCCL = 14,           /* collective failure (slab-decomposed grids) */
   FW_E_PICARD_DIVERGED = 15,/* fwave::PicardDiverged */
-  FW_E_CG_STAGNATED = 16    /* fwave::CgStagnated */
+  FW_E_CG_STAGNATED = 16,   /* fwave::CgStagnated */
+  FW_E_MEMORY_BUDGET = 17,  /* fwave::MemoryBudgetExceeded */
+  FW_E_NOT_CONSTANT = 18,   /* fwave::NotConstantOrder */
+  FW_E_DIM_UNSUPPORTED = 19 /* fwave::DimUnsupported */
 };
 
 typedef struct fw_ctx_s* fw_ctx;
@@ -67,6 +72,7 @@ typedef struct fw_op_s* fw_op;
 typedef struct fw_seis_s* fw_seis;
 typedef struct fw_tsfp2_s* fw_tsfp2;
 typedef struct fw_wave_s* fw_wave;
+typedef struct fw_dense_s* fw_dense;
 
 const char* fw_last_error(void);
 int fw_version(void);
@@ -215,6 +221,25 @@ int fw_apply_constant_order(fw_ctx ctx, int dim, const int* J, const double* lo,
                             const double* u_host, double s, double* out_host, double* imag_residue);
 int fw_apply_constant_order_spectrum(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
                                      const double* spec_host, double s, double* out_host);
+
+/* ---- the dense verification operator and the Toeplitz fast path (flap.hpp:43-58) ----
+ *   fw_dense_create   assemble_dense(OrderField(grid, s), memory_budget) (flap.cpp:170-230): row j is
+ *                     the inverse DFT of |mu|^{2 s(x_j)} at the periodic shifts, assembled on the device
+ *                     (batched row DFTs) and kept there; FW_E_MEMORY_BUDGET when N^2 x 8 >= budget
+ *                     (MemoryBudgetExceeded's message), order validation as OrderField
+ *   fw_dense_apply    apply_dense (flap.cpp:233-243): out = A u (one warp per row, tree-ordered sums)
+ *   fw_dense_entries  the N x N row-major entries (DenseOperator::entries)
+ *   fw_apply_toeplitz apply_toeplitz (flap.cpp:245-285): constant order (else FW_E_NOT_CONSTANT),
+ *                     1D (else FW_E_DIM_UNSUPPORTED), circulant embedding at 2J through device DFTs
+ * The reference's tolerances apply (its dense checks are 1e-10 .. 1e-12 relative): the symbol
+ * |mu|^{2s} of the dense rows is evaluated by the device pow. */
+int fw_dense_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                    const double* order_values, unsigned long long memory_budget, fw_dense* out);
+void fw_dense_destroy(fw_dense d);
+int fw_dense_apply(fw_dense d, const double* u_host, double* out_host);
+int fw_dense_entries(fw_dense d, double* entries_host);
+int fw_apply_toeplitz(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                      const double* order_values, const double* u_host, double* out_host);
 
 /* ---- canonical transforms (test hooks) ----
  * forward: real x[N] -> half spectrum H[N_half] (interleaved re,im), unscaled;

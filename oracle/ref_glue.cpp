@@ -133,6 +133,30 @@ int ref_forward(int d, const int* J, const double* lo, const double* hi, const d
   });
 }
 
+// assemble_dense + apply_dense (flap.cpp:170-243): entries (N x N, nullable) and A u
+int ref_dense(int d, const int* J, const double* lo, const double* hi, const double* s, const double* u,
+              double* entries, double* out) {
+  return guard([&] {
+    Grid g = make_grid(d, J, lo, hi);
+    const std::size_t N = g.total();
+    DenseOperator op = assemble_dense(OrderField(g, vec(s, N)));
+    if (entries) std::memcpy(entries, op.entries.data(), N * N * sizeof(double));
+    Field o = apply_dense(op, Field(g, vec(u, N)));
+    std::memcpy(out, o.values().data(), N * sizeof(double));
+  });
+}
+
+// apply_toeplitz (flap.cpp:245-285)
+int ref_toeplitz(int d, const int* J, const double* lo, const double* hi, const double* s, const double* u,
+                 double* out) {
+  return guard([&] {
+    Grid g = make_grid(d, J, lo, hi);
+    const std::size_t N = g.total();
+    Field o = apply_toeplitz(OrderField(g, vec(s, N)), Field(g, vec(u, N)));
+    std::memcpy(out, o.values().data(), N * sizeof(double));
+  });
+}
+
 // ricker_initial (seismic.cpp:70-83)
 int ref_ricker(int d, const int* J, const double* lo, const double* hi, double nu0, const double* xc,
                double* out) {

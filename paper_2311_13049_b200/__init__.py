@@ -25,6 +25,9 @@ from ._capi import (  # noqa: F401
     Error,
     GammaOutOfRange,
     GridMismatch,
+    DimUnsupported,
+    MemoryBudgetExceeded,
+    NotConstantOrder,
     NegativeM,
     OddSize,
     OrderOutOfRange,
@@ -54,7 +57,11 @@ from .api import (  # noqa: F401
     build_grid,
     build_medium,
     default_context,
+    DenseOperator,
     apply_constant_order,
+    apply_dense,
+    apply_toeplitz,
+    assemble_dense,
     forward,
     grid_dft,
     inverse,

@@ -56,6 +56,18 @@ class DimOutOfRange(Error):
     code = 10
 
 
+class MemoryBudgetExceeded(Error):
+    code = 17
+
+
+class NotConstantOrder(Error):
+    code = 18
+
+
+class DimUnsupported(Error):
+    code = 19
+
+
 class OutOfMemory(Error):
     code = 11
 
@@ -83,7 +95,8 @@ class ArgumentError(Error, ValueError):
 _BY_CODE = {c.code: c for c in (ArgumentError, GridMismatch, NegativeM, OrderOutOfRange,
                                  DeviationTooLarge, GammaOutOfRange, BlowupDetected, OddSize,
                                  EmptyInterval, DimOutOfRange, OutOfMemory, CudaError, Unsupported,
-                                 PicardDiverged, CgStagnated)}
+                                 PicardDiverged, CgStagnated, MemoryBudgetExceeded, NotConstantOrder,
+                                 DimUnsupported)}
 
 
 class OpInfo(C.Structure):
@@ -130,6 +143,12 @@ def load_library():
     lib.fw_op_path.argtypes = [_vp]
     lib.fw_ricker_initial.argtypes = [C.c_int, _ip, _dp, _dp, C.c_double, _dp, _dp]
     lib.fw_grid_dft.argtypes = [_vp, C.c_int, _ip, _dp, C.c_int]
+    lib.fw_dense_create.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp, C.c_ulonglong, C.POINTER(_vp)]
+    lib.fw_dense_destroy.argtypes = [_vp]
+    lib.fw_dense_destroy.restype = None
+    lib.fw_dense_apply.argtypes = [_vp, _dp, _dp]
+    lib.fw_dense_entries.argtypes = [_vp, _dp]
+    lib.fw_apply_toeplitz.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp, _dp, _dp]
     lib.fw_grid_dft_device.argtypes = [_vp, C.c_int, _ip, _vp, C.c_int]
     lib.fw_grid_forward.argtypes = [_vp, C.c_int, _ip, _dp, _dp]
     lib.fw_grid_inverse.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp]
@@ -186,4 +205,5 @@ EXPORTED_SYMBOLS = [
     "fw_tsfp2_destroy", "fw_tsfp2_step", "fw_tsfp2_get", "fw_wave_create", "fw_wave_destroy", "fw_wave_step",
     "fw_wave_get", "fw_rfftn", "fw_irfftn", "fw_op_path", "fw_ricker_initial", "fw_grid_dft", "fw_grid_dft_device",
     "fw_grid_forward", "fw_grid_inverse", "fw_apply_constant_order", "fw_apply_constant_order_spectrum",
+    "fw_dense_create", "fw_dense_destroy", "fw_dense_apply", "fw_dense_entries", "fw_apply_toeplitz",
 ]

@@ -622,6 +622,62 @@ def apply_constant_order(grid: Grid, u, s: float, residue: bool = False, ctx: Op
     return (out, res.value) if residue else out
 
 
+DEFAULT_MEMORY_BUDGET = 8 << 30  # kDefaultMemoryBudget (flap.hpp:48)
+
+
+class DenseOperator:
+    """assemble_dense (flap.cpp:170-230): the N x N spatial matrix of (-Delta)^{s(x)}, assembled and
+    kept on the device (fw_dense_*); the reference's verification oracle."""
+
+    def __init__(self, order: OrderField, memory_budget: int = DEFAULT_MEMORY_BUDGET, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.grid, self.order = order.grid, order
+        J, lo, hi = order.grid._carrays()
+        h = C.c_void_p()
+        check(load_library().fw_dense_create(self.ctx.handle, order.grid.dim, J, lo, hi, _ptr(order.values),
+                                             int(memory_budget), C.byref(h)))
+        self._h = h
+
+    @property
+    def entries(self) -> np.ndarray:
+        N = self.grid.total()
+        a = np.empty((N, N))
+        check(load_library().fw_dense_entries(self._h, _ptr(a)))
+        return a
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().fw_dense_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def assemble_dense(order: OrderField, memory_budget: int = DEFAULT_MEMORY_BUDGET,
+                   ctx: Optional[Context] = None) -> DenseOperator:
+    return DenseOperator(order, memory_budget, ctx)
+
+
+def apply_dense(op: DenseOperator, u) -> np.ndarray:
+    """apply_dense (flap.cpp:233-243)."""
+    u = _f64(u, op.grid.total())
+    out = np.empty(op.grid.shape)
+    check(load_library().fw_dense_apply(op._h, _ptr(u), _ptr(out)))
+    return out
+
+
+def apply_toeplitz(order: OrderField, u, ctx: Optional[Context] = None) -> np.ndarray:
+    """apply_toeplitz (flap.cpp:245-285): constant order, 1D; NotConstantOrder / DimUnsupported."""
+    ctx = ctx or default_context()
+    g = order.grid
+    J, lo, hi = g._carrays()
+    uu = _f64(u, g.total())
+    out = np.empty(g.shape)
+    check(load_library().fw_apply_toeplitz(ctx.handle, g.dim, J, lo, hi, _ptr(order.values), _ptr(uu), _ptr(out)))
+    return out
+
+
 def rfftn(x, ctx: Optional[Context] = None):
     """Canonical forward real transform on the device (unscaled half spectrum)."""
     ctx = ctx or default_context()

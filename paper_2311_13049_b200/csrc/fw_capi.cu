@@ -878,6 +878,125 @@ int fw_apply_constant_order_spectrum(fw_ctx ctx, int dim, const int* J, const do
   return FW_OK;
 }
 
+}  // extern "C"
+
+// ---- the dense verification operator (flap.cpp:170-243) and the Toeplitz fast path (flap.cpp:245-285)
+struct fw_dense_s {
+  fw_ctx ctx = nullptr;
+  fw::GridGeom g;
+  double* A = nullptr;  // N x N row-major, device-resident
+};
+
+extern "C" {
+
+int fw_dense_create(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                    const double* order_values, unsigned long long memory_budget, fw_dense* out) {
+  FW_SETDEV(ctx);
+  if (!ctx || !lo || !hi || !order_values || !out) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  bool full = false;
+  FW_TRY(plan_grid(dim, J, lo, hi, &g, &full));
+  double s0, smin, smax;
+  int constant;
+  FW_TRY(order_stats(order_values, g.N, nullptr, &s0, &smin, &smax, &constant));  // the OrderField
+  const unsigned long long required = (unsigned long long)g.N * (unsigned long long)g.N * sizeof(double);
+  if (required >= memory_budget) {  // flap.cpp:174-176 (strict bound) with MemoryBudgetExceeded's message
+    char b[160];
+    snprintf(b, sizeof b, "dense operator needs %llu bytes, budget is %llu", required, memory_budget);
+    return set_err(FW_E_MEMORY_BUDGET, b);
+  }
+  fw_dense d = new fw_dense_s();
+  d->ctx = ctx;
+  d->g = g;
+  std::vector<double> mu2 = half_mu2(full_geom(g), lo, hi);  // every bin (grid.cpp:60-80)
+  const long long rows = std::max<long long>(1, std::min<long long>((long long)g.N, (256ll << 20) / (16ll * (long long)g.N)));
+  double *dmu2 = nullptr, *ds = nullptr;
+  void* G = nullptr;
+  int rc = dalloc(&d->A, g.N * g.N);
+  if (rc == FW_OK) rc = dalloc(&dmu2, g.N);
+  if (rc == FW_OK) rc = dalloc(&ds, g.N);
+  if (rc == FW_OK) rc = ctx->get_scratch(SLOT_T, (size_t)rows * g.N * sizeof(double2), &G);
+  if (rc == FW_OK) {
+    cudaMemcpyAsync(dmu2, mu2.data(), g.N * 8, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(ds, order_values, g.N * 8, cudaMemcpyHostToDevice, ctx->stream);
+    cudaError_t e = fw::launch_dense_assemble(ctx->L(), ctx->chirps, g.d, g.J, (long long)g.N, dmu2, ds, (double2*)G,
+                                              rows, d->A);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = set_err(FW_E_CUDA, std::string("dense assembly: ") + cudaGetErrorString(e));
+  }
+  cudaFree(dmu2);
+  cudaFree(ds);
+  if (rc != FW_OK) {
+    fw_dense_destroy(d);
+    return rc;
+  }
+  *out = d;
+  return FW_OK;
+}
+
+void fw_dense_destroy(fw_dense d) {
+  if (!d) return;
+  if (d->ctx) cudaSetDevice(d->ctx->device);
+  if (d->A) cudaFree(d->A);
+  delete d;
+}
+
+int fw_dense_apply(fw_dense d, const double* u_host, double* out_host) {
+  FW_SETDEV(d ? d->ctx : nullptr);
+  if (!d || !u_host || !out_host) return set_err(FW_E_ARG, "null argument");
+  fw_ctx ctx = d->ctx;
+  void *du = nullptr, *dout = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_U, d->g.N * 8, &du));
+  FW_TRY(ctx->get_scratch(SLOT_OUT, d->g.N * 8, &dout));
+  FW_CUDA(cudaMemcpyAsync(du, u_host, d->g.N * 8, cudaMemcpyHostToDevice, ctx->stream));
+  cudaError_t e = fw::launch_dense_matvec(ctx->L(), (long long)d->g.N, d->A, (const double*)du, (double*)dout);
+  if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("dense apply: ") + cudaGetErrorString(e));
+  FW_CUDA(cudaMemcpyAsync(out_host, dout, d->g.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FW_OK;
+}
+
+int fw_dense_entries(fw_dense d, double* entries_host) {
+  FW_SETDEV(d ? d->ctx : nullptr);
+  if (!d || !entries_host) return set_err(FW_E_ARG, "null argument");
+  FW_CUDA(cudaMemcpyAsync(entries_host, d->A, d->g.N * d->g.N * 8, cudaMemcpyDeviceToHost, d->ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(d->ctx->stream));
+  return FW_OK;
+}
+
+int fw_apply_toeplitz(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
+                      const double* order_values, const double* u_host, double* out_host) {
+  FW_SETDEV(ctx);
+  if (!ctx || !lo || !hi || !order_values || !u_host || !out_host) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  bool full = false;
+  FW_TRY(plan_grid(dim, J, lo, hi, &g, &full));
+  double s0, smin, smax;
+  int constant;
+  FW_TRY(order_stats(order_values, g.N, nullptr, &s0, &smin, &smax, &constant));
+  if (!constant) return set_err(FW_E_NOT_CONSTANT, "toeplitz fast path requires a constant order");  // flap.cpp:247
+  if (dim != 1) return set_err(FW_E_DIM_UNSUPPORTED, "toeplitz fast path is one-dimensional");       // flap.cpp:249
+  const int n = 2 * J[0];
+  if (!fw::dft_length_supported(n)) return set_err(FW_E_UNSUPPORTED, "circulant embedding length beyond the device DFT");
+  std::vector<double> mu2 = half_mu2(full_geom(g), lo, hi);
+  std::vector<double2> t(J[0]);
+  for (int k = 0; k < J[0]; ++k) t[k] = make_double2(mu2[k] > 0.0 ? pow(mu2[k], s0) : 0.0, 0.0);  // flap.cpp:257-258
+  void *dt = nullptr, *dc = nullptr, *dx = nullptr, *du = nullptr, *dout = nullptr;
+  FW_TRY(ctx->get_scratch(SLOT_UH, (size_t)J[0] * sizeof(double2), &dt));
+  FW_TRY(ctx->get_scratch(SLOT_T, (size_t)n * sizeof(double2), &dc));
+  FW_TRY(ctx->get_scratch(SLOT_TMP, (size_t)n * sizeof(double2), &dx));
+  FW_TRY(ctx->get_scratch(SLOT_U, g.N * 8, &du));
+  FW_TRY(ctx->get_scratch(SLOT_OUT, g.N * 8, &dout));
+  FW_CUDA(cudaMemcpyAsync(dt, t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  FW_CUDA(cudaMemcpyAsync(du, u_host, g.N * 8, cudaMemcpyHostToDevice, ctx->stream));
+  cudaError_t e = fw::launch_toeplitz(ctx->L(), ctx->chirps, J[0], (double2*)dt, (const double*)du, (double2*)dc,
+                                      (double2*)dx, (double*)dout);
+  if (e != cudaSuccess) return set_err(FW_E_CUDA, std::string("toeplitz: ") + cudaGetErrorString(e));
+  FW_CUDA(cudaMemcpyAsync(out_host, dout, g.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  FW_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FW_OK;
+}
+
 int fw_rfftn(fw_ctx ctx, int dim, const int* J, const double* x_host, double* H_host) {
   FW_SETDEV(ctx);
   if (!ctx || !x_host || !H_host) return set_err(FW_E_ARG, "null argument");

@@ -138,6 +138,76 @@ __global__ void k_spectrum_mul(long long n, const double* __restrict__ f, double
   }
 }
 
+// ---- dense operator (flap.cpp:170-243) and the Toeplitz fast path (flap.cpp:245-285)
+// G[b][k] = |mu_k|^{2 s_j} (row j = j0 + b; 0 at k = 0)
+__global__ void k_dense_symbol(long long N, int B, long long j0, const double* __restrict__ mu2,
+                               const double* __restrict__ s, double2* __restrict__ G) {
+  const long long tot = (long long)B * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / N, k = e - b * N;
+    const double m2 = mu2[k];
+    G[e] = make_double2(m2 > 0.0 ? pow(m2, s[j0 + b]) : 0.0, 0.0);
+  }
+}
+// entries[j][l] = Re G_j[(j - l) mod J per axis] / N (flap.cpp:203-225)
+__global__ void k_dense_gather(long long N, int B, long long j0, int d, int J0, int J1, int J2,
+                               const double2* __restrict__ G, double* __restrict__ A) {
+  const int J[3] = {J0, J1, J2};
+  const long long tot = (long long)B * N;
+  const double inv = 1.0 / (double)N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / N, l = e - b * N, j = j0 + b;
+    int jm[3] = {0, 0, 0}, lm[3] = {0, 0, 0};
+    long long rj = j, rl = l;
+    for (int m = d - 1; m >= 0; --m) {
+      jm[m] = (int)(rj % J[m]);
+      rj /= J[m];
+      lm[m] = (int)(rl % J[m]);
+      rl /= J[m];
+    }
+    long long shift = 0;
+    for (int m = 0; m < d; ++m) shift = shift * J[m] + (jm[m] - lm[m] + J[m]) % J[m];
+    A[j * N + l] = G[b * N + shift].x * inv;
+  }
+}
+// out[j] = sum_l A[j][l] u[l]: one warp per row (flap.cpp:233-241; tree-ordered sum)
+__global__ void k_dense_matvec(long long N, const double* __restrict__ A, const double* __restrict__ u,
+                               double* __restrict__ out) {
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  for (long long j = blockIdx.x * (long long)(blockDim.x / 32) + threadIdx.x / 32; j < N; j += warps) {
+    const double* row = A + j * N;
+    double acc = 0.0;
+    for (long long l = threadIdx.x & 31; l < N; l += 32) acc += row[l] * u[l];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) out[j] = acc;
+  }
+}
+// circulant embedding at 2J of the symmetric Toeplitz column t/J; x = u zero-padded
+__global__ void k_toeplitz_embed(int J, const double2* __restrict__ t, const double* __restrict__ u,
+                                 double2* __restrict__ c, double2* __restrict__ x) {
+  const int n = 2 * J;
+  const double inv = 1.0 / (double)J;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double cv = 0.0;
+    if (i < J)
+      cv = t[i].x * inv;
+    else if (i > J)
+      cv = t[n - i].x * inv;
+    c[i] = make_double2(cv, 0.0);
+    x[i] = make_double2(i < J ? u[i] : 0.0, 0.0);
+  }
+}
+__global__ void k_cmul_inplace(int n, double2* __restrict__ x, const double2* __restrict__ c) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double2 a = x[i], b = c[i];  // std::complex<double> *= (flap.cpp:275)
+    x[i] = make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  }
+}
+__global__ void k_real_scale(int J, const double2* __restrict__ x, double* __restrict__ out, double scale) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < J; i += gridDim.x * blockDim.x) out[i] = x[i].x * scale;
+}
+
 int egrid(long long N) { return (int)std::min<long long>((N + kDftThreads - 1) / kDftThreads, 148 * 16); }
 
 bool is_pow2(int n) { return n >= 1 && (n & (n - 1)) == 0; }
@@ -189,10 +259,15 @@ cudaError_t ChirpCache::get(const LaunchCtx& L, int n, int sign, const Entry** o
 }
 
 cudaError_t launch_dft(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, int sign, double2* x) {
+  return launch_dft_batched(L, chirps, d, J, 1, sign, x);
+}
+
+cudaError_t launch_dft_batched(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, long long batch, int sign,
+                               double2* x) {
   long long S = 1;
   for (int a = d - 1; a >= 0; --a) {
     const int n = J[a];
-    long long outer = 1;
+    long long outer = batch;
     for (int b = 0; b < a; ++b) outer *= J[b];
     if (is_pow2(n)) {
       launch_c2c_lines(L, n, S, outer, sign < 0 ? -1 : +1, x, 1.0, false);
@@ -240,6 +315,44 @@ cudaError_t launch_full_apply(const LaunchCtx& L, ChirpCache& chirps, int d, con
 cudaError_t launch_real_part(const LaunchCtx& L, long long N, const double2* x, double* out, double* residue) {
   k_real_part<<<egrid(N), kDftThreads, 0, L.stream>>>(N, x, out, residue);
   if (L.launches) *L.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_assemble(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, long long N,
+                                  const double* mu2, const double* s, double2* G, long long rows_per_batch,
+                                  double* A) {
+  for (long long j0 = 0; j0 < N; j0 += rows_per_batch) {
+    const int B = (int)std::min<long long>(rows_per_batch, N - j0);
+    k_dense_symbol<<<egrid((long long)B * N), kDftThreads, 0, L.stream>>>(N, B, j0, mu2, s, G);
+    cudaError_t e = launch_dft_batched(L, chirps, d, J, B, +1, G);
+    if (e != cudaSuccess) return e;
+    k_dense_gather<<<egrid((long long)B * N), kDftThreads, 0, L.stream>>>(N, B, j0, d, J[0], d > 1 ? J[1] : 1,
+                                                                           d > 2 ? J[2] : 1, G, A);
+    if (L.launches) *L.launches += 2;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_matvec(const LaunchCtx& L, long long N, const double* A, const double* u, double* out) {
+  const int wpb = kDftThreads / 32;
+  k_dense_matvec<<<(unsigned)std::min<long long>((N + wpb - 1) / wpb, 148 * 32), kDftThreads, 0, L.stream>>>(N, A, u,
+                                                                                                            out);
+  if (L.launches) *L.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_toeplitz(const LaunchCtx& L, ChirpCache& chirps, int J, double2* t, const double* u, double2* c,
+                            double2* x, double* out) {
+  const int n = 2 * J;
+  cudaError_t e = launch_dft(L, chirps, 1, &J, +1, t);  // first column, flap.cpp:259-263
+  if (e != cudaSuccess) return e;
+  k_toeplitz_embed<<<egrid(n), kDftThreads, 0, L.stream>>>(J, t, u, c, x);
+  if ((e = launch_dft(L, chirps, 1, &n, -1, c)) != cudaSuccess) return e;
+  if ((e = launch_dft(L, chirps, 1, &n, -1, x)) != cudaSuccess) return e;
+  k_cmul_inplace<<<egrid(n), kDftThreads, 0, L.stream>>>(n, x, c);
+  if ((e = launch_dft(L, chirps, 1, &n, +1, x)) != cudaSuccess) return e;
+  k_real_scale<<<egrid(J), kDftThreads, 0, L.stream>>>(J, x, out, 1.0 / n);
+  if (L.launches) *L.launches += 4;
   return cudaGetLastError();
 }
 

@@ -77,6 +77,17 @@ struct FullApplyArgs {
 cudaError_t launch_full_apply(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, long long N,
                               const FullApplyArgs& a);
 cudaError_t launch_real_part(const LaunchCtx& L, long long N, const double2* x, double* out, double* residue);
+// the same over `batch` consecutive arrays (an extra outermost axis that is not transformed)
+cudaError_t launch_dft_batched(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, long long batch, int sign,
+                               double2* x);
+// dense operator entries A[N][N] (flap.cpp:170-230), rows in batches through scratch G (rows x N complex)
+cudaError_t launch_dense_assemble(const LaunchCtx& L, ChirpCache& chirps, int d, const int* J, long long N,
+                                  const double* mu2, const double* s, double2* G, long long rows_per_batch,
+                                  double* A);
+cudaError_t launch_dense_matvec(const LaunchCtx& L, long long N, const double* A, const double* u, double* out);
+// apply_toeplitz (flap.cpp:245-285): t (J complex, in: |mu|^{2s}, overwritten), c / x scratch 2J complex
+cudaError_t launch_toeplitz(const LaunchCtx& L, ChirpCache& chirps, int J, double2* t, const double* u, double2* c,
+                            double2* x, double* out);
 cudaError_t launch_spectrum_mul(const LaunchCtx& L, long long n, const double* f, double2* x);
 
 // u (N reals) -> Uh (Nh bins), scaled by 1/N (flap.cpp:46-50)

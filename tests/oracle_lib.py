@@ -213,6 +213,8 @@ def reference():
     lib.ref_constant_order.argtypes = [C.c_int, _ip, _dp, _dp, _dp, C.c_double, _dp]
     lib.ref_forward.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp]
     lib.ref_ricker.argtypes = [C.c_int, _ip, _dp, _dp, C.c_double, _dp, _dp]
+    lib.ref_dense.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_void_p, C.c_void_p]
+    lib.ref_toeplitz.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, _dp]
     lib.ref_medium.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                _dp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     lib.ref_seismic.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
@@ -270,6 +272,27 @@ def ref_forward(J, lo, hi, u):
     _chk(lib, lib.ref_forward(len(J), J, _f64(lo), _f64(hi), _f64(u).ravel(), out),
          lib.ref_last_error)
     return out.view(np.complex128).reshape(tuple(J))
+
+
+def ref_dense(J, lo, hi, s, u, entries=False):
+    """assemble_dense + apply_dense of the reference: (A u[, entries])."""
+    lib = reference()
+    J = _i32(J)
+    N = int(np.prod(J))
+    out = np.empty(N)
+    ent = np.empty(N * N) if entries else None
+    _chk(lib, lib.ref_dense(len(J), J, _f64(lo), _f64(hi), _f64(s).ravel(), _f64(u).ravel(),
+                            ent.ctypes.data_as(_dp) if entries else None, out.ctypes.data_as(_dp)), lib.ref_last_error)
+    return (out.reshape(tuple(J)), ent.reshape(N, N)) if entries else out.reshape(tuple(J))
+
+
+def ref_toeplitz(J, lo, hi, s, u):
+    lib = reference()
+    J = _i32(J)
+    out = np.empty(int(np.prod(J)))
+    _chk(lib, lib.ref_toeplitz(len(J), J, _f64(lo), _f64(hi), _f64(s).ravel(), _f64(u).ravel(), out),
+         lib.ref_last_error)
+    return out.reshape(tuple(J))
 
 
 def ref_ricker(J, lo, hi, nu0, xc):

@@ -137,3 +137,71 @@ def test_unsupported_lengths_raise():
     g = m.Grid([(0.0, 1.0)], (2050,))  # neither a power of two nor within the chirp-z reach
     with pytest.raises(m.Unsupported):
         m.build_expansion(m.OrderField(g, np.full(2050, 1.2)), 4)
+
+
+# ---------------------------------------------------------------- dense / Toeplitz (flap.cpp:170-285)
+
+def _s1(J, lo, hi):
+    X = np.meshgrid(*[lo[a] + (hi[a] - lo[a]) * np.arange(J[a]) / J[a] for a in range(len(J))], indexing="ij")
+    return 1.0 + 0.3 * np.sin(np.pi * X[0] / 8)
+
+
+@pytest.mark.parametrize("J", [(32,), (30,), (16, 12), (8, 6, 4)])
+def test_dense_entries_and_apply_vs_reference(J):
+    m = fw()
+    lo, hi = [-8.0] * len(J), [8.0] * len(J)
+    g = m.Grid(list(zip(lo, hi)), J)
+    s = _s1(J, lo, hi)
+    u = np.random.default_rng(3).standard_normal(J)
+    op = m.assemble_dense(m.OrderField(g, s))
+    ref_out, ref_ent = O.ref_dense(J, lo, hi, s, u, entries=True)
+    assert rel(op.entries, ref_ent) <= 1e-12
+    assert rel(m.apply_dense(op, u), ref_out) <= 1e-12
+
+
+def test_dense_known_answers_and_budget():
+    """test_flap.cpp:71-111 on the device: [0, 2pi), J = 4, s = 1 gives a_jj = 1.5; a constant order
+    gives a symmetric Toeplitz matrix; the memory budget is a strict bound with the reference's message."""
+    m = fw()
+    g = m.Grid([(0.0, 2 * np.pi)], (4,))
+    a = m.assemble_dense(m.OrderField(g, np.ones(4))).entries
+    assert np.allclose(np.diag(a), 1.5, rtol=1e-12, atol=0)
+    g2 = m.Grid([(-8.0, 8.0)], (32,))
+    a2 = m.assemble_dense(m.OrderField(g2, np.full(32, 0.7))).entries
+    assert np.abs(a2 - a2.T).max() < 1e-12 and np.abs(a2[1:, 1:] - a2[:-1, :-1]).max() < 1e-12
+    g3 = m.Grid([(0.0, 1.0), (0.0, 1.0)], (256, 256))
+    with pytest.raises(m.MemoryBudgetExceeded, match="needs 34359738368 bytes, budget is 34359738368"):
+        m.assemble_dense(m.OrderField(g3, np.ones((256, 256))), 32 << 30)
+
+
+def test_dense_vs_matrix_free_s1_profile():
+    """test_flap.cpp:179-186: the matrix-free operator (J = 256 on [-32, 32), M = 15, s1 profile) against
+    the dense oracle."""
+    m = fw()
+    J, lo, hi = (256,), (-32.0,), (32.0,)
+    g = m.Grid(list(zip(lo, hi)), J)
+    s = _s1(J, lo, hi)
+    u = np.random.default_rng(9).standard_normal(J)
+    dense = m.apply_dense(m.assemble_dense(m.OrderField(g, s)), u)
+    mf = m.apply_matrix_free(m.build_expansion(m.OrderField(g, s), 15), u)
+    assert np.abs(mf - dense).max() / np.abs(dense).max() < 1e-10
+
+
+@pytest.mark.parametrize("J", [(128,), (100,)])
+def test_toeplitz_fast_path(J):
+    """test_flap.cpp:114-129: against the dense operator and the reference; exact zeros; the errors."""
+    m = fw()
+    lo, hi = (-8.0,), (8.0,)
+    g = m.Grid(list(zip(lo, hi)), J)
+    u = np.random.default_rng(5).standard_normal(J)
+    of = m.OrderField(g, np.full(J, 0.5))
+    fast = m.apply_toeplitz(of, u)
+    slow = m.apply_dense(m.assemble_dense(of), u)
+    assert np.abs(fast - slow).max() / np.abs(slow).max() < 1e-10
+    assert rel(fast, O.ref_toeplitz(J, lo, hi, np.full(J, 0.5), u)) <= 1e-12
+    assert np.all(m.apply_toeplitz(of, np.zeros(J)) == 0.0)
+    with pytest.raises(m.NotConstantOrder):
+        m.apply_toeplitz(m.OrderField(g, _s1(J, lo, hi)), u)
+    g2 = m.Grid([(0.0, 1.0), (0.0, 1.0)], (8, 8))
+    with pytest.raises(m.DimUnsupported):
+        m.apply_toeplitz(m.OrderField(g2, np.full((8, 8), 0.5)), np.zeros((8, 8)))
