@@ -64,7 +64,8 @@ enum fw_status {
   FW_E_CG_STAGNATED = 16,   /* fwave::CgStagnated */
   FW_E_MEMORY_BUDGET = 17,  /* fwave::MemoryBudgetExceeded */
   FW_E_NOT_CONSTANT = 18,   /* fwave::NotConstantOrder */
-  FW_E_DIM_UNSUPPORTED = 19 /* fwave::DimUnsupported */
+  FW_E_DIM_UNSUPPORTED = 19,/* fwave::DimUnsupported */
+  FW_E_NONPOSITIVE_FREQ = 20/* fwave::NonpositiveFrequency */
 };
 
 typedef struct fw_ctx_s* fw_ctx;
@@ -240,6 +241,10 @@ int fw_dense_apply(fw_dense d, const double* u_host, double* out_host);
 int fw_dense_entries(fw_dense d, double* entries_host);
 int fw_apply_toeplitz(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi,
                       const double* order_values, const double* u_host, double* out_host);
+/* truncation_indicator(M, |mu|, s0) (flap.cpp:287-294): |mu|^{2 s0} (2 ln|mu|)^M / M!, the magnitude of
+ * the first dropped expansion term (host, the reference's operation order); FW_E_NONPOSITIVE_FREQ
+ * unless |mu| > 0 */
+int fw_truncation_indicator(int M, double mu_abs, double s0, double* out);
 
 /* ---- canonical transforms (test hooks) ----
  * forward: real x[N] -> half spectrum H[N_half] (interleaved re,im), unscaled;

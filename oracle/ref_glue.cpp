@@ -157,6 +157,11 @@ int ref_toeplitz(int d, const int* J, const double* lo, const double* hi, const 
   });
 }
 
+// truncation_indicator (flap.cpp:287-294)
+int ref_truncation_indicator(int M, double mu_abs, double s0, double* out) {
+  return guard([&] { *out = truncation_indicator(M, mu_abs, s0); });
+}
+
 // ricker_initial (seismic.cpp:70-83)
 int ref_ricker(int d, const int* J, const double* lo, const double* hi, double nu0, const double* xc,
                double* out) {

@@ -28,6 +28,7 @@ from ._capi import (  # noqa: F401
     DimUnsupported,
     MemoryBudgetExceeded,
     NotConstantOrder,
+    NonpositiveFrequency,
     NegativeM,
     OddSize,
     OrderOutOfRange,
@@ -68,6 +69,7 @@ from .api import (  # noqa: F401
     irfftn,
     rfftn,
     ricker_initial,
+    truncation_indicator,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

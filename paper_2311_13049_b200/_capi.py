@@ -68,6 +68,10 @@ class DimUnsupported(Error):
     code = 19
 
 
+class NonpositiveFrequency(Error):
+    code = 20
+
+
 class OutOfMemory(Error):
     code = 11
 
@@ -96,7 +100,7 @@ _BY_CODE = {c.code: c for c in (ArgumentError, GridMismatch, NegativeM, OrderOut
                                  DeviationTooLarge, GammaOutOfRange, BlowupDetected, OddSize,
                                  EmptyInterval, DimOutOfRange, OutOfMemory, CudaError, Unsupported,
                                  PicardDiverged, CgStagnated, MemoryBudgetExceeded, NotConstantOrder,
-                                 DimUnsupported)}
+                                 DimUnsupported, NonpositiveFrequency)}
 
 
 class OpInfo(C.Structure):
@@ -149,6 +153,7 @@ def load_library():
     lib.fw_dense_apply.argtypes = [_vp, _dp, _dp]
     lib.fw_dense_entries.argtypes = [_vp, _dp]
     lib.fw_apply_toeplitz.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp, _dp, _dp]
+    lib.fw_truncation_indicator.argtypes = [C.c_int, C.c_double, C.c_double, _dp]
     lib.fw_grid_dft_device.argtypes = [_vp, C.c_int, _ip, _vp, C.c_int]
     lib.fw_grid_forward.argtypes = [_vp, C.c_int, _ip, _dp, _dp]
     lib.fw_grid_inverse.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp]
@@ -206,4 +211,5 @@ EXPORTED_SYMBOLS = [
     "fw_wave_get", "fw_rfftn", "fw_irfftn", "fw_op_path", "fw_ricker_initial", "fw_grid_dft", "fw_grid_dft_device",
     "fw_grid_forward", "fw_grid_inverse", "fw_apply_constant_order", "fw_apply_constant_order_spectrum",
     "fw_dense_create", "fw_dense_destroy", "fw_dense_apply", "fw_dense_entries", "fw_apply_toeplitz",
+    "fw_truncation_indicator",
 ]

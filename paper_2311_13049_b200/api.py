@@ -678,6 +678,13 @@ def apply_toeplitz(order: OrderField, u, ctx: Optional[Context] = None) -> np.nd
     return out
 
 
+def truncation_indicator(M: int, mu_abs: float, s0: float) -> float:
+    """truncation_indicator (flap.cpp:287-294); NonpositiveFrequency unless |mu| > 0."""
+    out = C.c_double(0.0)
+    check(load_library().fw_truncation_indicator(int(M), float(mu_abs), float(s0), C.byref(out)))
+    return out.value
+
+
 def rfftn(x, ctx: Optional[Context] = None):
     """Canonical forward real transform on the device (unscaled half spectrum)."""
     ctx = ctx or default_context()

@@ -997,6 +997,16 @@ int fw_apply_toeplitz(fw_ctx ctx, int dim, const int* J, const double* lo, const
   return FW_OK;
 }
 
+int fw_truncation_indicator(int M, double mu_abs, double s0, double* out) {
+  if (!out) return set_err(FW_E_ARG, "null argument");
+  if (!(mu_abs > 0.0)) return set_err(FW_E_NONPOSITIVE_FREQ, "truncation indicator requires |mu| > 0");
+  const double l = 2.0 * log(mu_abs);
+  double term = pow(mu_abs, 2.0 * s0);
+  for (int m = 1; m <= M; ++m) term *= l / m;
+  *out = term;
+  return FW_OK;
+}
+
 int fw_rfftn(fw_ctx ctx, int dim, const int* J, const double* x_host, double* H_host) {
   FW_SETDEV(ctx);
   if (!ctx || !x_host || !H_host) return set_err(FW_E_ARG, "null argument");

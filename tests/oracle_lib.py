@@ -213,6 +213,7 @@ def reference():
     lib.ref_constant_order.argtypes = [C.c_int, _ip, _dp, _dp, _dp, C.c_double, _dp]
     lib.ref_forward.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp]
     lib.ref_ricker.argtypes = [C.c_int, _ip, _dp, _dp, C.c_double, _dp, _dp]
+    lib.ref_truncation_indicator.argtypes = [C.c_int, C.c_double, C.c_double, C.POINTER(C.c_double)]
     lib.ref_dense.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_void_p, C.c_void_p]
     lib.ref_toeplitz.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, _dp]
     lib.ref_medium.argtypes = [C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
@@ -272,6 +273,13 @@ def ref_forward(J, lo, hi, u):
     _chk(lib, lib.ref_forward(len(J), J, _f64(lo), _f64(hi), _f64(u).ravel(), out),
          lib.ref_last_error)
     return out.view(np.complex128).reshape(tuple(J))
+
+
+def ref_truncation_indicator(M, mu_abs, s0):
+    lib = reference()
+    out = C.c_double()
+    _chk(lib, lib.ref_truncation_indicator(int(M), float(mu_abs), float(s0), C.byref(out)), lib.ref_last_error)
+    return out.value
 
 
 def ref_dense(J, lo, hi, s, u, entries=False):

@@ -123,3 +123,14 @@ def test_ricker_initial_bitwise_vs_reference(J, lo, hi, nu0, xc):
     ref = O.ref_ricker(J, lo, hi, nu0, xc)
     assert np.array_equal(got, ref)
     assert got.flat[int(np.argmin(np.abs(got - 1.0)))] <= 1.0  # value 1 at the centre (test_seismic.cpp:51-58)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference (oracle/_ref) not built")
+def test_truncation_indicator_vs_reference():
+    """truncation_indicator (flap.cpp:287-294) bit for bit, and NonpositiveFrequency for |mu| <= 0."""
+    import paper_2311_13049_b200 as fw
+
+    for M, mu, s0 in [(0, 3.0, 1.2), (8, 17.5, 1.01), (16, 100.0, 0.55), (32, 0.3, 1.4)]:
+        assert fw.truncation_indicator(M, mu, s0) == O.ref_truncation_indicator(M, mu, s0)
+    with pytest.raises(fw.NonpositiveFrequency):
+        fw.truncation_indicator(4, 0.0, 1.0)
