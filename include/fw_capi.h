@@ -277,6 +277,23 @@ int fw_stage_c2c(fw_ctx ctx, int dim, const int* J, int axis, int dir, const dou
 int fw_stage_c2r_accum(fw_ctx ctx, int dim, const int* J, const double* src_dev, long long src_ts, int m_first,
                        int m_last, const double* dev1_dev, double* out_dev, double* residue_dev);
 int fw_op_device_tables(fw_op op, const double** w_dev, const double** dev1_dev, int* m_last);
+/* one rank's operator tables of a slab-decomposed 3D grid J (axis 0 split over P ranks):
+ * w [M+1][J0][J1/P][J2/2+1] on the rank's spectral columns, s - s0 [J0/P][J1][J2] on its planes;
+ * s0 and the OrderField checks from the GLOBAL order values (N doubles), so the tables equal the
+ * single-device operator's slices bit for bit.  Resident table bytes fall as 1/P (fw_op_info).
+ * The op serves the stage entry points only (fw_apply on it: FW_E_ARG). */
+int fw_op_create_slab(fw_ctx ctx, const int* J, const double* lo, const double* hi, const double* order_values,
+                      const double* s0_override, int M, int P, int rank, fw_op* out);
+/* the slab stepper's update (seismic.cpp:116-129) on a rank's planes with the state levels kept:
+ * next and l2out (the new L2prev = l2) are written unless *flag_dev already holds a step (a blow-up
+ * on some rank in an earlier step: every later update is frozen so the levels before the offending
+ * step survive); a blow-up mins `step` into *flag_dev and into every peer's flag (npeers <= 8 device
+ * addresses valid on this device, peer memory through fw_ipc_open), so after the next barrier all
+ * ranks agree without a collective. */
+int fw_stage_seis_update_peers(fw_ctx ctx, long long n, double tau, const double* cur, const double* prev,
+                               const double* l2prev, const double* l1, const double* l2, const double* c,
+                               const double* eta, const double* tau_coef, double* next, double* l2out, double thr,
+                               int step, int* flag_dev, int npeers, int* const* peer_flags_dev);
 /* distributed seismic stepper pieces (slab.SlabSeismicStepper), element-wise on a slab:
  *   fw_medium_coefficients  host: c, eta, tau_c from gamma, c0 (derive_medium, seismic.cpp:30-39; glibc
  *                           pow/cos/sin exactly as the reference), FW_E_GAMMA_RANGE outside [0, 0.5)
@@ -299,6 +316,10 @@ int fw_stage_seis_update(fw_ctx ctx, long long n, double tau, const double* cur,
                          const double* tau_coef, double* next, double thr, int step, int* flag_dev);
 /* CUDA IPC helpers for the fused-transpose slab path (one process per GPU of a node):
  * export a device allocation, map a peer's allocation into this device's address space */
+/* fw_ipc_alloc / fw_ipc_free: plain device allocations for exported buffers (a handle maps the
+ * allocation base: fw_ipc_handle refuses interior pointers with FW_E_ARG) */
+int fw_ipc_alloc(fw_ctx ctx, size_t bytes, void** dev_ptr_out);
+int fw_ipc_free(fw_ctx ctx, void* dev_ptr);
 int fw_ipc_handle(const void* dev_ptr, unsigned char handle_out[64]);
 int fw_ipc_open(const unsigned char handle[64], void** dev_ptr_out);
 int fw_ipc_close(void* dev_ptr);

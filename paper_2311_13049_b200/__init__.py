@@ -57,6 +57,7 @@ from .api import (  # noqa: F401
     build_expansion,
     build_grid,
     build_medium,
+    build_slab_expansion,
     default_context,
     DenseOperator,
     apply_constant_order,

@@ -154,6 +154,11 @@ def load_library():
     lib.fw_dense_entries.argtypes = [_vp, _dp]
     lib.fw_apply_toeplitz.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp, _dp, _dp]
     lib.fw_truncation_indicator.argtypes = [C.c_int, C.c_double, C.c_double, _dp]
+    lib.fw_op_create_slab.argtypes = [_vp, _ip, _dp, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
+    lib.fw_ipc_alloc.argtypes = [_vp, C.c_size_t, C.POINTER(_vp)]
+    lib.fw_ipc_free.argtypes = [_vp, _vp]
+    lib.fw_stage_seis_update_peers.argtypes = ([_vp, C.c_longlong, C.c_double] + [_vp] * 10
+                                               + [C.c_double, C.c_int, _vp, C.c_int, _vp])
     lib.fw_grid_dft_device.argtypes = [_vp, C.c_int, _ip, _vp, C.c_int]
     lib.fw_grid_forward.argtypes = [_vp, C.c_int, _ip, _dp, _dp]
     lib.fw_grid_inverse.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp]
@@ -211,5 +216,5 @@ EXPORTED_SYMBOLS = [
     "fw_wave_get", "fw_rfftn", "fw_irfftn", "fw_op_path", "fw_ricker_initial", "fw_grid_dft", "fw_grid_dft_device",
     "fw_grid_forward", "fw_grid_inverse", "fw_apply_constant_order", "fw_apply_constant_order_spectrum",
     "fw_dense_create", "fw_dense_destroy", "fw_dense_apply", "fw_dense_entries", "fw_apply_toeplitz",
-    "fw_truncation_indicator",
+    "fw_truncation_indicator", "fw_op_create_slab", "fw_stage_seis_update_peers", "fw_ipc_alloc", "fw_ipc_free",
 ]

@@ -153,6 +153,7 @@ class ExpansionOperator:
         self.smin, self.smax = info.smin, info.smax
         self.N, self.N_half = info.N, info.N_half
         self.device_bytes = info.device_bytes
+        self.slab = None  # (P, rank) for build_slab_expansion operators
 
     @property
     def handle(self):
@@ -213,6 +214,25 @@ def build_expansion(order: OrderField, M: int, ctx: Optional[Context] = None) ->
     check(load_library().fw_op_create(ctx.handle, g.dim, J, lo, hi, _ptr(order.values),
                                       C.byref(s0) if s0 is not None else None, int(M), C.byref(h)))
     return ExpansionOperator(h, g, ctx, order)
+
+
+def build_slab_expansion(order: OrderField, M: int, P: int, rank: int,
+                         ctx: Optional[Context] = None) -> ExpansionOperator:
+    """One rank's tables of a slab-decomposed 3D operator (fw_op_create_slab): w_m on the rank's
+    spectral columns, s - s0 on its planes; s0 and validation from the global order values."""
+    ctx = ctx or default_context()
+    g = order.grid
+    if g.dim != 3:
+        raise ArgumentError("slab decomposition is three-dimensional")
+    J, lo, hi = g._carrays()
+    s0 = C.c_double(order.s0_override) if order.s0_override is not None else None
+    h = C.c_void_p()
+    check(load_library().fw_op_create_slab(ctx.handle, J, lo, hi, _ptr(order.values),
+                                           C.byref(s0) if s0 is not None else None, int(M), int(P), int(rank),
+                                           C.byref(h)))
+    op = ExpansionOperator(h, g, ctx, order)
+    op.slab = (int(P), int(rank))
+    return op
 
 
 def _check_field(op: ExpansionOperator, u):

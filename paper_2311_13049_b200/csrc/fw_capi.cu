@@ -8,7 +8,9 @@
 // operator on the Hermitian half; the M-fold recurrences run on the device
 // (IEEE mul/div: bit-identical).  There is no CPU compute fallback: every
 // apply runs the sm_100a kernels in fw_kernels.cu.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -284,6 +286,7 @@ struct fw_op_s {
   size_t bytes = 0;
   bool step2d = false;
   bool full = false;       // non-power-of-two axes: full-spectrum tables, C2C apply (fw_dft.cu)
+  bool slab = false;       // fw_op_create_slab: tables of one rank's slab only (stage entry points)
 };
 
 extern "C" {
@@ -529,6 +532,7 @@ int apply_device(fw_op op, const double* u, double* out, int m_first, double* re
     FW_CUDA(cudaMemsetAsync(out, 0, g.N * sizeof(double), ctx->stream));
     return FW_OK;
   }
+  if (op->slab) return set_err(FW_E_ARG, "slab operator: its tables cover one rank's slab (use the stage entry points)");
   if (op->full) {  // non-power-of-two axes: the C2C form (fw_dft.cu)
     void *uh = nullptr, *buf = nullptr, *devm = nullptr;
     FW_TRY(ctx->get_scratch(SLOT_UH, g.N * sizeof(double2), &uh));
@@ -574,6 +578,91 @@ int fw_op_create(fw_ctx ctx, int dim, const int* J, const double* lo, const doub
   FW_TRY(plan_grid(dim, J, lo, hi, &g, &full));
   FW_CUDA(cudaSetDevice(ctx->device));
   return op_create_internal(ctx, g, lo, hi, order_values, s0_override, M, out, full);
+}
+
+// One rank's tables of a slab-decomposed 3D grid (slab.py): w_m on the rank's spectral columns
+// [J0][J1/P][H] (axis-1 bins [rank J1/P, (rank+1) J1/P)), s - s0 on its planes [J0/P][J1][J2]; s0 and
+// the OrderField checks from the GLOBAL order values (orderfield.cpp:10-36), so every rank's tables
+// equal the corresponding slices of the single-device operator's (bit for bit).
+int fw_op_create_slab(fw_ctx ctx, const int* J, const double* lo, const double* hi, const double* order_values,
+                      const double* s0_override, int M, int P, int rank, fw_op* out) {
+  FW_SETDEV(ctx);
+  if (!ctx || !out || !lo || !hi || !order_values) return set_err(FW_E_ARG, "null argument");
+  fw::GridGeom g;
+  FW_TRY(check_grid(3, J, lo, hi, &g));
+  if (P < 1 || rank < 0 || rank >= P || J[0] % P || J[1] % P)
+    return set_err(FW_E_ARG, "slab: axes 0 and 1 must be divisible by P and 0 <= rank < P");
+  double s0, smin, smax;
+  int constant;
+  FW_TRY(order_stats(order_values, g.N, s0_override, &s0, &smin, &smax, &constant));
+  if (M < 0) return set_err(FW_E_NEGATIVE_M, "truncation count M must be >= 0");
+  const int J1l = J[1] / P, J0l = J[0] / P, H = g.hp1;
+  const size_t nw = (size_t)J[0] * J1l * H;       // spectral bins of the rank's columns
+  const size_t nd = (size_t)J0l * J[1] * J[2];    // the rank's planes
+  fw_op_s* op = new fw_op_s();
+  op->ctx = ctx;
+  op->g = g;
+  for (int m = 0; m < 3; ++m) {
+    op->lo[m] = lo[m];
+    op->hi[m] = hi[m];
+  }
+  op->M = M;
+  op->slab = true;
+  op->s0 = s0;
+  op->smin = smin;
+  op->smax = smax;
+  op->constant_order = constant;
+  if (dalloc(&op->w, (size_t)(M + 1) * nw) || dalloc(&op->dev1, nd)) {
+    fw_op_destroy(op);
+    return FW_E_OOM;
+  }
+  op->bytes = ((size_t)(M + 1) * nw + nd) * sizeof(double);
+  // |mu|^2 at (k0, k1 in the rank's columns, k2 < H), summed m = 2..0 as grid.cpp:71-79
+  std::vector<double> ax[3];
+  for (int m = 0; m < 3; ++m) {
+    ax[m].resize(J[m]);
+    const double base = 2.0 * M_PI / (hi[m] - lo[m]);
+    for (int p = 0; p < J[m]; ++p) {
+      const int k = (p < J[m] / 2) ? p : p - J[m];
+      ax[m][p] = (base * k) * (base * k);
+    }
+  }
+  std::vector<double> mu2(nw), base(nw), logm(nw);
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < (long long)nw; ++i) {
+    const int k2 = (int)(i % H);
+    const int k1 = rank * J1l + (int)((i / H) % J1l);
+    const int k0 = (int)(i / ((size_t)H * J1l));
+    double v = 0.0;
+    v += ax[2][k2];
+    v += ax[1][k1];
+    v += ax[0][k0];
+    mu2[i] = v;
+    base[i] = v > 0.0 ? pow(v, s0) : 0.0;  // flap.cpp:108-110
+    logm[i] = v > 0.0 ? log(v) : 0.0;      // flap.cpp:119
+  }
+  double *d_mu2 = nullptr, *d_base = nullptr, *d_logm = nullptr, *d_s = nullptr;
+  int rc = FW_OK;
+  if ((rc = dalloc(&d_mu2, nw)) || (rc = dalloc(&d_base, nw)) || (rc = dalloc(&d_logm, nw)) || (rc = dalloc(&d_s, nd))) {
+    cudaFree(d_mu2); cudaFree(d_base); cudaFree(d_logm); cudaFree(d_s);
+    fw_op_destroy(op);
+    return rc;
+  }
+  auto L = ctx->L();
+  cudaMemcpyAsync(d_mu2, mu2.data(), nw * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(d_base, base.data(), nw * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(d_logm, logm.data(), nw * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(d_s, order_values + (size_t)rank * nd, nd * 8, cudaMemcpyHostToDevice, ctx->stream);
+  fw::launch_build_weights(L, nw, M, d_mu2, d_base, d_logm, op->w);
+  fw::launch_dev1(L, nd, d_s, s0, op->dev1);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d_mu2); cudaFree(d_base); cudaFree(d_logm); cudaFree(d_s);
+  if (e != cudaSuccess) {
+    fw_op_destroy(op);
+    return set_err(FW_E_CUDA, std::string("slab tables: ") + cudaGetErrorString(e));
+  }
+  *out = op;
+  return FW_OK;
 }
 
 int fw_op_create_from_tables(fw_ctx ctx, int dim, const int* J, const double* lo, const double* hi, int M,
@@ -1875,8 +1964,54 @@ int fw_stage_seis_update(fw_ctx ctx, long long n, double tau, const double* cur,
   return FW_OK;
 }
 
+int fw_stage_seis_update_peers(fw_ctx ctx, long long n, double tau, const double* cur, const double* prev,
+                               const double* l2prev, const double* l1, const double* l2, const double* c,
+                               const double* eta, const double* tau_coef, double* next, double* l2out, double thr,
+                               int step, int* flag_dev, int npeers, int* const* peer_flags_dev) {
+  FW_SETDEV(ctx);
+  if (!ctx || n < 0 || !cur || !prev || !l2prev || !l1 || !l2 || !c || !eta || !tau_coef || !next || !l2out || !flag_dev ||
+      npeers < 0 || npeers > fw::kMaxPeers || (npeers > 0 && !peer_flags_dev))
+    return set_err(FW_E_ARG, "bad argument");
+  fw::PeerFlags pf;
+  pf.n = npeers;
+  for (int q = 0; q < npeers; ++q) pf.f[q] = peer_flags_dev[q];
+  fw::launch_seis_update_peers(ctx->L(), (size_t)n, tau, cur, prev, l2prev, l1, l2, c, eta, tau_coef, next, l2out, thr,
+                               step, flag_dev, pf);
+  FW_CUDA(cudaGetLastError());
+  return FW_OK;
+}
+
+// receive buffers for peer stores: plain cudaMalloc allocations, so that a peer's
+// cudaIpcOpenMemHandle maps exactly this address (a handle maps the allocation BASE)
+int fw_ipc_alloc(fw_ctx ctx, size_t bytes, void** dev_ptr_out) {
+  FW_SETDEV(ctx);
+  if (!ctx || !dev_ptr_out || bytes == 0) return set_err(FW_E_ARG, "bad argument");
+  FW_CUDA(cudaMalloc(dev_ptr_out, bytes));
+  return FW_OK;
+}
+
+int fw_ipc_free(fw_ctx ctx, void* dev_ptr) {
+  FW_SETDEV(ctx);
+  if (dev_ptr) FW_CUDA(cudaFree(dev_ptr));
+  return FW_OK;
+}
+
 int fw_ipc_handle(const void* dev_ptr, unsigned char handle_out[64]) {
   if (!dev_ptr || !handle_out) return set_err(FW_E_ARG, "null argument");
+  {  // a handle maps the allocation base: refuse interior pointers (e.g. a caching allocator's block)
+    static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+    if (!range) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", (void**)&range, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        range = nullptr;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range && range(&base, &size, (CUdeviceptr)dev_ptr) == CUDA_SUCCESS && base != (CUdeviceptr)dev_ptr)
+      return set_err(FW_E_ARG, "IPC export of an interior pointer (the peer would map the allocation base); "
+                               "allocate the buffer with fw_ipc_alloc");
+  }
   cudaIpcMemHandle_t h;
   FW_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
   static_assert(sizeof(h) == 64, "CUDA IPC handle size");

@@ -39,6 +39,17 @@ struct LaunchCtx {
   bool generic_lines = false;       // FW_GENERIC_LINES=1: shared-memory line FFTs only (tests)
 };
 
+// every rank's blow-up flag (device addresses valid on this device: local or peer memory)
+constexpr int kMaxPeers = 8;
+struct PeerFlags {
+  int n = 0;
+  int* f[kMaxPeers] = {};
+};
+void launch_seis_update_peers(const LaunchCtx& L, size_t N, double tau, const double* cur, const double* prev,
+                              const double* ap, const double* l1, const double* l2, const double* c, const double* eta,
+                              const double* tc, double* next, double* l2out, double thr, int step, int* flag,
+                              const PeerFlags& peers);
+
 // every line of length n (power of two <= 4096) along a strided axis of a complex array, in
 // place: element j of line (o, in) at o n S + j S + in (in < S); canonical plan; x sc if scale
 void launch_c2c_lines(const LaunchCtx& L, int n, long long S, long long outer, int dir, double2* x, double sc,

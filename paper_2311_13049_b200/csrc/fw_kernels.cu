@@ -277,6 +277,31 @@ __global__ void k_seis_update(long long N, double tau, const double* __restrict_
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(flag, step);
 }
 
+// the slab stepper's update: as k_seis_update, plus the new L2prev copy (l2out) and the blow-up flag
+// min-ed into every rank's flag (peer memory, system scope) so that after the next barrier every
+// rank freezes its later updates (the state levels before the offending step stay intact)
+__global__ void k_seis_update_peers(long long N, double tau, const double* __restrict__ cur,
+                                    const double* __restrict__ prev, const double* __restrict__ ap,
+                                    const double* __restrict__ l1, const double* __restrict__ l2,
+                                    const double* __restrict__ c, const double* __restrict__ eta,
+                                    const double* __restrict__ tc, double* __restrict__ next,
+                                    double* __restrict__ l2out, double thr, int step, int* flag, PeerFlags peers) {
+  if (*reinterpret_cast<volatile int*>(flag) != kNoBlowup) return;  // an earlier step blew up (on some rank)
+  const double t2 = tau * tau;
+  bool bad = false;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const double c2 = c[j] * c[j];
+    const double v = 2.0 * cur[j] - prev[j] + t2 * c2 * (eta[j] * l1[j] + tc[j] * (l2[j] - ap[j]) / tau);
+    next[j] = v;
+    l2out[j] = l2[j];
+    bad |= fabs(v) > thr;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
+    atomicMin(flag, step);
+    for (int q = 0; q < peers.n; ++q) atomicMin_system(peers.f[q], step);
+  }
+}
+
 __global__ void k_osc_rotate(long long Nh, const double* __restrict__ w, const double* __restrict__ cw,
                              const double* __restrict__ sw, double dt, double2* __restrict__ uh,
                              double2* __restrict__ vh) {
@@ -468,6 +493,15 @@ void launch_seis_update(const LaunchCtx& L, size_t N, double tau, const double* 
                         const double* tc, double* next, double thr, int step, int* flag) {
   k_seis_update<<<elementwise_grid(N), kThreads, 0, L.stream>>>((long long)N, tau, cur, prev, ap, l1, l2, c, eta,
                                                                tc, next, thr, step, flag);
+  count(L);
+}
+
+void launch_seis_update_peers(const LaunchCtx& L, size_t N, double tau, const double* cur, const double* prev,
+                              const double* ap, const double* l1, const double* l2, const double* c, const double* eta,
+                              const double* tc, double* next, double* l2out, double thr, int step, int* flag,
+                              const PeerFlags& peers) {
+  k_seis_update_peers<<<elementwise_grid(N), kThreads, 0, L.stream>>>((long long)N, tau, cur, prev, ap, l1, l2, c, eta,
+                                                                     tc, next, l2out, thr, step, flag, peers);
   count(L);
 }
 

@@ -211,13 +211,20 @@ class DeviceStages:
         return out
 
     def local_tables(self, op, geo: SlabGeometry):
-        """(w_local [M+1][J0][J1/P][H] complex-layout-compatible real weights, dev1 slab, m_last)
-        sliced from the operator's resident device tables (zero-copy views + one gather)."""
+        """(w_local [M+1][J0][J1/P][H] real weights of this rank's spectral columns, dev1 of its
+        planes, m_last).  A per-rank operator (api.build_slab_expansion: table bytes 1/P) is used
+        as it is (zero-copy views); a full-grid operator is sliced (one gather)."""
         t = self.torch
         w, d1, ml = C.c_void_p(), C.c_void_p(), C.c_int()
         self.check(self.lib.fw_op_device_tables(op.handle, C.byref(w), C.byref(d1), C.byref(ml)))
         J0, J1, J2 = geo.J
         H = geo.H
+        if getattr(op, "slab", None) is not None:
+            if tuple(op.slab) != (geo.P, geo.rank):
+                raise ValueError(f"operator tables are rank {op.slab[1]} of {op.slab[0]}, not {geo.rank} of {geo.P}")
+            wl = t.as_tensor(_CAI(w.value, (op.M + 1, J0, geo.J1l, H)), device="cuda")
+            dl = t.as_tensor(_CAI(d1.value, (geo.J0l, J1, J2)), device="cuda")
+            return wl, dl, ml.value
         wt = t.as_tensor(_CAI(w.value, (op.M + 1, J0, J1, H)), device="cuda")
         dt = t.as_tensor(_CAI(d1.value, (J0, J1, J2)), device="cuda")
         with t.cuda.stream(self.stream):
@@ -289,26 +296,32 @@ class FusedSlabApply:
 
 class SlabSeismicStepper:
     """``SeismicStepper`` (seismic.hpp:36-46, seismic.cpp:85-142) on a slab-decomposed 3D
-    grid: every rank owns planes [r J0/P, (r+1) J0/P) of the wavefields.  Per step one
-    forward transform (fused transpose) shared by the two operators (orders 1+gamma and
-    1/2+gamma), their all-terms inverses (fused transposes into per-operator buffers), and
-    the fused update; the blow-up flag is combined over the ranks every step, and on a
-    blow-up every rank keeps its pre-step state (reference semantics).
+    grid: every rank owns planes [r J0/P, (r+1) J0/P) of the wavefields and only its slab of the
+    two operators' tables (build_slab_expansion: table bytes fall as 1/P).  Per step one forward
+    transform (fused transpose) shared by the two operators (orders 1+gamma and 1/2+gamma), their
+    all-terms inverses (fused transposes into per-operator buffers) and the fused update.
+
+    State: three wavefield levels and two L2prev levels rotate with the level counter (as the
+    single-GPU stepper); the update of a blown-up step mins the step into EVERY rank's flag (peer
+    memory), so after the next barrier all ranks freeze their later updates and the levels before
+    the offending step survive.  The host reads the flag once per ``advance`` (no per-step
+    collective or device-to-host read) and rewinds to the pre-step state (seismic.cpp:124-129).
 
     grid: the global ``Grid``; gamma, c0, phi, psi: global numpy fields (every rank passes the
     same arrays; only its slab is uploaded); peers_factory(op_index, geo, nt_max, ctx) -> peers
-    (IpcPeers across processes; shared LocalPeers for virtual ranks in one process).
+    (IpcPeers across processes; shared LocalPeers for virtual ranks in one process; peers of
+    operator 0 also carry the blow-up flags).
     With construct=False the caller runs the constructor's three applies itself and calls
     start() (tests interleave virtual ranks that way)."""
 
     def __init__(self, grid, gamma, c0, omega0, M, phi, psi, tau, geo: SlabGeometry, ctx, peers_factory,
-                 blowup_factor: float = 1e8, flag_reduce=None, construct: bool = True):
+                 blowup_factor: float = 1e8, construct: bool = True):
         import torch
 
         from . import api
         from ._capi import check, load_library
 
-        self.torch, self.lib, self.check = torch, load_library(), check
+        self.torch, self.lib, self._chk = torch, load_library(), check
         self.g, self.ctx, self.tau = geo, ctx, float(tau)
         rows = geo.rows
         J = tuple(geo.J)
@@ -325,33 +338,52 @@ class SlabSeismicStepper:
                                          co.ctypes.data_as(dp), eta.ctypes.data_as(dp), tc.ctypes.data_as(dp)))
         self._dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
         self.c, self.eta, self.tc = self._dev(co), self._dev(eta), self._dev(tc)
-        # the two operators (full tables on every rank, sliced to the slab)
+        # the two operators: this rank's slab of their tables only
         self.stages = DeviceStages(ctx)
-        self.ops = [api.build_expansion(api.OrderField(grid, 1.0 + gamma), M, ctx=ctx),
-                    api.build_expansion(api.OrderField(grid, 0.5 + gamma), M, ctx=ctx)]
+        self.ops = [api.build_slab_expansion(api.OrderField(grid, 1.0 + gamma), M, geo.P, geo.rank, ctx=ctx),
+                    api.build_slab_expansion(api.OrderField(grid, 0.5 + gamma), M, geo.P, geo.rank, ctx=ctx)]
+        self.table_bytes = sum(op.device_bytes for op in self.ops)
         self.apps = []
         for k, op in enumerate(self.ops):
             wl, dl, ml = self.stages.local_tables(op, geo)
             self.apps.append(FusedSlabApply(geo, self.stages, peers_factory(k, geo, ml + 1, ctx), wl, dl, ml))
         self.peers = self.apps[0].peers
-        self.flag = torch.full((1,), 0x7FFFFFFF, dtype=torch.int32, device="cuda")
-        self.flag_reduce = flag_reduce
+        self.flag = self.peers.flag(geo.rank)
+        self._pf = (C.c_void_p * len(self.peers.flag_ptrs))(*[C.c_void_p(int(x)) for x in self.peers.flag_ptrs])
         self.thr = blowup_factor * max(float(np.max(np.abs(phi))), 1e-300)  # seismic.cpp:93
         lib.fw_stage_seis_start.argtypes = [C.c_void_p, C.c_longlong, C.c_double] + [C.c_void_p] * 8
-        lib.fw_stage_seis_update.argtypes = ([C.c_void_p, C.c_longlong, C.c_double] + [C.c_void_p] * 9
-                                             + [C.c_double, C.c_int, C.c_void_p])
+        self.ub = [torch.empty(geo.J0l * J[1] * J[2], dtype=torch.float64, device="cuda").reshape(geo.J0l, J[1], J[2])
+                   for _ in range(3)]
+        self.ab = [torch.empty_like(self.ub[0]) for _ in range(2)]
         self.phi_l, self.psi_l = self._dev(phi[rows]), self._dev(psi[rows])
         if construct:  # seismic.cpp:85-109 (one process per rank)
             self.start(self.apps[0].apply(self.phi_l), self.apps[1].apply(self.psi_l), self.apps[1].apply(self.phi_l))
 
+    # levels: cur = ub[L % 3], prev = ub[(L + 2) % 3], next = ub[(L + 1) % 3]; L2prev = ab[(L + 1) % 2],
+    # the step's new L2prev = ab[L % 2]
+    @property
+    def cur(self):
+        return self.ub[self.lvl % 3]
+
+    @property
+    def prev(self):
+        return self.ub[(self.lvl + 2) % 3]
+
+    @property
+    def l2prev(self):
+        return self.ab[(self.lvl + 1) % 2]
+
     def start(self, l1phi, l2psi, l2phi):
         """cur = phi + tau psi + tau^2/2 c^2 (eta L1phi + tau_c L2psi), prev = phi, L2prev = L2phi, n = 1."""
-        cur = self.torch.empty_like(self.phi_l)
-        self.check(self.lib.fw_stage_seis_start(self.ctx.handle, self.nloc, self.tau, self.phi_l.data_ptr(),
+        st = self.stages.stream
+        self.lvl, self.n = 1, 1
+        with self.torch.cuda.stream(st):
+            self.prev.copy_(self.phi_l)
+            self.l2prev.copy_(l2phi)
+        self._chk(self.lib.fw_stage_seis_start(self.ctx.handle, self.nloc, self.tau, self.phi_l.data_ptr(),
                                                 self.psi_l.data_ptr(), self.c.data_ptr(), self.eta.data_ptr(),
                                                 self.tc.data_ptr(), l1phi.data_ptr(), l2psi.data_ptr(),
-                                                cur.data_ptr()))
-        self.prev, self.cur, self.l2prev, self.n = self.phi_l, cur, l2phi, 1
+                                                self.cur.data_ptr()))
 
     # ---- one step in three phases (peers.barrier() between them; step() does it all) ----
     def phase_forward(self):
@@ -363,46 +395,54 @@ class SlabSeismicStepper:
         self.apps[1].phase_inverse(0, uhat)
 
     def phase_update(self):
+        """The update (seismic.cpp:116-129) into the next level; advances n and the level whether or not
+        the step blew up (check() rewinds)."""
         l1, l2 = self.apps[0].phase_finish(0), self.apps[1].phase_finish(0)
-        self._next = self.torch.empty_like(self.cur)
-        self._l2 = l2
-        self.check(self.lib.fw_stage_seis_update(self.ctx.handle, self.nloc, self.tau, self.cur.data_ptr(),
-                                                 self.prev.data_ptr(), self.l2prev.data_ptr(), l1.data_ptr(),
-                                                 l2.data_ptr(), self.c.data_ptr(), self.eta.data_ptr(),
-                                                 self.tc.data_ptr(), self._next.data_ptr(), self.thr, self.n + 1,
-                                                 self.flag.data_ptr()))
-
-    def blown(self):
-        """The offending step over all ranks (flag_reduce = a min all-reduce), or None.
-        fw_stage_seis_update wrote the flag on the context's (non-blocking) stream: wait for
-        it before torch reads the flag on its own stream."""
-        self.ctx.sync()
-        f = self.flag.clone()
-        if self.flag_reduce is not None:
-            f = self.flag_reduce(f)
-        v = int(f.item())
-        return None if v == 0x7FFFFFFF else v
-
-    def commit(self):
-        self.prev, self.cur, self.l2prev = self.cur, self._next, self._l2
+        nxt, l2o = self.ub[(self.lvl + 1) % 3], self.ab[self.lvl % 2]
+        self._chk(self.lib.fw_stage_seis_update_peers(
+            self.ctx.handle, self.nloc, self.tau, self.cur.data_ptr(), self.prev.data_ptr(), self.l2prev.data_ptr(),
+            l1.data_ptr(), l2.data_ptr(), self.c.data_ptr(), self.eta.data_ptr(), self.tc.data_ptr(), nxt.data_ptr(),
+            l2o.data_ptr(), self.thr, self.n + 1, self.flag.data_ptr(), len(self.peers.flag_ptrs), self._pf))
+        self.lvl += 1
         self.n += 1
 
-    def step(self):
+    def blown(self):
+        """The offending step agreed by every rank, or None.  The flag is written on the context's
+        (non-blocking) stream and by the peers' updates: call after a barrier (check() does)."""
+        self.ctx.sync()
+        v = int(self.flag.item())
+        return None if v == 0x7FFFFFFF else v
+
+    def check(self):
+        """Once per advance: after a barrier every rank's flag holds the earliest offending step over
+        all ranks; rewind to the state before it and raise BlowupDetected (seismic.cpp:124-129)."""
         from ._capi import BlowupDetected
 
+        self.peers.barrier()
+        bad = self.blown()
+        if bad is None:
+            return
+        self.lvl -= self.n - bad + 1  # the levels before the offending step (later updates were frozen)
+        self.n = bad
+        self.peers.barrier()  # every rank has read the flag before any resets it
+        self.flag.fill_(0x7FFFFFFF)
+        self.ctx.sync()
+        raise BlowupDetected(f"sup|u| > {self.thr:g} at step {bad}")
+
+    def step_nocheck(self):
         self.phase_forward()
         self.peers.barrier()
         self.phase_inverse()
         self.peers.barrier()
         self.phase_update()
-        bad = self.blown()
-        if bad is not None:  # the state stays the pre-step one (seismic.cpp:124-129)
-            raise BlowupDetected(f"sup|u| > {self.thr:g} at step {bad}")
-        self.commit()
+
+    def step(self):
+        self.advance(1)
 
     def advance(self, steps: int):
         for _ in range(int(steps)):
-            self.step()
+            self.step_nocheck()
+        self.check()
 
     def state(self):
         """(cur, prev, L2prev) of this rank's slab (torch CUDA tensors) and n."""
@@ -411,7 +451,8 @@ class SlabSeismicStepper:
 
 class LocalPeers:
     """Receive buffers of P virtual ranks on ONE device (tests / single-GPU use of the fused
-    path): the pointer tables address local tensors; barrier() is a stream sync."""
+    path): the pointer tables address local tensors; barrier() is a stream sync.  One blow-up
+    flag per virtual rank (flag(r), flag_ptrs)."""
 
     def __init__(self, geo: SlabGeometry, nt_max: int, ctx):
         import torch
@@ -421,8 +462,10 @@ class LocalPeers:
         self._T = [torch.empty((J0, geo.J1l, geo.H), dtype=torch.complex128, device="cuda") for _ in range(geo.P)]
         self._Ts = [torch.empty((nt_max, geo.J0l, J1, geo.H), dtype=torch.complex128, device="cuda")
                     for _ in range(geo.P)]
+        self._flags = [torch.full((1,), 0x7FFFFFFF, dtype=torch.int32, device="cuda") for _ in range(geo.P)]
         self.T_ptrs = [t.data_ptr() for t in self._T]
         self.Ts_ptrs = [t.data_ptr() for t in self._Ts]
+        self.flag_ptrs = [f.data_ptr() for f in self._flags]
 
     def T(self, r):
         return self._T[r]
@@ -430,58 +473,99 @@ class LocalPeers:
     def Ts(self, r):
         return self._Ts[r]
 
+    def flag(self, r):
+        return self._flags[r]
+
     def barrier(self):
         self.ctx.sync()
 
 
 class IpcPeers(LocalPeers):
     """Receive buffers of the P ranks of a torch.distributed job on one node: each rank
-    allocates its own, exports CUDA IPC handles, and maps the others' (peer memory over
-    NVLink); barrier() = device sync + process-group barrier."""
+    allocates its own with fw_ipc_alloc (plain device allocations: a CUDA IPC handle maps the
+    allocation BASE, so a buffer inside a caching allocator's block would receive peer stores at
+    the wrong address), exports the handles and maps the others' (peer memory over NVLink);
+    barrier() = device sync + process-group barrier."""
 
     def __init__(self, geo: SlabGeometry, nt_max: int, ctx):
         import torch
         import torch.distributed as dist
 
-        J0, J1, _ = geo.J
-        self.ctx, self.dist = ctx, dist
-        self._mine_T = torch.empty((J0, geo.J1l, geo.H), dtype=torch.complex128, device="cuda")
-        self._mine_Ts = torch.empty((nt_max, geo.J0l, J1, geo.H), dtype=torch.complex128, device="cuda")
         from . import _capi
 
+        J0, J1, _ = geo.J
+        self.ctx, self.dist, self.torch = ctx, dist, torch
         lib, check = _capi.load_library(), _capi.check
+        self._lib = lib
         lib.fw_ipc_handle.argtypes = [C.c_void_p, C.c_char_p]
         lib.fw_ipc_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.fw_ipc_close.argtypes = [C.c_void_p]
+        shapes = {"T": ((J0, geo.J1l, geo.H), "<c16", 16), "Ts": ((nt_max, geo.J0l, J1, geo.H), "<c16", 16),
+                  "flag": ((1,), "<i4", 4)}
+        self._own, self._alloc = {}, []
+        for key, (shape, typestr, esize) in shapes.items():
+            ptr = C.c_void_p()
+            check(lib.fw_ipc_alloc(ctx.handle, max(256, int(np.prod(shape)) * esize), C.byref(ptr)))
+            self._alloc.append(ptr.value)
+            self._own[key] = torch.as_tensor(_CAI(ptr.value, shape, typestr), device="cuda")
+        self._own["flag"].fill_(0x7FFFFFFF)
         handles = []
-        for t in (self._mine_T, self._mine_Ts):
+        for key in ("T", "Ts", "flag"):
             hbuf = C.create_string_buffer(64)
-            check(lib.fw_ipc_handle(C.c_void_p(t.data_ptr()), hbuf))
+            check(lib.fw_ipc_handle(C.c_void_p(self._own[key].data_ptr()), hbuf))
             handles.append(hbuf.raw)
         allh = [None] * geo.P
         dist.all_gather_object(allh, handles)
-        self.T_ptrs, self.Ts_ptrs = [], []
-        for r, (hT, hTs) in enumerate(allh):
-            if r == geo.rank:
-                self.T_ptrs.append(self._mine_T.data_ptr())
-                self.Ts_ptrs.append(self._mine_Ts.data_ptr())
-                continue
-            for hnd, lst in ((hT, self.T_ptrs), (hTs, self.Ts_ptrs)):
+        _debug(f"rank {geo.rank}: IPC handles exchanged")
+        self.T_ptrs, self.Ts_ptrs, self.flag_ptrs, self._opened = [], [], [], []
+        for r, hs in enumerate(allh):
+            for key, hnd, lst in zip(("T", "Ts", "flag"), hs, (self.T_ptrs, self.Ts_ptrs, self.flag_ptrs)):
+                if r == geo.rank:
+                    lst.append(self._own[key].data_ptr())
+                    continue
                 p = C.c_void_p()
                 check(lib.fw_ipc_open(C.create_string_buffer(hnd, 64), C.byref(p)))
+                self._opened.append(p.value)
                 lst.append(p.value)
         self.rank = geo.rank
+        _debug(f"rank {geo.rank}: peer buffers mapped")
+        ctx.sync()
+        dist.barrier()
 
     def T(self, r):
         assert r == self.rank
-        return self._mine_T
+        return self._own["T"]
 
     def Ts(self, r):
         assert r == self.rank
-        return self._mine_Ts
+        return self._own["Ts"]
+
+    def flag(self, r):
+        assert r == self.rank
+        return self._own["flag"]
 
     def barrier(self):
         self.ctx.sync()
         self.dist.barrier()
+
+    def close(self):
+        """Unmap the peers' buffers, then free this rank's (after a barrier: no peer still writes)."""
+        self.barrier()
+        for p in self._opened:
+            self._lib.fw_ipc_close(C.c_void_p(p))
+        self._opened = []
+        self.barrier()
+        for p in self._alloc:
+            self._lib.fw_ipc_free(self.ctx.handle, C.c_void_p(p))
+        self._alloc = []
+
+
+def _debug(msg):
+    import os
+    import sys
+
+    if os.environ.get("FW_SLAB_DEBUG") == "1":
+        print(msg, file=sys.stderr, flush=True)
 
 
 class TorchComm:

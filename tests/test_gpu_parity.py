@@ -562,6 +562,7 @@ def _slab_run(P, tau, blowup_factor, nsteps):
     J, lo, hi, gamma, phi = _slab_case()
     c0, psi = np.ones(J), np.zeros(J)
     g = m.Grid(list(zip(lo, hi)), list(J))
+    from paper_2311_13049_b200.slab import SlabGeometry as _SG  # noqa: F401
     ref = m.SeismicStepper(m.build_medium(g, gamma, c0, 1.0, 6), phi, psi, tau, blowup_factor=blowup_factor)
     ref_exc = None
     try:
@@ -590,8 +591,7 @@ def _slab_run(P, tau, blowup_factor, nsteps):
         outs[key] = [st.apps[k].phase_finish(0) for st in sts]
     for r, st in enumerate(sts):
         st.start(outs["l1phi"][r], outs["l2psi"][r], outs["l2phi"][r])
-    bad = None
-    for _ in range(nsteps):
+    for _ in range(nsteps):  # no per-step flag read: the updates freeze once any rank flagged
         for st in sts:
             st.phase_forward()
         ctx.sync()
@@ -600,13 +600,12 @@ def _slab_run(P, tau, blowup_factor, nsteps):
         ctx.sync()
         for st in sts:
             st.phase_update()
-        flags = [st.blown() for st in sts]  # the min all-reduce of flag_reduce, by hand
-        flags = [f for f in flags if f is not None]
-        if flags:
-            bad = min(flags)
-            break
-        for st in sts:
-            st.commit()
+    bad = None
+    for st in sts:  # once, at the end (as advance(): every rank reads the same agreed step)
+        try:
+            st.check()
+        except m.BlowupDetected:
+            bad = st.n
     ctx.sync()
     got = [np.concatenate([st.state()[i].cpu().numpy() for st in sts]) for i in range(3)]
     return ref, ref_exc, got, sts[0].n, bad
@@ -627,9 +626,9 @@ def test_slab_seismic_stepper_equals_single_gpu(P):
 
 @pytest.mark.parametrize("P", [1, 2])
 def test_slab_seismic_stepper_blowup_matches_single_gpu(P):
-    """A blow-up inside the slab stepper: the flag written on the context stream is read
-    after that stream (blown() syncs it), the offending step equals the single-GPU
-    stepper's BlowupDetected step, and the slab state is the pre-step state (seismic.cpp:124-129)."""
+    """A blow-up inside the slab stepper: the offending rank's update mins the step into every
+    rank's flag, later updates freeze, and the single read at the end agrees with the single-GPU
+    stepper's BlowupDetected step; the slab state is rewound to the pre-step state (seismic.cpp:124-129)."""
     m = fw()
     J, lo, hi, gamma, phi = _slab_case()
     tau = 0.2  # far above the explicit scheme's stability limit: sup|u| grows every step from n = 2
