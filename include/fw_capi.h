@@ -74,6 +74,7 @@ typedef struct fw_seis_s* fw_seis;
 typedef struct fw_tsfp2_s* fw_tsfp2;
 typedef struct fw_wave_s* fw_wave;
 typedef struct fw_dense_s* fw_dense;
+typedef struct fw_slab_seis_s* fw_slab_seis;
 
 const char* fw_last_error(void);
 int fw_version(void);
@@ -84,6 +85,8 @@ void fw_ctx_destroy(fw_ctx ctx);
 int fw_ctx_sync(fw_ctx ctx);
 /* the CUDA stream (cudaStream_t) all work of this context is issued on */
 void* fw_ctx_stream(fw_ctx ctx);
+/* the CUDA device index of this context (-1 for a null context) */
+int fw_ctx_device(fw_ctx ctx);
 /* number of kernels this context has launched so far (diagnostics / bench) */
 long long fw_ctx_launches(fw_ctx ctx);
 /* diagnostics: the persistent 2D kernel's watchdog records (needs FW_TRACE=1 at context
@@ -327,6 +330,26 @@ int fw_stage_c2c_scatter(fw_ctx ctx, int dim, const int* J, int axis, int dir, c
                          const double* w_dev, long long src_ts, long long w_ts, int nterms, double scale, int nq,
                          double* const* dst_q, long long blk, long long jstride, long long ostride,
                          long long tstride, long long base);
+
+/* ---- the slab-decomposed SeismicStepper for C / C++ hosts (one process per GPU) ----
+ * SeismicStepper (seismic.hpp:36-46, seismic.cpp:85-142) on a 3D grid whose axis 0 is split over
+ * P <= 8 ranks: rank r owns planes [r J0/P, (r+1) J0/P) and only its slab of both operators'
+ * tables (fw_op_create_slab).  Transposes: the last FFT pass of each stage stores into the owning
+ * rank's buffer (CUDA IPC peer memory over NVLink); the NCCL communicator (fw_nccl_unique_id on
+ * rank 0, the id handed to every rank by the host) exchanges the IPC handles once and is the
+ * stream-ordered barrier between the phases.  gamma, c0, phi, psi are the GLOBAL fields (N
+ * doubles; every rank passes the same arrays).  fw_slab_seis_step(s, k) runs k steps and reads
+ * the blow-up flag once: FW_E_BLOWUP with n = the offending step and the pre-step state, as the
+ * reference's throw (seismic.cpp:124-129).  fw_slab_seis_get returns this rank's planes
+ * ([J0/P][J1][J2]).  FW_E_NCCL when P > 1 and libnccl.so.2 cannot be loaded. */
+int fw_nccl_unique_id(unsigned char id_out[128]);
+int fw_slab_seis_create(fw_ctx ctx, const unsigned char nccl_id[128], int P, int rank, const int* J, const double* lo,
+                        const double* hi, const double* gamma, const double* c0, double omega0, int M,
+                        const double* phi, const double* psi, double tau, double blowup_factor, fw_slab_seis* out);
+void fw_slab_seis_destroy(fw_slab_seis s);
+int fw_slab_seis_step(fw_slab_seis s, int nsteps);
+int fw_slab_seis_get(fw_slab_seis s, double* cur_host, double* prev_host, double* atten_prev_host, long* n);
+int fw_slab_seis_info(fw_slab_seis s, size_t* table_bytes, int* P, int* rank);
 
 #ifdef __cplusplus
 }

@@ -45,6 +45,7 @@ from .api import (  # noqa: F401
     OrderField,
     SeismicMedium,
     SeismicStepper,
+    SlabSeismicStepperC,
     Stepper,
     StepperConfig,
     TSFP2Stepper,
@@ -58,6 +59,7 @@ from .api import (  # noqa: F401
     build_grid,
     build_medium,
     build_slab_expansion,
+    nccl_unique_id,
     default_context,
     DenseOperator,
     apply_constant_order,

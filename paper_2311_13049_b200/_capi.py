@@ -154,6 +154,15 @@ def load_library():
     lib.fw_dense_entries.argtypes = [_vp, _dp]
     lib.fw_apply_toeplitz.argtypes = [_vp, C.c_int, _ip, _dp, _dp, _dp, _dp, _dp]
     lib.fw_truncation_indicator.argtypes = [C.c_int, C.c_double, C.c_double, _dp]
+    lib.fw_ctx_device.argtypes = [_vp]
+    lib.fw_nccl_unique_id.argtypes = [C.c_char_p]
+    lib.fw_slab_seis_create.argtypes = [_vp, C.c_char_p, C.c_int, C.c_int, _ip, _dp, _dp, _dp, _dp, C.c_double,
+                                        C.c_int, _dp, _dp, C.c_double, C.c_double, C.POINTER(_vp)]
+    lib.fw_slab_seis_destroy.argtypes = [_vp]
+    lib.fw_slab_seis_destroy.restype = None
+    lib.fw_slab_seis_step.argtypes = [_vp, C.c_int]
+    lib.fw_slab_seis_get.argtypes = [_vp, _dp, _dp, _dp, C.POINTER(C.c_long)]
+    lib.fw_slab_seis_info.argtypes = [_vp, C.POINTER(C.c_size_t), C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.fw_op_create_slab.argtypes = [_vp, _ip, _dp, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
     lib.fw_ipc_alloc.argtypes = [_vp, C.c_size_t, C.POINTER(_vp)]
     lib.fw_ipc_free.argtypes = [_vp, _vp]
@@ -216,5 +225,6 @@ EXPORTED_SYMBOLS = [
     "fw_wave_get", "fw_rfftn", "fw_irfftn", "fw_op_path", "fw_ricker_initial", "fw_grid_dft", "fw_grid_dft_device",
     "fw_grid_forward", "fw_grid_inverse", "fw_apply_constant_order", "fw_apply_constant_order_spectrum",
     "fw_dense_create", "fw_dense_destroy", "fw_dense_apply", "fw_dense_entries", "fw_apply_toeplitz",
-    "fw_truncation_indicator", "fw_op_create_slab", "fw_stage_seis_update_peers", "fw_ipc_alloc", "fw_ipc_free",
+    "fw_truncation_indicator", "fw_ctx_device", "fw_nccl_unique_id", "fw_slab_seis_create", "fw_slab_seis_destroy",
+    "fw_slab_seis_step", "fw_slab_seis_get", "fw_slab_seis_info", "fw_op_create_slab", "fw_stage_seis_update_peers", "fw_ipc_alloc", "fw_ipc_free",
 ]

@@ -235,6 +235,67 @@ def build_slab_expansion(order: OrderField, M: int, P: int, rank: int,
     return op
 
 
+def nccl_unique_id() -> bytes:
+    """An NCCL unique id for SlabSeismicStepperC (made on rank 0, handed to every rank by the host)."""
+    buf = C.create_string_buffer(128)
+    check(load_library().fw_nccl_unique_id(buf))
+    return buf.raw
+
+
+class SlabSeismicStepperC:
+    """The slab-decomposed SeismicStepper of the C-ABI (fw_slab_seis_*: the stepping logic in C++,
+    one process per GPU, NCCL-bootstrapped IPC transposes, stream-ordered barriers) -- what a C/C++
+    host of the reference drives; gamma, c0, phi, psi are the GLOBAL fields."""
+
+    def __init__(self, grid: Grid, gamma, c0, omega0: float, M: int, phi, psi, tau: float, P: int = 1,
+                 rank: int = 0, nccl_id: Optional[bytes] = None, blowup_factor: float = 1e8,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.grid, self.P, self.rank = grid, int(P), int(rank)
+        N = grid.total()
+        J, lo, hi = grid._carrays()
+        self._keep = [_f64(a, N) for a in (gamma, c0, phi, psi)]
+        h = C.c_void_p()
+        check(load_library().fw_slab_seis_create(self.ctx.handle, nccl_id, int(P), int(rank), J, lo, hi,
+                                                 *[_ptr(a) for a in self._keep[:2]], float(omega0), int(M),
+                                                 *[_ptr(a) for a in self._keep[2:]], float(tau),
+                                                 float(blowup_factor), C.byref(h)))
+        self._h = h
+        self.slab_shape = (grid.sizes[0] // self.P,) + tuple(grid.sizes[1:])
+
+    def advance(self, steps: int):
+        check(load_library().fw_slab_seis_step(self._h, int(steps)))
+
+    def step(self):
+        self.advance(1)
+
+    def state(self):
+        """(cur, prev, L2prev) of this rank's planes and n."""
+        cur, prev, ap = (np.empty(self.slab_shape) for _ in range(3))
+        n = C.c_long(0)
+        check(load_library().fw_slab_seis_get(self._h, _ptr(cur), _ptr(prev), _ptr(ap), C.byref(n)))
+        return cur, prev, ap, n.value
+
+    def n(self) -> int:
+        n = C.c_long(0)
+        check(load_library().fw_slab_seis_get(self._h, None, None, None, C.byref(n)))
+        return n.value
+
+    @property
+    def table_bytes(self) -> int:
+        b = C.c_size_t(0)
+        check(load_library().fw_slab_seis_info(self._h, C.byref(b), None, None))
+        return b.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().fw_slab_seis_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
 def _check_field(op: ExpansionOperator, u):
     if hasattr(u, "grid") and not u.grid.same_as(op.grid):
         raise GridMismatch("field defined on a different grid than the operator")

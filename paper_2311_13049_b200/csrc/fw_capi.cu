@@ -375,6 +375,10 @@ int fw_ctx_sync(fw_ctx c) {
 }
 
 void* fw_ctx_stream(fw_ctx c) { return c ? (void*)c->stream : nullptr; }
+int fw_ctx_device(fw_ctx c) { return c ? c->device : -1; }
+
+// the thread-local error of the C-ABI, for the library's other translation units (fw_slab.cu)
+int fw_internal_set_error(int code, const char* msg) { return set_err(code, msg ? msg : ""); }
 
 /* diagnostics: the persistent kernel's watchdog records (kTraceWords u64: per CTA 8 words = site, thread,
    counter value seen, target, term, globaltimer), readable even after the kernel trapped; FW_E_ARG if

@@ -74,6 +74,17 @@ def test_cpp_gpu_seismic_stepper(tmp_path):
 
 
 @pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(os.path.join(BUILD, "slab_seis_check")), reason="drop-in not built")
+def test_cpp_slab_stepper(tmp_path):
+    """A C++ host of the reference drives the slab-decomposed stepper of the C-ABI (fw_slab_seis_*)
+    on a 3D grid (P = 1 on this one-GPU run; FW_WORLD / FW_RANK / FW_NCCL_ID_FILE select P > 1)
+    against the reference's own SeismicStepper."""
+    r = subprocess.run([os.path.join(BUILD, "slab_seis_check")], cwd=tmp_path, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "[PASS]" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
 @pytest.mark.skipif(not os.path.exists(os.path.join(BUILD, "stepper_gpu_check")), reason="drop-in not built")
 def test_cpp_gpu_stepper(tmp_path):
     """fwave::gpu::Stepper (reference Stepper API; LFFP / CNFP / TSFP2 on the device)

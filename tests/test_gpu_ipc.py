@@ -143,3 +143,40 @@ def test_ipc_slab_two_processes_blowup():
     cur_r, prev_r, ap_r, _ = ref.state()
     for i, want in zip((4, 5, 6), (cur_r, prev_r, ap_r)):
         assert np.array_equal(np.concatenate([r[i] for r in res]), want)
+
+
+@pytest.mark.parametrize("blowup", [False, True])
+def test_c_abi_slab_stepper_p1_vs_single_gpu(blowup):
+    """The C++ slab stepper of the C-ABI (fw_slab_seis_*; P = 1 on this one-GPU run: the same stage,
+    scatter, update and flag code as P > 1, the transposes into the own buffers): bitwise equal to
+    the single-GPU SeismicStepper, including a blow-up rewind."""
+    import paper_2311_13049_b200 as fw
+
+    J, lo, hi, gamma, phi = _case()
+    g = fw.Grid(list(zip(lo, hi)), list(J))
+    tau, factor, steps = (1e-3, 1e8, 5) if not blowup else (0.2, 1.0, 6)
+    if blowup:  # threshold between the sups of steps 4 and 5 (see the IPC blow-up test)
+        probe = fw.SeismicStepper(fw.build_medium(g, gamma, np.ones(J), 1.0, 6), phi, np.zeros(J), tau,
+                                  blowup_factor=1e300)
+        sups = []
+        for _ in range(4):
+            probe.step()
+            sups.append(np.abs(probe.current()).max())
+        factor = np.sqrt(max(max(sups[:3]), 1.0) * sups[3]) / np.abs(phi).max()
+    ref = fw.SeismicStepper(fw.build_medium(g, gamma, np.ones(J), 1.0, 6), phi, np.zeros(J), tau, blowup_factor=factor)
+    st = fw.SlabSeismicStepperC(g, gamma, np.ones(J), 1.0, 6, phi, np.zeros(J), tau, blowup_factor=factor)
+    e1 = e2 = None
+    try:
+        ref.advance(steps)
+    except fw.BlowupDetected as e:
+        e1 = e
+    try:
+        st.advance(steps)
+    except fw.BlowupDetected as e:
+        e2 = e
+    assert (e1 is None) == (e2 is None) == (not blowup)
+    cur, prev, ap, n = st.state()
+    rcur, rprev, rap, rn = ref.state()
+    assert n == rn
+    assert np.array_equal(cur, rcur) and np.array_equal(prev, rprev) and np.array_equal(ap, rap)
+    assert st.table_bytes > 0
