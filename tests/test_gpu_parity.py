@@ -745,3 +745,29 @@ def test_time_multiplexed_step2d_variant_bitwise():
     st_t.advance(5)
     for a, b in zip(st_d.state(), st_t.state()):
         assert np.array_equal(a, b)
+
+
+def test_persistent_kernel_repeatable_race_probe():
+    """compute-sanitizer is closed on this GPU pool, so the persistent kernel's cross-CTA protocol
+    (counters, mbarriers, TMA tiles; fw_step2d.cu) is probed by repetition instead: 24 applies of the
+    C2 operator and two 60-step seismic runs must reproduce the same bits every time (a missed
+    acquire/release or an early tile read would show up as run-to-run differences; the reference's
+    determinism contract is flap.cpp:82-90)."""
+    m = fw()
+    cfg = cfgs.c2()
+    g = grid_of(cfg.J, cfg.lo, cfg.hi)
+    op = m.build_expansion(m.OrderField(g, 1.0 + cfg.gamma), cfg.M)
+    assert op.persistent
+    rng = np.random.default_rng(11)
+    u = rng.standard_normal(cfg.J)
+    first = op.apply(u)
+    for _ in range(23):
+        assert np.array_equal(op.apply(u), first)
+    med = m.build_medium(g, cfg.gamma, cfg.c0, cfg.omega0, cfg.M)
+    runs = []
+    for _ in range(2):
+        st = m.SeismicStepper(med, cfg.phi, cfg.psi, cfg.tau)
+        st.advance(60)
+        runs.append(st.state())
+    for a, b in zip(runs[0], runs[1]):
+        assert np.array_equal(a, b)
