@@ -337,7 +337,7 @@ int fw_ctx_create(int device, fw_ctx* out) {
   FW_CUDA(cudaMemset(c->counters, 0, 2 * (size_t)fw::kStep2dCStride * sizeof(unsigned long long)));
   const char* tr = getenv("FW_TRACE");
   if (tr && tr[0] == '1') {
-    const size_t n = (size_t)fw::kTraceWords;
+    const size_t n = (size_t)fw::kTraceAlloc;
     if (cudaHostAlloc((void**)&c->trace_host, n * sizeof(unsigned long long), cudaHostAllocMapped) == cudaSuccess) {
       memset(c->trace_host, 0, n * sizeof(unsigned long long));
       if (cudaHostGetDevicePointer((void**)&c->trace, c->trace_host, 0) != cudaSuccess) c->trace = nullptr;

@@ -9,6 +9,10 @@ namespace fw {
 constexpr int kStep2dMaxTerms = 2 * 65;                 // nops <= 2, M <= 64
 constexpr int kStep2dCStride = 1 + 2 * kStep2dMaxTerms;  // counters per set
 constexpr int kTraceWords = 1024 * 16;                  // watchdog records: 2 x 8 words per CTA
+// the mapped buffer also holds the warp-specialised kernel's phase timestamps of a
+// -DFW_STEP2D_TRACE=1 build (2 x 32 x 136 x 8 + 2 x 160 x 2 x 136 words)
+constexpr int kTraceAlloc = 2 * 32 * 136 * 8 + 2 * 160 * 2 * 136 > kTraceWords ? 2 * 32 * 136 * 8 + 2 * 160 * 2 * 136
+                                                                                : kTraceWords;
 
 struct Step2DParams {
   int J0, J1;
