@@ -356,6 +356,7 @@ class SlabSeismicStepper:
                    for _ in range(3)]
         self.ab = [torch.empty_like(self.ub[0]) for _ in range(2)]
         self.phi_l, self.psi_l = self._dev(phi[rows]), self._dev(psi[rows])
+        torch.cuda.synchronize()  # the uploads ran on torch's stream; the stepper works on the context's
         if construct:  # seismic.cpp:85-109 (one process per rank)
             self.start(self.apps[0].apply(self.phi_l), self.apps[1].apply(self.psi_l), self.apps[1].apply(self.phi_l))
 
@@ -425,7 +426,8 @@ class SlabSeismicStepper:
         self.lvl -= self.n - bad + 1  # the levels before the offending step (later updates were frozen)
         self.n = bad
         self.peers.barrier()  # every rank has read the flag before any resets it
-        self.flag.fill_(0x7FFFFFFF)
+        with self.torch.cuda.stream(self.stages.stream):  # ordered with the context's kernels
+            self.flag.fill_(0x7FFFFFFF)
         self.ctx.sync()
         raise BlowupDetected(f"sup|u| > {self.thr:g} at step {bad}")
 
@@ -466,6 +468,7 @@ class LocalPeers:
         self.T_ptrs = [t.data_ptr() for t in self._T]
         self.Ts_ptrs = [t.data_ptr() for t in self._Ts]
         self.flag_ptrs = [f.data_ptr() for f in self._flags]
+        torch.cuda.synchronize()  # torch filled the flags on its stream; the context's kernels use its own
 
     def T(self, r):
         return self._T[r]
@@ -509,6 +512,7 @@ class IpcPeers(LocalPeers):
             self._alloc.append(ptr.value)
             self._own[key] = torch.as_tensor(_CAI(ptr.value, shape, typestr), device="cuda")
         self._own["flag"].fill_(0x7FFFFFFF)
+        torch.cuda.synchronize()  # the fill ran on torch's stream, the context's kernels run on its own
         handles = []
         for key in ("T", "Ts", "flag"):
             hbuf = C.create_string_buffer(64)
