@@ -176,6 +176,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef FW_S2D_TWTM
 #define FW_S2D_TWTM 1
 #endif
+// warp roles: the SM's schedulers issue from the highest eligible warp id first, so the column
+// warps (the per-term critical path) take warps 16-23 and the row warps 0-15 (0: the round-1
+// layout, column warps 0-7, row warps 8-23; A/B)
+#ifndef FW_S2D_COLHI
+#define FW_S2D_COLHI 1
+#endif
+constexpr int kColW0 = FW_S2D_COLHI ? 16 : 0;  // first column warp
+constexpr int kRowW0 = FW_S2D_COLHI ? 0 : 8;   // first row warp
 // L2 promotion of the tile TMA loads (A/B)
 #ifndef FW_S2D_L2PROMO
 #define FW_S2D_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_NONE  // measured 0.2 % faster than L2_256B
@@ -654,10 +662,10 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
   const int nterms = M + 1 - prm.m_first;
   const int ntot = prm.nops * nterms;
 
-  if (warp < 8) {
+  if (warp >= kColW0 && warp < kColW0 + 8) {
     // ============================================ column warps (2 groups of 4)
     setmaxnreg_inc<112>();
-    const int g = warp >> 2;   // group
+    const int g = (warp - kColW0) >> 2;  // group
     const int cg = tid & 127;  // thread within the group
     const int slot = b + g * nblk;
     const int mbr = cg / CT0, i0 = cg % CT0;
@@ -740,7 +748,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         // per-thread constants re-derived from the special registers each term (volatile reads
         // are not hoisted): fewer live registers across the FFT passes
         const int tidc = (int)vtid();
-        const int g_ = tidc >> 7, cg_ = tidc & 127;
+        const int g_ = (tidc >> 7) - kColW0 / 4, cg_ = tidc & 127;
         const int slot_ = (int)vctaid() + g_ * nblk;
         const int i0_ = cg_ % CT0;
         const int kA_ = slot_ == 0 ? 0 : slot_;
@@ -827,7 +835,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
   } else {
     // ============================================ row warps (8 pairs)
     setmaxnreg_dec<64>();
-    const int rw = warp - 8;
+    const int rw = warp - kRowW0;
     const int pair = rw >> 1;
     const int l = (rw & 1) * 32 + lane;  // lane within the pair = butterfly index
     const int r0 = (int)(((long long)b * J0) / nblk);
@@ -942,7 +950,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       // per-thread constants re-derived from the special registers each term (volatile reads
       // are not hoisted): cheaper than keeping them live, the row warps run at 64 registers
       const int tidr = (int)vtid();
-      const int rw_ = (tidr >> 5) - 8, pair_ = rw_ >> 1, l_ = (rw_ & 1) * 32 + (tidr & 31);
+      const int rw_ = (tidr >> 5) - kRowW0, pair_ = rw_ >> 1, l_ = (rw_ & 1) * 32 + (tidr & 31);
       const int row_ = (int)(((long long)vctaid() * J0) / nblk) + pair_;
       double2* work_ = sm + G::OFF_RW + (size_t)pair_ * G::LROW;
       const unsigned tacc_ = tmem_base + ((unsigned)(32 * ((tidr >> 5) & 3)) << 16) + 32u * (unsigned)(rw_ >> 2);
