@@ -61,6 +61,14 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
 __device__ __forceinline__ void red_relaxed_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -181,6 +189,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // layout, column warps 0-7, row warps 8-23; A/B)
 #ifndef FW_S2D_COLHI
 #define FW_S2D_COLHI 1
+#endif
+// publication of a term's Z columns (red.release.gpu on the term counter): by a publisher lane
+// in an otherwise idle row warp, told through a monotone shared-memory counter per column group,
+// so that the release fence's drain of the Z stores is off the column warps' critical path
+// (0: the column group's first thread publishes term t-1 after pass 0 of term t; A/B)
+#ifndef FW_S2D_PUBLISHER
+#define FW_S2D_PUBLISHER 1
 #endif
 constexpr int kColW0 = FW_S2D_COLHI ? 16 : 0;  // first column warp
 constexpr int kRowW0 = FW_S2D_COLHI ? 0 : 8;   // first row warp
@@ -367,7 +382,7 @@ struct Geo {
   static_assert(npass(J0) == 3 && npass(h) == 3, "3-pass plans");
   static_assert(RR0 == 8 && RR1 == 8 && RR2 == 8 && RT == 64, "row pair: one radix-8 butterfly per lane");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
-  static_assert(RMAX < 8, "one row pair is the tile producer");
+  static_assert(RMAX < 8, "one row pair is the tile producer and the publisher");
   static_assert(h % 256 == 0, "whole TMA boxes");
 
   // column layouts: pass-1 input (i, r) = logical i + CT1 r lives at i CR1 + r
@@ -602,6 +617,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
   extern __shared__ __align__(16) double2 sm[];
   __shared__ unsigned tmem_base_sh;
   __shared__ __align__(8) unsigned long long tile_full, tile_empty;  // row tile pipeline (TMA producer)
+  __shared__ unsigned zdone[2];  // FW_S2D_PUBLISHER: terms of the launch whose Z stores group g has issued
   double2* twc = sm;
   double2* twr = sm + G::OFF_TWR;
   double2* twp = sm + G::OFF_TWP;
@@ -640,6 +656,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
     fill(twr, twoff(h, 2), pprod(h, 2), radix(h, 2));
     for (int e = tid; e <= h; e += NT) twp[e] = prm.master[e * (kTwMaster / J1)];
   }
+  if (tid < 2) zdone[tid] = 0u;
   if (tid == 0) {
     const int nr0 = (int)(((long long)(b + 1) * J0) / nblk) - (int)(((long long)b * J0) / nblk);
     mbar_init(&tile_full, 1);
@@ -797,12 +814,21 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         if (FW_DBG(8)) Z = prm.T + (size_t)(KRING - 1) * J0 * h;  // all terms into one slot
         if (FW_DBG(32)) {  // timing experiment: columns skip the FFT
           gb_();
-          if (cg_ == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz_);
+          if (FW_S2D_PUBLISHER) {
+            if (cg_ == 0) st_release_cta_u32(&zdone[g_], (unsigned)gt + 1u);
+          } else if (cg_ == 0 && t > 0) {
+            red_release_add(&cC[t - 1], (unsigned long long)nz_);
+          }
           continue;
         }
         const unsigned ttw_ = tmem_base + ((unsigned)(32 * ((tidc >> 5) & 3)) << 16) + (unsigned)(G::TM_TWC + g_ * 56);
         column_pair<G, +1>(work_, twc, ttw_, cg_, a, gb_, [&] {
-          if (cg_ == 0 && t > 0) red_release_add(&cC[t - 1], (unsigned long long)nz_);
+          if (!FW_S2D_PUBLISHER && cg_ == 0 && t > 0) {
+            if (FW_DBG(64))
+              red_relaxed_add(&cC[t - 1], (unsigned long long)nz_);  // timing: publication without the fence
+            else
+              red_release_add(&cC[t - 1], (unsigned long long)nz_);
+          }
         }, [&](int i, const double2* xa, const double2* xb) {
 #pragma unroll
           for (int r = 0; r < G::CR2; ++r) {
@@ -820,13 +846,14 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         }, [&](int sl) { FW_TRACE(t, sl); });
         FW_TRACE(t, 5);
         gb_();  // work_ buffers free again; all Z stores of the group issued
+        if (FW_S2D_PUBLISHER && cg_ == 0) st_release_cta_u32(&zdone[g_], (unsigned)gt + 1u);  // -> publisher
         FW_TRACE(t, 6);
 #if FW_STEP2D_TRACE
         if (prm.trace && cg_ == 0 && vctaid() < 160)
           prm.trace[2 * 32 * 136 * 8 + ((size_t)vctaid() * 2 + g_) * 136 + t] = gtimer();
 #endif
       }
-      if (cg == 0 && ntot > 0) red_release_add(&cC[ntot - 1], (unsigned long long)nz);
+      if (!FW_S2D_PUBLISHER && cg == 0 && ntot > 0) red_release_add(&cC[ntot - 1], (unsigned long long)nz);
       }  // steps
       if (prm.residue && rmax > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(prm.residue),
@@ -899,6 +926,30 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           mbar_wait(&tile_empty, (unsigned)(gtot - 1) & 1u);
           red_relaxed_add(&cR[ntot - 1], (unsigned long long)nr);
         }
+      }
+    }
+
+    if (FW_S2D_PUBLISHER && rw == 2 * RMAX + 1 && lane == 0) {
+      // ---- publisher (one lane of the other idle warp): term gt's Z columns of this CTA are
+      // stored once every active column group has counted it in zdone (st.release.cta after the
+      // group barrier that follows its Z stores); one red.release.gpu makes them visible to every
+      // tile producer (cumulative over the group's stores: they precede the release in causality order)
+      int ng = 0;
+      unsigned long long nzs = 0;
+      for (int g = 0; g < 2; ++g) {
+        const int sl = b + g * nblk;
+        if (sl >= G::NSLOT) continue;
+        ++ng;
+        const int kA = sl == 0 ? 0 : sl;
+        const int kB = sl == 0 ? h : (sl == h / 2 ? -1 : h - sl);
+        nzs += (unsigned long long)((kA < h) + (kB >= 0 && kB < h));
+      }
+      const int gtot = prm.nsteps * ntot;
+      for (int gt = 0; gt < gtot; ++gt) {
+        for (int g = 0; g < ng; ++g)
+          while (ld_acquire_cta_u32(&zdone[g]) <= (unsigned)gt) {
+          }
+        red_release_add(&cC[gt % ntot], nzs);
       }
     }
 
