@@ -197,6 +197,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef FW_S2D_PUBLISHER
 #define FW_S2D_PUBLISHER 1
 #endif
+// ring-slot wait (Z[gt % KRING] consumed everywhere) by the group's first thread only, its
+// acquire load overlapping the weight loads (the group barrier after pass 0 orders the other
+// threads' Z stores after it); 0: every column warp waits after the weights (A/B)
+#ifndef FW_S2D_RING1
+#define FW_S2D_RING1 1
+#endif
 constexpr int kColW0 = FW_S2D_COLHI ? 16 : 0;  // first column warp
 constexpr int kRowW0 = FW_S2D_COLHI ? 0 : 8;   // first row warp
 // L2 promotion of the tile TMA loads (A/B)
@@ -785,11 +791,14 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           if (kB_ >= 0) prefetch_l2_hint(prm.w[op1] + ((size_t)m1 * prm.wcols + kB_) * J0, J0 * sizeof(double), pf);
         }
         double2 a[CR0];
+        const int gt = s * ntot + t;  // term index over the launch
         {
           double wk[CR0];  // all weight loads in flight before the first use (one L2 latency)
 #pragma unroll
           for (int r = 0; r < CR0; ++r)
             wk[r] = (mycol_ >= 0 && !FW_DBG(2)) ? ld_stream(&w[r * CT0], pol_evict_first()) : 0.5;
+          if (FW_S2D_RING1 && cg_ == 0 && gt >= KRING && !FW_DBG(128))
+            spin_until(&cR[(gt - KRING) % ntot], (unsigned long long)((gt - KRING) / ntot + 1) * J0);
 #pragma unroll
           for (int c = 0; c < 4 * CR0; c += 32) {
             unsigned v[32];
@@ -801,8 +810,8 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           }
         }
         FW_TRACE(t, 1);
-        const int gt = s * ntot + t;  // term index over the launch
-        if (gt >= KRING) warp_wait(&cR[(gt - KRING) % ntot], (unsigned long long)((gt - KRING) / ntot + 1) * J0);
+        if (!FW_S2D_RING1 && gt >= KRING && !FW_DBG(128))  // (128: timing experiment without the ring wait)
+          warp_wait(&cR[(gt - KRING) % ntot], (unsigned long long)((gt - KRING) / ntot + 1) * J0);
         FW_TRACE(t, 2);
 #if FW_STEP2D_TRACE
         if (prm.trace && cg_ == 0 && vctaid() < 160)
