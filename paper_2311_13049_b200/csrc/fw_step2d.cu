@@ -314,6 +314,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(b))
                : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* b,
+                                              unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_test(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
@@ -363,12 +380,11 @@ struct Geo {
   static constexpr int RLT = ilog2c(RT);
   static constexpr int LCOL = J0 + (J0 >> CL1) + (J0 >> CLT) + 1;  // per column work buffer
   static constexpr int LROW = (h + (h >> RLT)) | 1;                // per row work buffer (odd)
-  static constexpr int TWC = twtotal(J0);
-  static constexpr int TWR = twtotal(h);
-  static constexpr int TWP = h + 1;
-  static constexpr size_t OFF_TWR = TWC;
-  static constexpr size_t OFF_TWP = TWC + TWR;
-  static constexpr size_t OFF_CW = TWC + TWR + TWP;                // column work [2 groups][2 members][LCOL]
+  // the current term's weights of the CTA's columns, landed by bulk copy: [2 groups][2 members][J0]
+  // doubles; then the C2R pre-processing twiddles of each group's pair (W_J1^kA, W_J1^kB)
+  static constexpr size_t OFF_W = 0;
+  static constexpr size_t OFF_TWQ = OFF_W + (size_t)2 * J0;
+  static constexpr size_t OFF_CW = OFF_TWQ + 8;                    // column work [2 groups][2 members][LCOL]
   static constexpr size_t OFF_RW = OFF_CW + (size_t)4 * LCOL;      // row work [RMAX][LROW]
   // next term's 8 rows of Z: two TMA boxes [256 k][8 rows] (128-B swizzled), 1 KB aligned at run time
   static constexpr size_t OFF_TILE = OFF_RW + (size_t)RMAX * LROW;
@@ -381,13 +397,17 @@ struct Geo {
   // twiddles (4 warps x 28), per lane quadrant
   static constexpr int TM_TWC = 256;
   static constexpr int TM_TWR = 368;
-  static constexpr int TM_COLS = FW_S2D_TWTM ? 512 : 256;
-  static_assert(TM_U + 2 * 4 * CR0 <= 256 && TM_TWR + 4 * 28 <= 512, "tensor memory budget");
+  // [480, 508) row pass-1 twiddles: lane (32 q + j) holds the set of butterfly index j & 7 (all
+  // row warps of quadrant q read it)
+  static constexpr int TM_TWR1 = 480;
+  static constexpr int TM_COLS = 512;
+  static_assert(FW_S2D_TWTM && FW_S2D_PUBLISHER, "twiddles in tensor memory; the publisher lane loads the weights");
+  static_assert(TM_U + 2 * 4 * CR0 <= 256 && TM_TWR + 4 * 28 <= TM_TWR1 && TM_TWR1 + 28 <= 512, "tensor memory budget");
   static_assert(CR1 == 8 && CR2 == 8, "radix-8 column passes 1-2");
   static_assert(2 * CT0 == 128, "column pass 0: one butterfly per group thread");
   static_assert(npass(J0) == 3 && npass(h) == 3, "3-pass plans");
   static_assert(RR0 == 8 && RR1 == 8 && RR2 == 8 && RT == 64, "row pair: one radix-8 butterfly per lane");
-  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(SMEM + 128 <= 227 * 1024, "shared memory budget (with the static barriers)");
   static_assert(RMAX < 8, "one row pair is the tile producer and the publisher");
   static_assert(h % 256 == 0, "whole TMA boxes");
 
@@ -475,6 +495,14 @@ __device__ __forceinline__ void tw_park(unsigned taddr, const double2* t) {
   tmem_st8_nw(taddr + 16, v + 16);
   tmem_st4_nw(taddr + 24, v + 24);
   tmem_wait_st();
+}
+// the same from the master table: the 7 twiddles of butterfly index k of a radix-8 pass with
+// p = pprod (entries r k (kTwMaster / (8 p)), r = 1..7 = the per-pass table of butterfly())
+__device__ __forceinline__ void tw_park_master(unsigned taddr, const double2* master, int k, int p) {
+  double2 t[7];
+#pragma unroll
+  for (int r = 0; r < 7; ++r) t[r] = __ldg(&master[((r + 1) * k) * (kTwMaster / (8 * p))]);
+  tw_park(taddr, t);
 }
 template <int DIR>
 __device__ __forceinline__ void tw_load(unsigned taddr, double2 (&w)[7]) {
@@ -592,8 +620,7 @@ __device__ __forceinline__ void column_pair(double2* work, const double2* tw, un
 // passes 0 and 1 in place (pass-0 input in natural order, padded); returns after the
 // pair barrier that follows pass 1.  Lane l (0..63) owns butterfly l of every pass.
 template <class G, int DIR>
-__device__ __forceinline__ void row_passes01(double2* work, const double2* tw, int l, int pair) {
-  constexpr int h = G::h;
+__device__ __forceinline__ void row_passes01(double2* work, unsigned ttw1, int l, int pair) {
   {
     double2 a[8];
 #pragma unroll
@@ -607,7 +634,7 @@ __device__ __forceinline__ void row_passes01(double2* work, const double2* tw, i
     double2 a[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) a[r] = work[G::r_p1in(l) + r * G::RS1];
-    butterfly<h, 1, DIR>(a, l, tw);
+    butterfly_tm8_lean<DIR>(a, ttw1);
 #pragma unroll
     for (int r = 0; r < 8; ++r) work[G::r_p1in(l) + r * G::RS1] = a[r];
   }
@@ -623,10 +650,10 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
   extern __shared__ __align__(16) double2 sm[];
   __shared__ unsigned tmem_base_sh;
   __shared__ __align__(8) unsigned long long tile_full, tile_empty;  // row tile pipeline (TMA producer)
-  __shared__ unsigned zdone[2];  // FW_S2D_PUBLISHER: terms of the launch whose Z stores group g has issued
-  double2* twc = sm;
-  double2* twr = sm + G::OFF_TWR;
-  double2* twp = sm + G::OFF_TWP;
+  __shared__ unsigned zdone[2];  // terms of the launch whose Z stores group g has issued (-> publisher)
+  __shared__ unsigned ringok;    // terms of the launch whose ring slot is free (<- loader)
+  __shared__ __align__(8) unsigned long long wfull[2], wempty[2];  // weights of group g (bulk copy)
+  double2* twq = sm + G::OFF_TWQ;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.x;
@@ -648,22 +675,22 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
   unsigned long long* cC = cnt + 1;                      // Z columns of term t stored
   unsigned long long* cR = cnt + 1 + prm.nterms_total;  // rows of Z[t] consumed
 
-  {  // twiddle tables (values = master entries, identical to fw_fft.cuh's twiddle())
-    auto fill = [&](double2* dst, int off, int p, int R) {
-      const int n = p * (R - 1);
-      for (int e = tid; e < n; e += NT) {
-        const int k = e / (R - 1), r = e % (R - 1) + 1;
-        dst[off + e] = prm.master[(r * k) * (kTwMaster / (p * R))];
-      }
-    };
-    fill(twc, twoff(J0, 1), pprod(J0, 1), radix(J0, 1));
-    fill(twc, twoff(J0, 2), pprod(J0, 2), radix(J0, 2));
-    fill(twr, twoff(h, 1), pprod(h, 1), radix(h, 1));
-    fill(twr, twoff(h, 2), pprod(h, 2), radix(h, 2));
-    for (int e = tid; e <= h; e += NT) twp[e] = prm.master[e * (kTwMaster / J1)];
+  // FFT twiddles live in tensor memory (parked below, values = the master entries, identical to
+  // fw_fft.cuh's twiddle()); shared memory keeps only the pre-processing twiddles of the pairs
+  if (tid < 2) {
+    const int sl = b + tid * nblk;
+    const int kA = sl == 0 ? 0 : sl;
+    const int kB = sl == 0 ? h : h - sl;
+    twq[2 * tid] = sl < G::NSLOT ? prm.master[kA * (kTwMaster / J1)] : make_double2(0.0, 0.0);
+    twq[2 * tid + 1] = sl < G::NSLOT ? prm.master[kB * (kTwMaster / J1)] : make_double2(0.0, 0.0);
+    zdone[tid] = 0u;
   }
-  if (tid < 2) zdone[tid] = 0u;
   if (tid == 0) {
+    ringok = (unsigned)KRING;
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&wfull[g], 1);
+      mbar_init(&wempty[g], 4);  // one arrive per column warp of the group
+    }
     const int nr0 = (int)(((long long)(b + 1) * J0) / nblk) - (int)(((long long)b * J0) / nblk);
     mbar_init(&tile_full, 1);
     mbar_init(&tile_empty, 2 * nr0);  // one arrive per consumer warp
@@ -680,6 +707,12 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const unsigned tmem_base = tmem_base_sh;
+  if (warp >= kRowW0 && warp < kRowW0 + 4)  // one row warp per lane quadrant: row pass-1 twiddles
+    tw_park_master(tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)G::TM_TWR1, prm.master,
+                   lane & (pprod(h, 1) - 1), pprod(h, 1));
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   const int M = prm.M;
   const int nterms = M + 1 - prm.m_first;
@@ -710,10 +743,8 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       const unsigned tu = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_U + g * 4 * CR0);
       // this thread's pass-1 / pass-2 twiddles (butterfly index cg in both passes) -> TMEM
       const unsigned ttw = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_TWC + g * 56);
-      if (FW_S2D_TWTM) {
-        tw_park(ttw, twc + twoff(J0, 1) + (cg & (pprod(J0, 1) - 1)) * 7);
-        tw_park(ttw + 28, twc + twoff(J0, 2) + (cg & (pprod(J0, 2) - 1)) * 7);
-      }
+      tw_park_master(ttw, prm.master, cg & (pprod(J0, 1) - 1), pprod(J0, 1));
+      tw_park_master(ttw + 28, prm.master, cg & (pprod(J0, 2) - 1), pprod(J0, 2));
 
       double rmax = 0.0;
 #pragma unroll 1
@@ -731,7 +762,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         double2 x0[G::CR2], x1[G::CR2];
         int ix = 0;
         column_pair<G, -1>(
-            work, twc, ttw, cg, a, gb, [] {},
+            work, nullptr, ttw, cg, a, gb, [] {},
             [&](int i, const double2* c0, const double2* c1) {
               ix = i;
 #pragma unroll
@@ -783,22 +814,19 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         auto gb_ = [g_] { groupbar(g_); };
         FW_TRACE(t, 0);
         const int op = t / nterms, m = prm.m_first + t % nterms;
-        const double* w = prm.w[op] + ((size_t)m * prm.wcols + (mycol_ >= 0 ? mycol_ : 0)) * J0 + i0_;
-        if (cg_ == 0 && t + 1 < ntot) {  // the next term's weights of both columns -> L2
-          const int op1 = (t + 1) / nterms, m1 = prm.m_first + (t + 1) % nterms;
-          const unsigned long long pf = pol_evict_first();
-          if (kA_ >= 0) prefetch_l2_hint(prm.w[op1] + ((size_t)m1 * prm.wcols + kA_) * J0, J0 * sizeof(double), pf);
-          if (kB_ >= 0) prefetch_l2_hint(prm.w[op1] + ((size_t)m1 * prm.wcols + kB_) * J0, J0 * sizeof(double), pf);
-        }
+        (void)op;
+        (void)m;
         double2 a[CR0];
         const int gt = s * ntot + t;  // term index over the launch
         {
-          double wk[CR0];  // all weight loads in flight before the first use (one L2 latency)
+          // this term's weights of the group's columns, landed in shared memory by the loader lane
+          mbar_wait(&wfull[g_], (unsigned)gt & 1u);
+          const double* ws = reinterpret_cast<const double*>(sm + G::OFF_W) + (size_t)(2 * g_ + cg_ / CT0) * J0 + i0_;
+          double wk[CR0];
 #pragma unroll
-          for (int r = 0; r < CR0; ++r)
-            wk[r] = (mycol_ >= 0 && !FW_DBG(2)) ? ld_stream(&w[r * CT0], pol_evict_first()) : 0.5;
-          if (FW_S2D_RING1 && cg_ == 0 && gt >= KRING && !FW_DBG(128))
-            spin_until(&cR[(gt - KRING) % ntot], (unsigned long long)((gt - KRING) / ntot + 1) * J0);
+          for (int r = 0; r < CR0; ++r) wk[r] = (mycol_ >= 0 && !FW_DBG(2)) ? ws[r * CT0] : 0.5;
+          __syncwarp();
+          if ((tidc & 31) == 0) mbar_arrive(&wempty[g_]);  // the buffer may take the next term's weights
 #pragma unroll
           for (int c = 0; c < 4 * CR0; c += 32) {
             unsigned v[32];
@@ -810,8 +838,12 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           }
         }
         FW_TRACE(t, 1);
-        if (!FW_S2D_RING1 && gt >= KRING && !FW_DBG(128))  // (128: timing experiment without the ring wait)
-          warp_wait(&cR[(gt - KRING) % ntot], (unsigned long long)((gt - KRING) / ntot + 1) * J0);
+        // ring slot gt % KRING free (rows of term gt - KRING consumed everywhere; the loader lane
+        // polls the global counter): the group's first thread, ordered before every Z store of the
+        // term by the group barrier after pass 0  (128: timing experiment without the ring wait)
+        if (cg_ == 0 && !FW_DBG(128))
+          while (ld_acquire_cta_u32(&ringok) <= (unsigned)gt) {
+          }
         FW_TRACE(t, 2);
 #if FW_STEP2D_TRACE
         if (prm.trace && cg_ == 0 && vctaid() < 160)
@@ -831,7 +863,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           continue;
         }
         const unsigned ttw_ = tmem_base + ((unsigned)(32 * ((tidc >> 5) & 3)) << 16) + (unsigned)(G::TM_TWC + g_ * 56);
-        column_pair<G, +1>(work_, twc, ttw_, cg_, a, gb_, [&] {
+        column_pair<G, +1>(work_, nullptr, ttw_, cg_, a, gb_, [&] {
           if (!FW_S2D_PUBLISHER && cg_ == 0 && t > 0) {
             if (FW_DBG(64))
               red_relaxed_add(&cC[t - 1], (unsigned long long)nz_);  // timing: publication without the fence
@@ -844,12 +876,12 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
             const int k0 = i + r * G::CT2;
             if (kA_ == 0) {  // Z_0 from X_0 and X_h (member 1 = column h has no Z of its own)
               if (prm.residue) rmax = fmax(rmax, fabs(xa[r].y) + fabs(xb[r].y));
-              st_keep(&Z[k0], pre_c2r(xa[r], xb[r], true, twp[0]), pol_evict_last());
+              st_keep(&Z[k0], pre_c2r(xa[r], xb[r], true, twq[2 * g_]), pol_evict_last());
             } else if (kA_ == h / 2) {
-              st_keep(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xa[r], false, twp[kA_]), pol_evict_last());
+              st_keep(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xa[r], false, twq[2 * g_]), pol_evict_last());
             } else {
-              st_keep(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xb[r], false, twp[kA_]), pol_evict_last());
-              st_keep(&Z[(size_t)kB_ * J0 + k0], pre_c2r(xb[r], xa[r], false, twp[kB_]), pol_evict_last());
+              st_keep(&Z[(size_t)kA_ * J0 + k0], pre_c2r(xa[r], xb[r], false, twq[2 * g_]), pol_evict_last());
+              st_keep(&Z[(size_t)kB_ * J0 + k0], pre_c2r(xb[r], xa[r], false, twq[2 * g_ + 1]), pol_evict_last());
             }
           }
         }, [&](int sl) { FW_TRACE(t, sl); });
@@ -881,10 +913,11 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
     const int row = r0 + (active ? pair : 0);
     // this warp's 32 TMEM columns in its lane quadrant: (s-s0)^m-weighted sums of outputs l + 64 r
     const unsigned tacc = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + 32u * (unsigned)(rw >> 2);
-    // this lane's pass-2 twiddles (butterfly index l) -> TMEM, once per launch
-    if (FW_S2D_TWTM)
-      tw_park(tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_TWR + 28 * (rw >> 2)),
-              twr + twoff(h, 2) + (l & (pprod(h, 2) - 1)) * 7);
+    // this lane's pass-2 twiddles (butterfly index l) -> TMEM, once per launch; pass-1 twiddles
+    // were parked per lane quadrant before the role split
+    const unsigned ttw2 = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(G::TM_TWR + 28 * (rw >> 2));
+    const unsigned ttw1 = tmem_base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)G::TM_TWR1;
+    tw_park_master(ttw2, prm.master, l & (pprod(h, 2) - 1), pprod(h, 2));
     double2* work = sm + G::OFF_RW + (size_t)(active ? pair : 0) * G::LROW;
     // the tile: rows r0..r0+7 of Z[t] as two [256 k][8 rows] TMA boxes, 128-B swizzled
     double2* tile;
@@ -938,27 +971,66 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
       }
     }
 
-    if (FW_S2D_PUBLISHER && rw == 2 * RMAX + 1 && lane == 0) {
-      // ---- publisher (one lane of the other idle warp): term gt's Z columns of this CTA are
-      // stored once every active column group has counted it in zdone (st.release.cta after the
-      // group barrier that follows its Z stores); one red.release.gpu makes them visible to every
-      // tile producer (cumulative over the group's stores: they precede the release in causality order)
+    if (rw == 2 * RMAX + 1 && lane == 0) {
+      // ---- loader + publisher (one lane of the other idle warp), one event loop over the
+      // launch's terms gt:
+      //  * weights: as soon as group g's column warps have read term gt-1's weights (wempty), the
+      //    bulk copies of term gt's weights of its two columns land in shared memory (wfull);
+      //  * ring: once the columns have started term gt-1, poll the global "rows of term gt-KRING
+      //    consumed" counter and post ring slot gt as free (ringok, st.release.cta);
+      //  * publication: term gt's Z columns of this CTA are stored once every active group has
+      //    counted it in zdone (st.release.cta after the group barrier that follows its Z stores);
+      //    one red.release.gpu makes them visible to every tile producer (cumulative over the
+      //    groups' stores: they precede the release in causality order).  The release fence's
+      //    drain is off the column warps' critical path.
       int ng = 0;
       unsigned long long nzs = 0;
+      int colA[2] = {-1, -1}, colB[2] = {-1, -1};
+      unsigned bytes[2] = {0u, 0u};
       for (int g = 0; g < 2; ++g) {
         const int sl = b + g * nblk;
         if (sl >= G::NSLOT) continue;
         ++ng;
-        const int kA = sl == 0 ? 0 : sl;
-        const int kB = sl == 0 ? h : (sl == h / 2 ? -1 : h - sl);
-        nzs += (unsigned long long)((kA < h) + (kB >= 0 && kB < h));
+        colA[g] = sl == 0 ? 0 : sl;
+        colB[g] = sl == 0 ? h : (sl == h / 2 ? -1 : h - sl);
+        nzs += (unsigned long long)((colA[g] < h) + (colB[g] >= 0 && colB[g] < h));
+        bytes[g] = (unsigned)((colA[g] >= 0) + (colB[g] >= 0)) * (unsigned)(J0 * sizeof(double));
       }
+      const unsigned long long pol = pol_evict_first();
+      auto issue = [&](int g, int gt) {
+        const int t = gt % ntot;
+        const int op = t / nterms, m = prm.m_first + t % nterms;
+        double* dst = reinterpret_cast<double*>(sm + G::OFF_W) + (size_t)(2 * g) * J0;
+        const double* src = prm.w[op] + (size_t)m * prm.wcols * J0;
+        mbar_expect_tx(&wfull[g], bytes[g]);
+        if (colA[g] >= 0) bulk_g2s_hint(dst, src + (size_t)colA[g] * J0, J0 * sizeof(double), &wfull[g], pol);
+        if (colB[g] >= 0) bulk_g2s_hint(dst + J0, src + (size_t)colB[g] * J0, J0 * sizeof(double), &wfull[g], pol);
+      };
       const int gtot = prm.nsteps * ntot;
-      for (int gt = 0; gt < gtot; ++gt) {
-        for (int g = 0; g < ng; ++g)
-          while (ld_acquire_cta_u32(&zdone[g]) <= (unsigned)gt) {
+      int nl[2] = {1, 1};
+      if (gtot > 0)
+        for (int g = 0; g < ng; ++g) issue(g, 0);
+      int np = 0, nr = KRING;
+      while (np < gtot) {
+        int nlmin = gtot;
+        for (int g = 0; g < ng; ++g) {
+          if (nl[g] < gtot && mbar_test(&wempty[g], (unsigned)(nl[g] - 1) & 1u)) {
+            issue(g, nl[g]);
+            ++nl[g];
           }
-        red_release_add(&cC[gt % ntot], nzs);
+          nlmin = min(nlmin, nl[g]);
+        }
+        if (nr < gtot && nr <= nlmin &&
+            ld_acquire(&cR[(nr - KRING) % ntot]) >= (unsigned long long)((nr - KRING) / ntot + 1) * J0) {
+          st_release_cta_u32(&ringok, (unsigned)nr + 1u);
+          ++nr;
+        }
+        bool done = true;
+        for (int g = 0; g < ng; ++g) done = done && ld_acquire_cta_u32(&zdone[g]) > (unsigned)np;
+        if (done) {
+          red_release_add(&cC[np % ntot], nzs);
+          ++np;
+        }
       }
     }
 
@@ -974,11 +1046,11 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
 #pragma unroll
       for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = u2[l + r * G::RT];
       pairbar(pair);
-      row_passes01<G, -1>(work, twr, l, pair);
+      row_passes01<G, -1>(work, ttw1, l, pair);
       double2 a[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) a[r] = work[G::r_p2in(l) + r * G::RS2];
-      butterfly<h, 2, -1>(a, l, twr);
+      butterfly_tm8_lean<-1>(a, ttw2);
       pairbar(pair);
 #pragma unroll
       for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = a[r];
@@ -992,8 +1064,8 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         } else {
           const double2 A = work[G::rpad(jj)];
           const double2 B = work[G::rpad(h - jj)];
-          __stcg(&Yr[jj], post_r2c(A, B, twp[jj]));
-          if (jj != h - jj) __stcg(&Yr[h - jj], post_r2c(B, A, twp[h - jj]));
+          __stcg(&Yr[jj], post_r2c(A, B, __ldg(&prm.master[jj * (kTwMaster / J1)])));
+          if (jj != h - jj) __stcg(&Yr[h - jj], post_r2c(B, A, __ldg(&prm.master[(h - jj) * (kTwMaster / J1)])));
         }
       }
       pairbar(pair);  // both warps' Y stores precede the signal
@@ -1048,7 +1120,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         double2 a[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) a[r] = work_[G::r_p1in(l_) + r * G::RS1];
-        butterfly<h, 1, +1>(a, l_, twr);
+        butterfly_tm8_lean<+1>(a, tmem_base + ((unsigned)(32 * ((tidr >> 5) & 3)) << 16) + (unsigned)G::TM_TWR1);
 #pragma unroll
         for (int r = 0; r < 8; ++r) work_[G::r_p1in(l_) + r * G::RS1] = a[r];
       }
@@ -1059,11 +1131,8 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         double2 a[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) a[r] = work_[G::r_p2in(l_) + r * G::RS2];
-        if (FW_S2D_TWTM)
-          butterfly_tm8_lean<+1>(a, tmem_base + ((unsigned)(32 * ((tidr >> 5) & 3)) << 16) +
-                                        (unsigned)(G::TM_TWR + 28 * (rw_ >> 2)));
-        else
-          butterfly<h, 2, +1>(a, l_, twr);
+        butterfly_tm8_lean<+1>(a, tmem_base + ((unsigned)(32 * ((tidr >> 5) & 3)) << 16) +
+                                      (unsigned)(G::TM_TWR + 28 * (rw_ >> 2)));
 #pragma unroll
         for (int qt = 0; qt < 4; ++qt) {
           double2 d[2];
