@@ -91,8 +91,9 @@ int fw_ctx_device(fw_ctx ctx);
 long long fw_ctx_launches(fw_ctx ctx);
 /* diagnostics: the persistent 2D kernel's watchdog records (needs FW_TRACE=1 at context
  * creation; mapped host memory, readable even after the kernel trapped): out receives
- * 1024 x 16 unsigned 64-bit words, per CTA two records (producer, compute warps) of 8 words
- * {wait site, thread, value seen, target, term, globaltimer} */
+ * 156672 unsigned 64-bit words: the watchdog records first (1024 x 16 words, per CTA two records
+ * (producer, compute warps) of 8 words {wait site, thread, value seen, target, term, globaltimer}),
+ * or, in a trace build (-DFW_STEP2D_TRACE=1), the phase marks read by tools/trace_step2d.py */
 int fw_ctx_trace(fw_ctx ctx, unsigned long long* out);
 
 /* ---- operator: ExpansionOperator resident on the device ----

@@ -386,7 +386,7 @@ int fw_internal_set_error(int code, const char* msg) { return set_err(code, msg 
 int fw_ctx_trace(fw_ctx c, unsigned long long* out) {
   if (!c || !c->trace_host || !out) return set_err(FW_E_ARG, "tracing disabled (set FW_TRACE=1 before fw_ctx_create)");
   if (c->stream) cudaStreamSynchronize(c->stream);  // a trapped kernel leaves a sticky error: ignored here
-  memcpy(out, c->trace_host, (size_t)fw::kTraceWords * sizeof(unsigned long long));
+  memcpy(out, c->trace_host, (size_t)fw::kTraceAlloc * sizeof(unsigned long long));
   return FW_OK;
 }
 long long fw_ctx_launches(fw_ctx c) { return c ? c->launches : 0; }
