@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         double2 a[CR0];
 #pragma unroll
         for (int r = 0; r < CR0; ++r)
-          a[r] = mycol >= 0 ? __ldcg(&prm.Y[(size_t)(i0 + r * CT0) * H + mycol]) : make_double2(0.0, 0.0);
+          a[r] = mycol >= 0 ? __ldcg(&prm.Y[(size_t)mycol * J0 + i0 + r * CT0]) : make_double2(0.0, 0.0);
         double2 x0[G::CR2], x1[G::CR2];
         int ix = 0;
         column_pair<G, -1>(
@@ -1055,17 +1055,23 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
 #pragma unroll
       for (int r = 0; r < 8; ++r) work[G::rpad(l) + r * G::RS0] = a[r];
       pairbar(pair);
-      double2* Yr = prm.Y + (size_t)row * H;
-      for (int jj = l; jj <= h / 2; jj += 64) {
+      // Y is stored column-major, Y[k][k0] (the forward column pass reads each column contiguously)
+      double2* Yc = prm.Y + row;
+#pragma unroll
+      for (int it = 0; it < h / 128 + 1; ++it) {
+        const int jj = l + 64 * it;
+        if (jj > h / 2) break;
         if (jj == 0) {
           const double2 z0 = work[0];
-          __stcg(&Yr[0], make_double2(z0.x + z0.y, 0.0));
-          __stcg(&Yr[h], make_double2(z0.x - z0.y, 0.0));
+          __stcg(&Yc[0], make_double2(z0.x + z0.y, 0.0));
+          __stcg(&Yc[(size_t)h * J0], make_double2(z0.x - z0.y, 0.0));
         } else {
+          const double2 wa = __ldg(&prm.master[jj * (kTwMaster / J1)]);
+          const double2 wb = __ldg(&prm.master[(h - jj) * (kTwMaster / J1)]);
           const double2 A = work[G::rpad(jj)];
           const double2 B = work[G::rpad(h - jj)];
-          __stcg(&Yr[jj], post_r2c(A, B, __ldg(&prm.master[jj * (kTwMaster / J1)])));
-          if (jj != h - jj) __stcg(&Yr[h - jj], post_r2c(B, A, __ldg(&prm.master[(h - jj) * (kTwMaster / J1)])));
+          __stcg(&Yc[(size_t)jj * J0], post_r2c(A, B, wa));
+          if (jj != h - jj) __stcg(&Yc[(size_t)(h - jj) * J0], post_r2c(B, A, wb));
         }
       }
       pairbar(pair);  // both warps' Y stores precede the signal

@@ -18,7 +18,7 @@ struct Step2DParams {
   int J0, J1;
   int M, m_first, nops, nterms_total;
   const double* u;          // input field (cur)
-  double2* Y;               // J0 x (J1/2+1) forward scratch
+  double2* Y;               // (J1/2+1) x J0 forward scratch, column-major Y[k][k0]
   double2* T;               // KRING x J0 x (J1/2+1) term ring
   const double* w[2];       // per op: [M+1][wcols][J0] weights (column-major per term)
   int wcols;                // columns per term in w (>= J1/2+1)
