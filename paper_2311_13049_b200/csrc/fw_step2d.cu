@@ -772,6 +772,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
               }
             },
             [](int) {});
+        FW_TRACE(135, 3);
         gb();  // pass-2 reads done: the buffers may take the natural-order result
         if (cg < G::CT2) {
 #pragma unroll
@@ -1182,6 +1183,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
     }
 
     // ---- seismic update (seismic.cpp:116-129)
+    FW_TRACE(135, 6);
     if (prm.seismic) {
       bool bad = false;
       const double tau = prm.tau;
@@ -1217,6 +1219,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
       }
       if (__any_sync(0xffffffffu, bad) && lane == 0 && !FW_DBG(-1)) atomicMin(prm.flag, prm.step + s);
+      FW_TRACE(135, 2);
     }
     }  // steps
   }

@@ -75,14 +75,14 @@ if len(ok):
 # step start marks (term slot 135): columns [0] before the F1 wait, [1] F1 complete, [2] F2 complete;
 # rows [0] F1 start, [1] F1 signalled
 for sel in range(2):
-    c = (tr[sel, COLW0, 135, :3] - t0) / 1000.0
+    c = (tr[sel, COLW0, 135, :4] - t0) / 1000.0
     r = (tr[sel, ROWW0, 135, :7] - t0) / 1000.0
     lt = (tr[sel, ROWW0, ntot - 1, :8] - t0) / 1000.0
     f = (tr[sel, COLW0, 0, 0] - t0) / 1000.0
     print(f"CTA {0 if sel == 0 else 100}: rows F1 {r[0]:.1f} -> {r[1]:.1f} us; columns wait F1 {c[0]:.1f} -> {c[1]:.1f},"
-          f" F2 done {c[2]:.1f}, first term starts {f:.1f} us (t0 = earliest mark)")
+          f" F2 passes done {c[3]:.1f}, F2 done {c[2]:.1f}, first term starts {f:.1f} us (t0 = earliest mark)")
     print(f"  rows' last term: start {lt[0]:.1f}, tile {lt[2]:.1f}, pass 2 done {lt[6]:.1f}, pairbar {lt[7]:.1f};"
-          f" update start {r[6]:.1f} flag read {r[3]:.1f} iter0 {r[4]:.1f} iter3 {r[5]:.1f} done {r[2]:.1f} us")
+          f" update start {r[6]:.1f} done {r[2]:.1f} us")
 
 # producer (row warp 14, lane 0): [0] loop top, [1] cC[t] complete, [2] tile_empty(t-1), [3] TMA issued;
 # consumers (row warp 0): [0] term start, [2] tile landed; columns (first column warp): [6] term done
