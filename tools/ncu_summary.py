@@ -78,3 +78,9 @@ for (f, l), (w, e) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:25]:
         cache[f] = open(p).read().split("\n") if os.path.exists(p) else []
     s = cache[f][l - 1].strip()[:78] if l and l <= len(cache[f]) else ""
     print(f"  {w / tot:6.3f} {e:10.0f} {f}:{l}  {s}")
+ex = sorted(((e, f, l) for (f, l), (w, e) in agg.items() if e > 0), reverse=True)[:10]
+if ex:
+    print("most excess smem wavefronts (bank conflicts):")
+    for e, f, l in ex:
+        s = cache.get(f, [])
+        print(f"  {e:10.0f} {f}:{l}  {s[l - 1].strip()[:78] if l and l <= len(s) else ''}")
