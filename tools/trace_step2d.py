@@ -31,7 +31,9 @@ tr = buf[:2 * 32 * 136 * 8].reshape(2, 32, 136, 8).astype(np.int64)
 colend = buf[2 * 32 * 136 * 8:2 * 32 * 136 * 8 + 160 * 2 * 136].reshape(160, 2, 136).astype(np.int64)
 colgo = buf[2 * 32 * 136 * 8 + 160 * 2 * 136:].reshape(160, 2, 136).astype(np.int64)  # after the ring wait
 ntot = 34
-COLW0, ROWW0 = (16, 0) if os.environ.get("FW_S2D_COLHI", "1") == "1" else (0, 8)  # warp roles (fw_step2d.cu)
+# warp roles (fw_step2d.cu): FW_TRACE_LAYOUT=w16 -> rows 0-6, agents 7, columns 8-15
+LAYOUT = os.environ.get("FW_TRACE_LAYOUT", "w24")
+COLW0, ROWW0, PRODW = {"w16": (8, 0, 7), "w20": (12, 0, 8)}.get(LAYOUT, (16, 0, 14))
 t0 = tr[:, :24][tr[:, :24] > 0].min()
 COL = ["w+uhat", "ring", "pass0", "pass1", "pass2+Z", "gbar"]
 ROW = ["tile wait", "pass0", "pass1", "pass2+acc", "pairbar"]
@@ -87,7 +89,7 @@ for sel in range(2):
 # producer (row warp 14, lane 0): [0] loop top, [1] cC[t] complete, [2] tile_empty(t-1), [3] TMA issued;
 # consumers (row warp 0): [0] term start, [2] tile landed; columns (first column warp): [6] term done
 for sel in range(2):
-    P = (tr[sel, ROWW0 + 14, :ntot, :4] - t0) / 1000.0
+    P = (tr[sel, PRODW, :ntot, :4] - t0) / 1000.0
     R = (tr[sel, ROWW0, :ntot, :8] - t0) / 1000.0
     Cw = (tr[sel, COLW0, :ntot, :8] - t0) / 1000.0
     print(f"CTA {0 if sel == 0 else 100}: t | cols done | cC ready | empty(t-1) | TMA issue | landed | row wants")
