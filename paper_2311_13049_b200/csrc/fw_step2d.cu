@@ -845,6 +845,10 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         if (cg_ == 0 && !FW_DBG(128))
           while (ld_acquire_cta_u32(&ringok) <= (unsigned)gt) {
           }
+        // the warp reconverges here: the group barriers below are bar.sync (.aligned), which a
+        // diverged warp must not reach (measured with the DBG 32 timing build: lanes 1-31 arriving
+        // while lane 0 still spun let the group pass without it)
+        __syncwarp();
         FW_TRACE(t, 2);
 #if FW_STEP2D_TRACE
         if (prm.trace && cg_ == 0 && vctaid() < 160)
@@ -970,6 +974,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
           red_relaxed_add(&cR[ntot - 1], (unsigned long long)nr);
         }
       }
+      __syncwarp();  // reconverge before the kernel's final (aligned) barrier
     }
 
     if (rw == 2 * RMAX + 1 && lane == 0) {
@@ -1034,6 +1039,7 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
         }
       }
     }
+    if (rw == 2 * RMAX + 1) __syncwarp();  // the loader's warp reconverges before the final barrier
 
     // this step's state buffers (multi-step launches rotate them with the level)
     auto lvl_u = [&](int s, int d) -> double* { return prm.ub[(int)((prm.lvl0 + s + d) % 3)]; };
