@@ -203,6 +203,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef FW_S2D_RING1
 #define FW_S2D_RING1 1
 #endif
+// the column warps take half of the step's fused update (idle otherwise at the step's tail; 0: the
+// row warps do all of it; A/B)
+#ifndef FW_S2D_TAILHELP
+#define FW_S2D_TAILHELP 1
+#endif
 constexpr int kColW0 = FW_S2D_COLHI ? 16 : 0;  // first column warp
 constexpr int kRowW0 = FW_S2D_COLHI ? 0 : 8;   // first row warp
 // L2 promotion of the tile TMA loads (A/B)
@@ -641,6 +646,58 @@ __device__ __forceinline__ void row_passes01(double2* work, unsigned ttw1, int l
   pairbar(pair);
 }
 
+// ---------------------------------------------------------------- fused seismic update
+// (seismic.cpp:116-129) of outputs q = l + 64 r, r in [rb, re), of NW row warps at once (their
+// loads in flight together); the L2 sums come from each row warp's tensor-memory accumulators
+// (lane quadrant of the calling warp).  Returns this lane's blow-up test.
+template <class G, int NW>
+__device__ __forceinline__ bool seis_update_part(const Step2DParams& prm, int s, const int (&row)[NW],
+                                                 const int (&l)[NW], const unsigned (&tacc)[NW],
+                                                 const bool (&on)[NW], int rb, int re, bool frozen) {
+  constexpr int J1 = 2 * G::h;
+  const double tau = prm.tau;
+  const double t2 = tau * tau;
+  const bool ms = prm.nsteps > 1;
+  const double* ucur = ms ? prm.ub[(int)((prm.lvl0 + s) % 3)] : prm.u;
+  const double* uprev = ms ? prm.ub[(int)((prm.lvl0 + s + 2) % 3)] : prm.prev;
+  const double* aprev = ms ? prm.ab[(int)((prm.lvl0 + s + 1) % 2)] : prm.ap;
+  double* unext = ms ? prm.ub[(int)((prm.lvl0 + s + 1) % 3)] : prm.next;
+  double* aout = ms ? prm.ab[(int)((prm.lvl0 + s) % 2)] : prm.out[1];
+  bool bad = false;
+#pragma unroll 1
+  for (int r = rb; r < re; ++r) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      if (!on[w]) continue;  // warp-uniform
+      unsigned v[4];
+      tmem_ld4(tacc[w] + 4u * r, v);
+      const size_t rowoff = (size_t)row[w] * J1;
+      const int q = l[w] + r * G::RT;
+      const double2 vc = reinterpret_cast<const double2*>(ucur + rowoff)[q];
+      const double2 vp = reinterpret_cast<const double2*>(uprev + rowoff)[q];
+      const double2 va = reinterpret_cast<const double2*>(aprev + rowoff)[q];
+      const double2 v1 = reinterpret_cast<const double2*>(prm.out[0] + rowoff)[q];
+      const double2 cc = reinterpret_cast<const double2*>(prm.c + rowoff)[q];
+      const double2 ve = reinterpret_cast<const double2*>(prm.eta + rowoff)[q];
+      const double2 vt = reinterpret_cast<const double2*>(prm.tc + rowoff)[q];
+      const double l2x = tm_d(v, 0), l2y = tm_d(v, 1);
+      const double c2x = cc.x * cc.x, c2y = cc.y * cc.y;
+      const double nx0 = 2.0 * vc.x - vp.x + t2 * c2x * (ve.x * v1.x + vt.x * (l2x - va.x) / tau);
+      const double nx1 = 2.0 * vc.y - vp.y + t2 * c2y * (ve.y * v1.y + vt.y * (l2y - va.y) / tau);
+      if (!frozen) {
+        reinterpret_cast<double2*>(unext + rowoff)[q] = make_double2(nx0, nx1);
+        reinterpret_cast<double2*>(aout + rowoff)[q] = make_double2(l2x, l2y);
+      }
+      bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
+    }
+  }
+  return bad;
+}
+// the step's tail: the active row warps and the active column groups' warps meet on named
+// barrier 12 before and after the fused update (the column warps take outputs r = 4..7 of the
+// row warps of their lane quadrant, see k_step2d)
+__device__ __forceinline__ void tailbar(int nthreads) { asm volatile("bar.sync 12, %0;" ::"r"(nthreads) : "memory"); }
+
 // --------------------------------------------------------------------------
 template <int J0, int J1, int RMAX>
 __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const __grid_constant__ CUtensorMap zmap) {
@@ -900,6 +957,29 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
 #endif
       }
       if (!FW_S2D_PUBLISHER && cg == 0 && ntot > 0) red_release_add(&cC[ntot - 1], (unsigned long long)nz);
+      if (FW_S2D_TAILHELP && prm.seismic) {
+        // help with the step's update: outputs r = 4..7 of row warps q + 8g and q + 8g + 4 (lane
+        // quadrant q = this warp's), whose accumulators this warp can read from tensor memory
+        const int nrow = (int)(((long long)(b + 1) * J0) / nblk) - (int)(((long long)b * J0) / nblk);
+        const int ngrp = 1 + (b + nblk < G::NSLOT);
+        const int q = warp & 3;
+        int rowv[2], lv[2];
+        unsigned tav[2];
+        bool onv[2];
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          const int rw = q + 8 * g + 4 * w;
+          onv[w] = rw < 2 * nrow;
+          rowv[w] = (int)(((long long)b * J0) / nblk) + (rw >> 1);
+          lv[w] = (rw & 1) * 32 + lane;
+          tav[w] = tmem_base + ((unsigned)(32 * q) << 16) + 32u * (unsigned)(rw >> 2);
+        }
+        tailbar((2 * nrow + 4 * ngrp) * 32);
+        const bool frozen = s > 0 && *reinterpret_cast<volatile int*>(prm.flag) < prm.step + s;
+        const bool bad = seis_update_part<G, 2>(prm, s, rowv, lv, tav, onv, 4, 8, frozen);
+        if (__any_sync(0xffffffffu, bad) && lane == 0 && !FW_DBG(-1)) atomicMin(prm.flag, prm.step + s);
+        tailbar((2 * nrow + 4 * ngrp) * 32);
+      }
       }  // steps
       if (prm.residue && rmax > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(prm.residue),
@@ -1191,40 +1271,29 @@ __global__ void __launch_bounds__(768, 1) k_step2d(const Step2DParams prm, const
     // ---- seismic update (seismic.cpp:116-129)
     FW_TRACE(135, 6);
     if (prm.seismic) {
-      bool bad = false;
-      const double tau = prm.tau;
-      const double t2 = tau * tau;
-      const size_t rowoff = (size_t)row * J1;
-      const bool ms = prm.nsteps > 1;
-      const double2* cur = reinterpret_cast<const double2*>((ms ? lvl_u(s, 0) : prm.u) + rowoff);
-      const double2* prev = reinterpret_cast<const double2*>((ms ? lvl_u(s, 2) : prm.prev) + rowoff);
-      const double2* ap = reinterpret_cast<const double2*>((ms ? lvl_a(s, 1) : prm.ap) + rowoff);
       // a blow-up in an EARLIER step of this launch: keep the state the host restores
       // (this step would overwrite the offending step's prev / L2prev)
       const bool frozen = s > 0 && *reinterpret_cast<volatile int*>(prm.flag) < prm.step + s;
-      const double2* l1 = reinterpret_cast<const double2*>(prm.out[0] + rowoff);
-      const double2* c = reinterpret_cast<const double2*>(prm.c + rowoff);
-      const double2* eta = reinterpret_cast<const double2*>(prm.eta + rowoff);
-      const double2* tc = reinterpret_cast<const double2*>(prm.tc + rowoff);
-      double2* nx = reinterpret_cast<double2*>((ms ? lvl_u(s, 1) : prm.next) + rowoff);
-      double2* l2o = reinterpret_cast<double2*>((ms ? lvl_a(s, 0) : prm.out[1]) + rowoff);
-#pragma unroll 1
-      for (int r = 0; r < 8; ++r) {
-        unsigned v[4];
-        tmem_ld4(tacc + 4u * r, v);
-        const int q = l + r * G::RT;
-        const double2 vc = cur[q], vp = prev[q], va = ap[q], v1 = l1[q], cc = c[q], ve = eta[q], vt = tc[q];
-        const double l2x = tm_d(v, 0), l2y = tm_d(v, 1);
-        const double c2x = cc.x * cc.x, c2y = cc.y * cc.y;
-        const double nx0 = 2.0 * vc.x - vp.x + t2 * c2x * (ve.x * v1.x + vt.x * (l2x - va.x) / tau);
-        const double nx1 = 2.0 * vc.y - vp.y + t2 * c2y * (ve.y * v1.y + vt.y * (l2y - va.y) / tau);
-        if (!frozen) {
-          nx[q] = make_double2(nx0, nx1);
-          l2o[q] = make_double2(l2x, l2y);
-        }
-        bad |= (fabs(nx0) > prm.thr) || (fabs(nx1) > prm.thr);
+      bool bad;
+      if (FW_S2D_TAILHELP) {
+        // outputs r = 0..3 here, r = 4..7 by the column warp of this lane quadrant when its group
+        // is active (otherwise all eight)
+        const int ngrp = 1 + (b + nblk < G::NSLOT);
+        const bool helped = ((rw >> 3) < ngrp);
+        tailbar((2 * nr + 4 * ngrp) * 32);
+        const int rowv[1] = {row}, lv[1] = {l};
+        const unsigned tav[1] = {tacc};
+        const bool onv[1] = {true};
+        bad = seis_update_part<G, 1>(prm, s, rowv, lv, tav, onv, 0, helped ? 4 : 8, frozen);
+        if (__any_sync(0xffffffffu, bad) && lane == 0 && !FW_DBG(-1)) atomicMin(prm.flag, prm.step + s);
+        tailbar((2 * nr + 4 * ngrp) * 32);
+      } else {
+        const int rowv[1] = {row}, lv[1] = {l};
+        const unsigned tav[1] = {tacc};
+        const bool onv[1] = {true};
+        bad = seis_update_part<G, 1>(prm, s, rowv, lv, tav, onv, 0, 8, frozen);
+        if (__any_sync(0xffffffffu, bad) && lane == 0 && !FW_DBG(-1)) atomicMin(prm.flag, prm.step + s);
       }
-      if (__any_sync(0xffffffffu, bad) && lane == 0 && !FW_DBG(-1)) atomicMin(prm.flag, prm.step + s);
       FW_TRACE(135, 2);
     }
     }  // steps
