@@ -22,6 +22,7 @@
  *   fw_seis_step            SeismicStepper::step / advance               seismic.cpp:111-137
  *   fw_seis_get             SeismicStepper::current / n                  seismic.hpp:44-46
  *   fw_seis_step_io         current() = u; step(); u = current()         seismic.cpp:111-133, seismic.hpp:44
+ *   fw_seis_step_io_async / fw_seis_wait   the same, split for overlapping independent steppers
  *   fw_tsfp2_*              Stepper (Method::TSFP2) ctor / step            stepping.cpp:119-138, 266-304
  *   fw_wave_*               Stepper (Method::LFFP / CNFP) ctor / step      stepping.cpp:88-104, 119-138, 170-264
  *                           (the Laplacian seam stepping.hpp:52-60 served by the device apply)
@@ -171,6 +172,14 @@ int fw_seis_set_current(fw_seis s, const double* cur_host);
  * (both host buffers nullable, may alias; pinned memory for full PCIe speed).  On
  * FW_E_BLOWUP cur_out_host holds the pre-step state, as fw_seis_get would return. */
 int fw_seis_step_io(fw_seis s, const double* cur_in_host, int nsteps, double* cur_out_host);
+/* The two halves of fw_seis_step_io for pipelines of independent steppers (e.g. the shots of a
+ * survey, one fw_ctx = one stream each): _async enqueues the upload, the steps and the download on
+ * the stepper's context stream and returns without a host synchronisation; fw_seis_wait is the
+ * synchronisation and the blow-up check of everything enqueued so far (on FW_E_BLOWUP the pending
+ * cur_out_host is rewritten with the pre-step state).  The host buffers must stay valid until
+ * fw_seis_wait; with pinned buffers the copies of one stepper run under the steps of another. */
+int fw_seis_step_io_async(fw_seis s, const double* cur_in_host, int nsteps, double* cur_out_host);
+int fw_seis_wait(fw_seis s);
 /* device pointer of the current wavefield (valid until the next step) */
 const double* fw_seis_current_device(fw_seis s);
 /* the two operators, for diagnostics */

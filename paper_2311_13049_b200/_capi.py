@@ -185,6 +185,8 @@ def load_library():
     lib.fw_seis_get.argtypes = [_vp, _dp, _dp, _dp, C.POINTER(C.c_long)]
     lib.fw_seis_set_current.argtypes = [_vp, _dp]
     lib.fw_seis_step_io.argtypes = [_vp, _dp, C.c_int, _dp]
+    lib.fw_seis_step_io_async.argtypes = [_vp, _dp, C.c_int, _dp]
+    lib.fw_seis_wait.argtypes = [_vp]
     lib.fw_seis_current_device.argtypes = [_vp]
     lib.fw_seis_current_device.restype = _vp
     lib.fw_seis_ops.argtypes = [_vp, C.POINTER(_vp), C.POINTER(_vp)]
@@ -220,6 +222,7 @@ EXPORTED_SYMBOLS = [
     "fw_apply", "fw_apply_device", "fw_apply_batch_device", "fw_stage_c2c_scatter", "fw_ipc_handle", "fw_ipc_open", "fw_ipc_close",
     "fw_medium_coefficients", "fw_stage_seis_start", "fw_stage_seis_update", "fw_seis_create", "fw_seis_destroy",
     "fw_seis_step", "fw_seis_enqueue", "fw_seis_get", "fw_seis_set_current", "fw_seis_step_io",
+    "fw_seis_step_io_async", "fw_seis_wait",
     "fw_seis_current_device", "fw_seis_ops", "fw_seis_medium", "fw_tsfp2_create",
     "fw_tsfp2_destroy", "fw_tsfp2_step", "fw_tsfp2_get", "fw_wave_create", "fw_wave_destroy", "fw_wave_step",
     "fw_wave_get", "fw_rfftn", "fw_irfftn", "fw_op_path", "fw_ricker_initial", "fw_grid_dft", "fw_grid_dft_device",

@@ -443,6 +443,23 @@ class SeismicStepper:
                                              None if cur_out is None else _ptr(cur_out)))
         return cur_out
 
+    def step_io_async(self, cur_in=None, cur_out=None, steps: int = 1):
+        """The enqueue half of step_io (fw_seis_step_io_async): upload, `steps` steps and download
+        go onto this stepper's context stream and the call returns at once; `wait()` completes
+        it.  Both arrays must be C-contiguous float64 of the grid's size and stay alive (pinned
+        for overlap) until wait().  Steppers on different contexts overlap each other."""
+        for a in (cur_in, cur_out):
+            if a is not None and (a.dtype != np.float64 or not a.flags.c_contiguous
+                                  or a.size != self.grid.total()):
+                raise ValueError("host fields must be C-contiguous float64 arrays of the grid's size")
+        check(load_library().fw_seis_step_io_async(self._h, None if cur_in is None else _ptr(cur_in), int(steps),
+                                                   None if cur_out is None else _ptr(cur_out)))
+
+    def wait(self):
+        """Completes step_io_async (fw_seis_wait): one host synchronisation and the blow-up
+        check; BlowupDetected as step(), with the pending cur_out holding the pre-step state."""
+        check(load_library().fw_seis_wait(self._h))
+
     def n(self) -> int:
         n = C.c_long(0)
         check(load_library().fw_seis_get(self._h, None, None, None, C.byref(n)))

@@ -1152,6 +1152,7 @@ struct fw_seis_s {
   const void* btab_T = nullptr;
   long n = 0;    // reported step count (SeismicStepper::n)
   long lvl = 0;  // index of the current level for buffer rotation
+  double* pending_out = nullptr;  // host destination of a pending fw_seis_step_io_async
   double* cur() { return ubuf[lvl % 3]; }
   double* prev() { return ubuf[(lvl + 2) % 3]; }
   double* ap() { return abuf[(lvl + 1) % 2]; }
@@ -1430,21 +1431,36 @@ int fw_seis_set_current(fw_seis s, const double* cur_host) {
   return FW_OK;
 }
 
-int fw_seis_step_io(fw_seis s, const double* cur_in_host, int nsteps, double* cur_out_host) {
+int fw_seis_step_io_async(fw_seis s, const double* cur_in_host, int nsteps, double* cur_out_host) {
   FW_SETDEV((s ? s->ctx : nullptr));
   if (!s) return set_err(FW_E_ARG, "null stepper");
   const size_t N = s->g.N;
   cudaStream_t st = s->ctx->stream;
   if (cur_in_host) FW_CUDA(cudaMemcpyAsync(s->cur(), cur_in_host, N * 8, cudaMemcpyHostToDevice, st));
   FW_TRY(fw_seis_enqueue(s, nsteps));
-  // the new wavefield and the blow-up flag come back behind the steps: one host synchronisation
+  // the new wavefield comes back behind the steps, in stream order; no host synchronisation here
   if (cur_out_host) FW_CUDA(cudaMemcpyAsync(cur_out_host, s->cur(), N * 8, cudaMemcpyDeviceToHost, st));
-  const int rc = seis_check(s);
-  if (rc == FW_E_BLOWUP && cur_out_host) {  // the state was rolled back to before the offending step
-    FW_CUDA(cudaMemcpyAsync(cur_out_host, s->cur(), N * 8, cudaMemcpyDeviceToHost, st));
+  s->pending_out = cur_out_host;
+  return FW_OK;
+}
+
+int fw_seis_wait(fw_seis s) {
+  FW_SETDEV((s ? s->ctx : nullptr));
+  if (!s) return set_err(FW_E_ARG, "null stepper");
+  double* out = s->pending_out;
+  s->pending_out = nullptr;
+  const int rc = seis_check(s);  // the one host synchronisation: everything enqueued has landed
+  if (rc == FW_E_BLOWUP && out) {  // the state was rolled back to before the offending step
+    cudaStream_t st = s->ctx->stream;
+    FW_CUDA(cudaMemcpyAsync(out, s->cur(), s->g.N * 8, cudaMemcpyDeviceToHost, st));
     FW_CUDA(cudaStreamSynchronize(st));
   }
   return rc;
+}
+
+int fw_seis_step_io(fw_seis s, const double* cur_in_host, int nsteps, double* cur_out_host) {
+  FW_TRY(fw_seis_step_io_async(s, cur_in_host, nsteps, cur_out_host));
+  return fw_seis_wait(s);
 }
 
 const double* fw_seis_current_device(fw_seis s) { return s ? s->cur() : nullptr; }

@@ -120,3 +120,62 @@ def test_c4_full_size_apply_vs_oracle(order):
     del op
     ref, _ = O.port_apply(cfg.J, cfg.lo, cfg.hi, s, cfg.phi, cfg.M)
     assert rel_l2(got, ref) <= APPLY_TOL and np.array_equal(got, ref)
+
+
+def test_c2_pipelined_shots_equal_serial_stepper():
+    """fw_seis_step_io_async / fw_seis_wait: three independent shots (one context = one stream
+    each) stepped round-robin with the host owning every shot's wavefield between steps give,
+    for every shot, exactly the fields a lone stepper computes with fw_seis_step_io; the
+    persistent kernels of the shots serialise on the device while their copies overlap."""
+    m = fw()
+    cfg = cfgs.c2()
+    med = m.build_medium(grid_of(cfg), cfg.gamma, cfg.c0, cfg.omega0, cfg.M)
+    nshots, nsteps = 3, 4
+    phis = [cfg.phi * (1.0 + 0.125 * i) for i in range(nshots)]
+    want = []
+    for phi in phis:
+        st = m.SeismicStepper(med, phi, cfg.psi, cfg.tau)
+        assert st.persistent
+        buf = st.current()
+        for _ in range(nsteps):
+            st.step_io(buf, buf)
+        want.append(buf.copy())
+        del st
+    ctxs = [m.Context(0) for _ in range(nshots)]
+    shots = [m.SeismicStepper(med, phi, cfg.psi, cfg.tau, ctx=c) for phi, c in zip(phis, ctxs)]
+    bufs = [s.current() for s in shots]
+    for r in range(nsteps):
+        for s, b in zip(shots, bufs):
+            if r:
+                s.wait()
+                b += 0.0  # the host touches the wavefield between the steps
+            s.step_io_async(b, b)
+    for s in shots:
+        s.wait()
+    for b, w, s in zip(bufs, want, shots):
+        assert np.array_equal(b, w)
+        assert s.n() == nsteps + 1
+
+
+def test_step_io_async_blowup_reports_at_wait():
+    """A blow-up inside an asynchronous call surfaces at fw_seis_wait with the reference's
+    semantics (seismic.cpp:124-129): n = the offending step, the pending output = the pre-step
+    wavefield, exactly as the synchronous stepper reports it."""
+    m = fw()
+    J, lo, hi = (128, 128), (-16.0, -16.0), (16.0, 16.0)
+    g = m.Grid(list(zip(lo, hi)), J)
+    x = np.linspace(-16, 16, J[0], endpoint=False)
+    phi = np.exp(-(x[:, None] ** 2 + x[None, :] ** 2) / 0.5)
+    med = m.build_medium(g, np.full(J, 0.05), np.ones(J), 1.0, 4)
+    tau = 0.5  # far beyond stability (tau c |mu|_max^(1+gamma) >> 2)
+    ref = m.SeismicStepper(med, phi, np.zeros(J), tau)
+    with pytest.raises(m.BlowupDetected):
+        ref.advance(400)
+    rcur, _, _, rn = ref.state()
+    assert 2 < rn < 400
+    st = m.SeismicStepper(med, phi, np.zeros(J), tau)
+    out = np.empty(J)
+    st.step_io_async(None, out, steps=400)
+    with pytest.raises(m.BlowupDetected):
+        st.wait()
+    assert st.n() == rn and np.array_equal(out, rcur)
