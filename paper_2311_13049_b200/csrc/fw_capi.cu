@@ -564,7 +564,8 @@ int apply_device(fw_op op, const double* u, double* out, int m_first, double* re
     Uh = (const double2*)uh;
   }
   void* T = nullptr;
-  if (g.d >= 2) FW_TRY(ctx->get_scratch(SLOT_T, (size_t)(m_last - m_first + 1) * g.Nh * sizeof(double2), &T));
+  if (g.d >= 2)
+    FW_TRY(ctx->get_scratch(SLOT_T, (size_t)(m_last - m_first + 1) * fw::term_elems(L, g) * sizeof(double2), &T));
   fw::InverseArgs a{Uh, op->w, op->dev1, (double2*)T, out, m_first, m_last, residue, guard};
   fw::launch_inverse(L, g, a);
   return FW_OK;
@@ -814,7 +815,7 @@ int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_
   fw_ctx ctx = o0->ctx;
   const fw::GridGeom& g = o0->g;
   const int m_last = o0->constant_order ? 0 : o0->M;
-  const size_t per_field = (size_t)(m_last + 1) * g.Nh * sizeof(double2);
+  const size_t per_field = (size_t)(m_last + 1) * fw::term_elems(ctx->L(), g) * sizeof(double2);
   // fields per batched pipeline: the all-terms spectra of a chunk live in scratch (up to 16 GiB of
   // the 180 GB HBM); chunks are balanced (64 fields at M = 16 fit in one chunk; an unbalanced
   // 59 + 5 split under a 2 GiB cap left the GPU idle in the small chunk)
@@ -1245,7 +1246,7 @@ int seis_enqueue_step(fw_seis s) {
   if (g.d >= 2 && s->A1->M == s->A2->M && s->A1->constant_order == s->A2->constant_order) {
     // both inverses in one batched pipeline (grid.z = operator): twice the blocks per launch
     const int m_last = s->A1->constant_order ? 0 : s->A1->M;
-    const size_t per_op = (size_t)(m_last + 1) * g.Nh * sizeof(double2);
+    const size_t per_op = (size_t)(m_last + 1) * fw::term_elems(L, g) * sizeof(double2);
     void* T = nullptr;
     FW_TRY(ctx->get_scratch(SLOT_BT, 2 * per_op, &T));
     if (!s->btab) FW_TRY(dalloc(&s->btab, 12));

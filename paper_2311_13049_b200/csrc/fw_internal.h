@@ -121,6 +121,13 @@ struct InverseArgs {
   const int* guard;
 };
 void launch_inverse(const LaunchCtx& L, const GridGeom& g, const InverseArgs& a);
+// Row stride (complex elements) of the term scratch T the inverse pipelines write between the
+// axes, and its elements per term.  2D grids served by the register-resident line kernels pad
+// the rows of T from J1/2 + 1 (odd) to a multiple of 8 elements, so that the strided 128-B runs
+// of the axis-0 pass and the rows the C2R fetches are 128-B aligned; everything else keeps the
+// Spectrum layout.
+long long term_row_stride(const LaunchCtx& L, const GridGeom& g);
+inline size_t term_elems(const LaunchCtx& L, const GridGeom& g) { return g.rows * (size_t)term_row_stride(L, g); }
 
 constexpr int kNoBlowup = 0x7fffffff;
 
@@ -202,18 +209,21 @@ struct Scatter {
 };
 
 // register-resident line FFTs (fw_lines.cu) for n in {256, 512, 1024}; false = not served
+// (Sd: stride of the destination along the axis when it differs from the source's S -- the
+// all-terms inverse of a 2D grid writes term spectra whose rows are padded to 128 B; 0 = S)
 bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double2* dst, const double* w,
                   long long S, long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts,
                   int nterms, int nfields, double sc, bool scale, const BatchLine* bl,
-                  const Scatter* scatter = nullptr);
+                  const Scatter* scatter = nullptr, long long Sd = 0);
 
 // register-resident row R2C (fw_lines.cu) for nl in {256, 512, 1024}
 bool launch_rows_r2c(const LaunchCtx& L, int nl, const double* u, double2* Uh, long long rows, int nfields,
                      double sc, bool scale, const BatchLine* bl);
 // register-resident row C2R + ascending-m recombination (fw_lines.cu) for nl in {256, 512, 1024}
+// (xrs: row stride of src in complex elements, 0 = nl/2 + 1)
 bool launch_rows_c2r(const LaunchCtx& L, int nl, const double2* src, long long src_ts, int m_first, int m_last,
                      const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
-                     const BatchLine* bl);
+                     const BatchLine* bl, long long xrs = 0);
 
 // stage entry points (distributed orchestration on local sub-arrays)
 void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, double2* H, double scale, bool do_scale);

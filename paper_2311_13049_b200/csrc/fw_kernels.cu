@@ -353,9 +353,11 @@ void count(const LaunchCtx& L, int n = 1) {
   if (L.launches) *L.launches += n;
 }
 
+// (Sd: destination stride along the axis, 0 = the source's; only the register-resident line
+// kernels take a different one, see term_row_stride)
 void c2c_axis(const LaunchCtx& L, const GridGeom& g, int a, int dir, const double2* src, double2* dst,
               const double* w, long long src_ts, long long dst_ts, long long w_ts, int nterms, double sc,
-              bool scale) {
+              bool scale, long long Sd = 0) {
   const int n = g.J[a];
   long long S = g.hp1;
   for (int b = a + 1; b <= g.d - 2; ++b) S *= g.J[b];
@@ -363,7 +365,8 @@ void c2c_axis(const LaunchCtx& L, const GridGeom& g, int a, int dir, const doubl
   for (int b = 0; b < a; ++b) outer *= g.J[b];
   const long long inner = S;
   if (!L.generic_lines &&
-      launch_lines(L, n, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, 1, sc, scale, nullptr))
+      launch_lines(L, n, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, 1, sc, scale, nullptr,
+                   nullptr, Sd))
     return;
   const int lpb = std::max(1, std::min(8, 4096 / n));
   const long long bpo = (inner + lpb - 1) / lpb;
@@ -427,12 +430,15 @@ void launch_forward(const LaunchCtx& L, const GridGeom& g, const double* u, doub
     c2c_axis(L, g, a, -1, Uh, Uh, nullptr, 0, 0, 0, 1, inv, scale && a == 0);
 }
 
+#ifndef FW_TERM_PAD
+#define FW_TERM_PAD 1  // 2D term scratch rows padded to 128 B (0: Spectrum layout; A/B)
+#endif
 static void c2r_accum(const LaunchCtx& L, const GridGeom& g, const double2* src, long long src_ts, const double* w,
                       long long w_ts, int m_first, int m_last, const double* dev1, double* out, double* residue,
-                      const int* guard) {
+                      const int* guard, long long xrs = 0) {
   if (!w && !L.generic_lines &&
       launch_rows_c2r(L, g.nl, src, src_ts, m_first, m_last, dev1, out, (long long)g.rows, 1, residue, guard,
-                      nullptr))
+                      nullptr, xrs))
     return;
   const int h = g.nl / 2;
   const int lpb = std::max(1, std::min(8, 4096 / g.nl));
@@ -450,12 +456,21 @@ void launch_inverse(const LaunchCtx& L, const GridGeom& g, const InverseArgs& a)
     c2r_accum(L, g, a.Uh, 0, a.w, (long long)g.Nh, a.m_first, a.m_last, a.dev1, a.out, a.residue, a.guard);
     return;
   }
-  // axis 0 for all terms: T[t] = IFFT_0(w_{m_first+t} .* Uh)
-  c2c_axis(L, g, 0, +1, a.Uh, a.T, a.w + (long long)a.m_first * g.Nh, 0, (long long)g.Nh, (long long)g.Nh, nterms,
-           1.0, false);
+  // axis 0 for all terms: T[t] = IFFT_0(w_{m_first+t} .* Uh); T's rows may be padded (term_row_stride)
+  const long long xrs = term_row_stride(L, g);
+  const long long tts = (long long)term_elems(L, g);
+  c2c_axis(L, g, 0, +1, a.Uh, a.T, a.w + (long long)a.m_first * g.Nh, 0, tts, (long long)g.Nh, nterms, 1.0, false,
+           xrs != g.hp1 ? xrs : 0);
   for (int ax = 1; ax <= g.d - 2; ++ax)
-    c2c_axis(L, g, ax, +1, a.T, a.T, nullptr, (long long)g.Nh, (long long)g.Nh, 0, nterms, 1.0, false);
-  c2r_accum(L, g, a.T, (long long)g.Nh, nullptr, 0, a.m_first, a.m_last, a.dev1, a.out, a.residue, a.guard);
+    c2c_axis(L, g, ax, +1, a.T, a.T, nullptr, tts, tts, 0, nterms, 1.0, false);
+  c2r_accum(L, g, a.T, tts, nullptr, 0, a.m_first, a.m_last, a.dev1, a.out, a.residue, a.guard, xrs);
+}
+
+long long term_row_stride(const LaunchCtx& L, const GridGeom& g) {
+  const int h = g.nl / 2;
+  const bool lines2d = FW_TERM_PAD && g.d == 2 && !L.generic_lines && (g.J[0] == 256 || g.J[0] == 512 || g.J[0] == 1024) &&
+                       (h == 128 || h == 256 || h == 512);
+  return lines2d ? (long long)((g.hp1 + 7) & ~7) : (long long)g.hp1;
 }
 
 void launch_irfft(const LaunchCtx& L, const GridGeom& g, double2* H, double* x, const int* guard) {
@@ -587,9 +602,11 @@ void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_fi
     for (int b = a + 1; b <= g.d - 2; ++b) S *= g.J[b];
     long long outer = 1;
     for (int b = 0; b < a; ++b) outer *= g.J[b];
-    const long long ts = (long long)g.Nh;
+    const long long ts = (long long)term_elems(L, g);  // T's term stride (rows padded for 2D grids)
+    const long long xrs = term_row_stride(L, g);
     if (!L.generic_lines && launch_lines(L, n, +1, nullptr, nullptr, nullptr, S, outer, S, a == 0 ? 0 : ts, ts,
-                                         a == 0 ? ts : 0, nterms, F, 1.0, false, a == 0 ? tab0 : tab1))
+                                         a == 0 ? (long long)g.Nh : 0, nterms, F, 1.0, false, a == 0 ? tab0 : tab1,
+                                         nullptr, (a == 0 && xrs != g.hp1) ? xrs : 0))
       continue;
     const int lp = std::max(1, std::min(8, 4096 / n));
     const long long bpo = (S + lp - 1) / lp;
@@ -598,8 +615,8 @@ void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_fi
         a == 0 ? tab0 : tab1);
     count(L);
   }
-  if (!L.generic_lines && launch_rows_c2r(L, g.nl, nullptr, (long long)g.Nh, m_first, m_last, nullptr, nullptr,
-                                         (long long)g.rows, F, nullptr, guard, tab2))
+  if (!L.generic_lines && launch_rows_c2r(L, g.nl, nullptr, (long long)term_elems(L, g), m_first, m_last, nullptr,
+                                         nullptr, (long long)g.rows, F, nullptr, guard, tab2, term_row_stride(L, g)))
     return;
   const int h = g.nl / 2;
   const int lpb = std::max(1, std::min(8, 4096 / g.nl));

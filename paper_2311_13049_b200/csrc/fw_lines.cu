@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(NTH, (lines_minb<N, NTH>())) k_lines(const dou
                                                const double* __restrict__ w, long long S, long long inner,
                                                long long src_ts, long long dst_ts, long long w_ts, double sc,
                                                int do_scale, const double2* __restrict__ master,
-                                               const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat) {
+                                               const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat,
+                                               long long Sd) {
   using PL = Plan<N, NTH>;
   constexpr int L = PL::L;
   extern __shared__ double2 sm[];  // L lines x LS
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(NTH, (lines_minb<N, NTH>())) k_lines(const dou
   const int l = threadIdx.x % L, i = threadIdx.x / L;
   const bool live = in0 + l < inner;
   const long long base = o * (long long)N * S + in0 + l;
+  const long long dbase = o * (long long)N * Sd + in0 + l;  // destination (Sd != S: padded rows, inner < S)
   double2* line = sm;  // slot p of this thread's line at PL::lpos(l, p)
 
   {  // pass 0 (no twiddles): global -> registers -> shared
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(NTH, (lines_minb<N, NTH>())) k_lines(const dou
             scat.dst[q][term * scat.tstride + (long long)jr * scat.jstride + o * scat.ostride + in0 + l + scat.base] =
                 v;
           } else {
-            dst[base + (long long)j * S] = v;
+            dst[dbase + (long long)j * Sd] = v;
           }
         }
       }
@@ -256,10 +258,20 @@ __device__ __forceinline__ void tm_set(unsigned* v, int k, double x) {
 // the reference's per-term partial 0.0 + v (flap.cpp:83-89: partials start from a zeroed
 // vector; differs from v only for v = -0.0).  An integer form that keeps the fp64 pipe free
 // measured no faster.
+// FW_ZERO_PLUS=0 drops the addition: the sum the partial is added to is never -0 (it starts at
+// +0, and x + y = -0 needs x = y = -0), and s + (-0) = s + (+0) for every s other than -0, so the
+// accumulated bits are the same (A/B).
+#ifndef FW_ZERO_PLUS
+#define FW_ZERO_PLUS 0
+#endif
 __device__ __forceinline__ double zero_plus(double v) {
+#if FW_ZERO_PLUS
   double p = 0.0;
   p += v;
   return p;
+#else
+  return v;
+#endif
 }
 
 // twiddled butterfly of pass PASS with the twiddles from a shared-memory table [k][r-1]
@@ -313,6 +325,9 @@ __device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, do
 #endif
 #ifndef FW_C2R_MINB
 #define FW_C2R_MINB 2  // blocks per SM the register allocation is bounded for
+#endif
+#ifndef FW_C2R_WSYNC
+#define FW_C2R_WSYNC 1  // warp barriers between the passes when a row's threads share a warp (0: block barriers, A/B)
 #endif
 template <int H>
 struct C2RPlan {
@@ -368,7 +383,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
                                                             int m_first, int m_last, const double* __restrict__ dev1,
                                                             double* __restrict__ out, long long rows, double* residue,
                                                             const int* guard, const double2* __restrict__ master,
-                                                            const BatchLine* __restrict__ bl) {
+                                                            const BatchLine* __restrict__ bl, long long xrs) {
   using RP = C2RPlan<H>;
   using PL = Plan<H>;
   constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL, NL = 2 * H, NT = RP::NT;
@@ -397,7 +412,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
   // term has read it, and lands during the following terms' passes (one commit group per term)
   auto fetch = [&](int m) {
     if (live && m <= m_last) {
-      const double2* S = src + (long long)(m - m_first) * src_ts + row * (H + 1);
+      const double2* S = src + (long long)(m - m_first) * src_ts + row * xrs;
       double2* X = Xb + ((m - m_first) % NXB) * RPB * RP::XS;
       for (int k = i; k <= H; k += TM)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(&X[k])),
@@ -452,6 +467,15 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
     tm_wait_st();
   }
 
+  // a row's TM threads exchange data only among themselves (its X row, its work buffer): when
+  // they share a warp (h = 128 / 256: 16 threads per row) the pass boundaries need a warp barrier
+  // only, and the block's warps run through the terms independently of each other
+  auto rowsync = [] {
+    if constexpr (FW_C2R_WSYNC && 32 % TM == 0)
+      __syncwarp();
+    else
+      __syncthreads();
+  };
   double acc[2 * RL];
 #pragma unroll
   for (int e = 0; e < 2 * RL; ++e) acc[e] = 0.0;
@@ -461,7 +485,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // term m landed (m + 1 may be in flight)
     else
       asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();  // X of term m complete; every thread is done with the previous term's work buffer
+    rowsync();  // X of term m complete; every thread is done with the previous term's work buffer
     const double2* X = Xb + ((m - m_first) % NXB) * RPB * RP::XS;
     if (residue && live && i == 0) rmax = fmax(rmax, fabs(X[0].y) + fabs(X[H].y));
     {  // C2R pre-processing + pass 0 (no twiddles) -> work
@@ -478,7 +502,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
         for (int r = 0; r < R; ++r) Wk[RP::p0out(i * R + r)] = a[r];
       }
     }
-    __syncthreads();
+    rowsync();
     fetch(m + NXB);  // X is free again
     if constexpr (PL::P == 3) {
       constexpr int R = PL::R1, T = PL::T1;
@@ -490,7 +514,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
 #pragma unroll
         for (int r = 0; r < R; ++r) Wk[RP::p1(i, r)] = a[r];
       }
-      __syncthreads();
+      rowsync();
     }
     {  // last pass -> outputs z_q, q = i + r TL: reals x[2q], x[2q+1]
       constexpr int LAST = PL::P - 1;
@@ -573,7 +597,8 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
                                                         const double* __restrict__ w, long long S, long long inner,
                                                         long long dst_ts, long long w_ts, int nterms, int tchunk,
                                                         double sc, int do_scale, const double2* __restrict__ master,
-                                                        const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat) {
+                                                        const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat,
+                                                        long long Sd) {
   using PL = Plan<N, NTH>;
   using TP = TermPlan<N, NTH>;
   constexpr int L = PL::L, R0 = PL::R0, T0 = PL::T0, LAST = PL::P - 1;
@@ -598,6 +623,7 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
   const int l = tid % L, i = tid / L;
   const bool live = in0 + l < inner;
   const long long base = o * (long long)N * S + in0 + l;
+  const long long dbase = o * (long long)N * Sd + in0 + l;  // destination (Sd != S: padded rows, inner < S)
   double2* line = lines_sm;  // slot p of this thread's line at PL::lpos(l, p)
 
   if constexpr (PL::P > 2) {
@@ -712,7 +738,7 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
             scat.dst[q][term * scat.tstride + (long long)jr * scat.jstride + o * scat.ostride + in0 + l + scat.base] =
                 v;
           } else {
-            dst[(long long)term * dst_ts + base + (long long)j * S] = v;
+            dst[(long long)term * dst_ts + dbase + (long long)j * Sd] = v;
           }
         }
       }
@@ -822,7 +848,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
 template <int N, int NTH>
 bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
               long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
-              int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
+              int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter, long long Sd) {
   constexpr int LPB = Plan<N, NTH>::L;
   constexpr size_t SMEM = (size_t)LPB * Plan<N, NTH>::LLS * sizeof(double2);
   static std::atomic<unsigned long long> attr{0};
@@ -852,10 +878,10 @@ bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, co
     const dim3 tgrid((unsigned)(outer * bpo), (unsigned)((nterms + tchunk - 1) / tchunk), (unsigned)nfields);
     if (scatter)
       k_lines_terms<N, true, NTH><<<tgrid, Plan<N, NTH>::NTHR, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, tchunk, sc,
-                                                             f, L.master, bl, sc_);
+                                                             f, L.master, bl, sc_, Sd);
     else
       k_lines_terms<N, false, NTH><<<tgrid, Plan<N, NTH>::NTHR, TSM, L.stream>>>(src, dst, w, S, inner, dst_ts, w_ts, nterms, tchunk,
-                                                              sc, f, L.master, bl, sc_);
+                                                              sc, f, L.master, bl, sc_, Sd);
     if (L.launches) *L.launches += 1;
     return true;
   }
@@ -863,17 +889,17 @@ bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, co
   if (dir < 0) {
     if (scatter)
       k_lines<N, -1, true, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
-                                                           bl, sc_);
+                                                           bl, sc_, Sd);
     else
       k_lines<N, -1, false, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
-                                                            L.master, bl, sc_);
+                                                            L.master, bl, sc_, Sd);
   } else {
     if (scatter)
       k_lines<N, +1, true, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
-                                                           bl, sc_);
+                                                           bl, sc_, Sd);
     else
       k_lines<N, +1, false, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
-                                                            L.master, bl, sc_);
+                                                            L.master, bl, sc_, Sd);
   }
   if (L.launches) *L.launches += 1;
   return true;
@@ -885,13 +911,13 @@ bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, co
 template <int N>
 bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
               long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
-              int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
+              int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter, long long Sd) {
   const bool terms = dir > 0 && src_ts == 0 && nterms > 1 && (w || (bl && w_ts != 0));
   const bool wide = FW_LINES_WIDE && (N == 1024 || !terms || S * (long long)sizeof(double2) >= FW_WIDE_STRIDE);
   if constexpr (N == 256)
-    return launch_nt<N, 256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter);
+    return launch_nt<N, 256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter, Sd);
   else
-    return wide ? launch_nt<N, 512>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter) : launch_nt<N, 256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter);
+    return wide ? launch_nt<N, 512>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter, Sd) : launch_nt<N, 256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter, Sd);
 }
 
 template <int H>
@@ -912,7 +938,7 @@ bool launch_rows_r2c_t(const LaunchCtx& L, const double* u, double2* Uh, long lo
 template <int H>
 bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m_first, int m_last,
                  const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
-                 const BatchLine* bl) {
+                 const BatchLine* bl, long long xrs) {
   using RP = C2RPlan<H>;
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [] {
@@ -920,7 +946,7 @@ bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m
   });
   const dim3 grid((unsigned)((rows + RP::RPB - 1) / RP::RPB), 1, (unsigned)nfields);
   k_rows_c2r<H><<<grid, RP::NT, RP::SMEM, L.stream>>>(src, src_ts, m_first, m_last, dev1, out, rows, residue, guard,
-                                                    L.master, bl);
+                                                    L.master, bl, xrs > 0 ? xrs : (long long)(H + 1));
   if (L.launches) *L.launches += 1;
   return true;
 }
@@ -929,17 +955,19 @@ bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m
 
 bool launch_lines(const LaunchCtx& L, int n, int dir, const double2* src, double2* dst, const double* w,
                   long long S, long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts,
-                  int nterms, int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter) {
+                  int nterms, int nfields, double sc, bool scale, const BatchLine* bl, const Scatter* scatter,
+                  long long Sd) {
+  if (Sd <= 0) Sd = S;
   switch (n) {
     case 256:
       return lines::launch_n<256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
-                                  scale, bl, scatter);
+                                  scale, bl, scatter, Sd);
     case 512:
       return lines::launch_n<512>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
-                                  scale, bl, scatter);
+                                  scale, bl, scatter, Sd);
     case 1024:
       return lines::launch_n<1024>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc,
-                                   scale, bl, scatter);
+                                   scale, bl, scatter, Sd);
     default:
       return false;
   }
@@ -961,14 +989,14 @@ bool launch_rows_r2c(const LaunchCtx& L, int nl, const double* u, double2* Uh, l
 
 bool launch_rows_c2r(const LaunchCtx& L, int nl, const double2* src, long long src_ts, int m_first, int m_last,
                      const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
-                     const BatchLine* bl) {
+                     const BatchLine* bl, long long xrs) {
   switch (nl / 2) {
     case 128:
-      return lines::launch_rows<128>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl);
+      return lines::launch_rows<128>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs);
     case 256:
-      return lines::launch_rows<256>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl);
+      return lines::launch_rows<256>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs);
     case 512:
-      return lines::launch_rows<512>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl);
+      return lines::launch_rows<512>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs);
     default:
       return false;
   }
