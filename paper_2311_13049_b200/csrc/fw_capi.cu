@@ -243,6 +243,9 @@ struct fw_ctx_s {
   int steps_per_launch = 0;                   // FW_STEPS_PER_LAUNCH: seismic steps per persistent launch (0 = all)
   bool step2d_tm = false;                     // FW_STEP2D_TM=1: time-multiplexed persistent kernel (A/B)
   int batch_fields = 0;                       // FW_BATCH_FIELDS: fields per batched pipeline (0 = all that fit)
+  int batch_l2_mb = 0;                        // FW_BATCH_L2_MB: term spectra a batched chunk keeps in L2 (0 = no term chunks, the
+                                              // default: measured slower at every chunk size)
+  int batch_group = 8;                        // FW_BATCH_GROUP: fields per L2-resident chunk
   unsigned long long* counters = nullptr;     // persistent-kernel counters (2 sets)
   unsigned long long* trace = nullptr;        // FW_TRACE=1: persistent-kernel watchdog records (device view)
   unsigned long long* trace_host = nullptr;   //   ... the same buffer, mapped host memory (survives a trap)
@@ -326,6 +329,10 @@ int fw_ctx_create(int device, fw_ctx* out) {
   c->dbg = dg ? atoi(dg) : 0;
   const char* bf = getenv("FW_BATCH_FIELDS");
   c->batch_fields = bf ? std::max(0, atoi(bf)) : 0;
+  const char* bl2 = getenv("FW_BATCH_L2_MB");
+  if (bl2) c->batch_l2_mb = std::max(0, atoi(bl2));
+  const char* bgr = getenv("FW_BATCH_GROUP");
+  if (bgr) c->batch_group = std::max(1, atoi(bgr));
   const char* tm = getenv("FW_STEP2D_TM");
   c->step2d_tm = tm && tm[0] == '1';
   const char* spl = getenv("FW_STEPS_PER_LAUNCH");
@@ -815,7 +822,60 @@ int fw_apply_batch_device(fw_op const* ops, int nfields, const double* const* u_
   fw_ctx ctx = o0->ctx;
   const fw::GridGeom& g = o0->g;
   const int m_last = o0->constant_order ? 0 : o0->M;
-  const size_t per_field = (size_t)(m_last + 1) * fw::term_elems(ctx->L(), g) * sizeof(double2);
+  // L2-resident chunks (FW_BATCH_L2_MB > 0; off by default): the all-terms spectra of the whole
+  // batch (64 x 17 x 2.1 MB at C5) make a round trip through HBM between the axis-0 pass and the
+  // row C2R.  In this mode a group of fields runs the two kernels over a few terms at a time,
+  // sized so that the chunk's spectra (written once, read once, the scratch reused by the next
+  // chunk) stay in the 126 MB L2; the row C2R resumes the ascending-m recombination from the
+  // partial sums of the earlier chunks (same order of additions, same bits).  Measured at C5
+  // (M = 16): 1.72 ms unchunked against 2.2 - 5.4 ms for 56 - 400 MB chunks -- the small launches
+  // lose more (per-block set-up amortised over 1-3 terms instead of 17, partial waves) than the
+  // HBM round trip costs, so the batch-wide pipeline stays the default.
+  const size_t term_bytes = fw::term_elems(ctx->L(), g) * sizeof(double2);
+  if (ctx->batch_l2_mb > 0 && ctx->batch_fields == 0 && m_last >= 1 && fw::rows_resumable(ctx->L(), g) &&
+      (size_t)nfields * (size_t)(m_last + 1) * term_bytes > ((size_t)ctx->batch_l2_mb << 20)) {
+    const int Fg = std::min(nfields, ctx->batch_group);
+    const int Tc = (int)std::max<size_t>(1, std::min<size_t>((size_t)(m_last + 1),
+                                                              ((size_t)ctx->batch_l2_mb << 20) / ((size_t)Fg * term_bytes)));
+    const int nchunk = (m_last + Tc) / Tc;
+    void *uh = nullptr, *T = nullptr, *tab = nullptr;
+    FW_TRY(ctx->get_scratch(SLOT_BUH, (size_t)Fg * g.Nh * sizeof(double2), &uh));
+    FW_TRY(ctx->get_scratch(SLOT_BT, (size_t)Fg * Tc * term_bytes, &T));
+    const int ngroup = (nfields + Fg - 1) / Fg;
+    const size_t per_group = (size_t)(4 + nchunk) * Fg;  // R2C, forward C2C, axes 1.., C2R, axis 0 per chunk
+    FW_TRY(ctx->get_scratch(SLOT_BTAB, (size_t)ngroup * per_group * sizeof(fw::BatchLine), &tab));
+    fw::BatchLine* dt = static_cast<fw::BatchLine*>(tab);
+    std::vector<fw::BatchLine> h((size_t)ngroup * per_group);
+    for (int gi = 0; gi < ngroup; ++gi) {
+      const int f0 = gi * Fg, F = std::min(Fg, nfields - f0);
+      fw::BatchLine* hg = h.data() + (size_t)gi * per_group;
+      for (int i = 0; i < F; ++i) {
+        const fw_op o = ops[f0 + i];
+        double2* Uh = static_cast<double2*>(uh) + (size_t)i * g.Nh;
+        double2* Ti = reinterpret_cast<double2*>(static_cast<char*>(T) + (size_t)i * Tc * term_bytes);
+        hg[0 * Fg + i] = {u_dev[f0 + i], Uh, nullptr, nullptr, nullptr};       // R2C
+        hg[1 * Fg + i] = {Uh, Uh, nullptr, nullptr, nullptr};                  // forward C2C
+        hg[2 * Fg + i] = {Ti, Ti, nullptr, nullptr, nullptr};                  // inverse axes 1..d-2
+        hg[3 * Fg + i] = {Ti, nullptr, nullptr, o->dev1, out_dev[f0 + i]};    // C2R + recombination
+        for (int c = 0; c < nchunk; ++c)                                       // inverse axis 0 (x w_m) of chunk c
+          hg[(size_t)(4 + c) * Fg + i] = {Uh, Ti, o->w + (size_t)c * Tc * g.Nh, nullptr, nullptr};
+      }
+    }
+    FW_CUDA(cudaMemcpyAsync(dt, h.data(), h.size() * sizeof(fw::BatchLine), cudaMemcpyHostToDevice, ctx->stream));
+    auto L = ctx->L();
+    for (int gi = 0; gi < ngroup; ++gi) {
+      const int F = std::min(Fg, nfields - gi * Fg);
+      const fw::BatchLine* dg = dt + (size_t)gi * per_group;
+      fw::launch_forward_batch(L, g, F, dg, dg + Fg, true);
+      for (int c = 0; c < nchunk; ++c) {
+        const int m0 = c * Tc, m1 = std::min(m_last, m0 + Tc - 1);
+        fw::launch_inverse_batch(L, g, F, m0, m1, dg + (size_t)(4 + c) * Fg, dg + 2 * Fg, dg + 3 * Fg, nullptr, c > 0);
+      }
+    }
+    FW_CUDA(cudaGetLastError());
+    return FW_OK;
+  }
+  const size_t per_field = (size_t)(m_last + 1) * term_bytes;
   // fields per batched pipeline: the all-terms spectra of a chunk live in scratch (up to 16 GiB of
   // the 180 GB HBM); chunks are balanced (64 fields at M = 16 fit in one chunk; an unbalanced
   // 59 + 5 split under a 2 GiB cap left the GPU idle in the small chunk)

@@ -128,6 +128,9 @@ void launch_inverse(const LaunchCtx& L, const GridGeom& g, const InverseArgs& a)
 // Spectrum layout.
 long long term_row_stride(const LaunchCtx& L, const GridGeom& g);
 inline size_t term_elems(const LaunchCtx& L, const GridGeom& g) { return g.rows * (size_t)term_row_stride(L, g); }
+// true when the register-resident kernels serve every pass of the grid's inverse, i.e. the row
+// C2R can resume a recombination from the partial sums of earlier term chunks
+bool rows_resumable(const LaunchCtx& L, const GridGeom& g);
 
 constexpr int kNoBlowup = 0x7fffffff;
 
@@ -193,9 +196,11 @@ void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const Ba
                           const BatchLine* tab_c2c, bool scale);
 // inverse + recombination for F fields of one grid and term range:
 // tab0[f] = {Uh_f, T_f, w_f + m_first Nh}, tab1[f] = {T_f, T_f} (axes 1..d-2), tab2[f] = {T_f, -, -, dev1_f, out_f}
+// (resume: the terms before m_first were recombined into out_f by an earlier launch -- term
+// chunks sized so that a chunk's spectra stay in L2 between the two kernels)
 void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_first, int m_last,
                           const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2,
-                          const int* guard = nullptr);
+                          const int* guard = nullptr, bool resume = false);
 
 // fused transpose: the last pass of a line C2C writes output element j of line (o, in), term t
 // to dst[q] + t tstride + (j - q blk) jstride + o ostride + in + base, q = j / blk -- the
@@ -223,7 +228,7 @@ bool launch_rows_r2c(const LaunchCtx& L, int nl, const double* u, double2* Uh, l
 // (xrs: row stride of src in complex elements, 0 = nl/2 + 1)
 bool launch_rows_c2r(const LaunchCtx& L, int nl, const double2* src, long long src_ts, int m_first, int m_last,
                      const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
-                     const BatchLine* bl, long long xrs = 0);
+                     const BatchLine* bl, long long xrs = 0, int resume = 0);
 
 // stage entry points (distributed orchestration on local sub-arrays)
 void launch_stage_r2c(const LaunchCtx& L, const GridGeom& g, const double* u, double2* H, double scale, bool do_scale);

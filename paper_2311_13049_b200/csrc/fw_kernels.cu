@@ -466,6 +466,14 @@ void launch_inverse(const LaunchCtx& L, const GridGeom& g, const InverseArgs& a)
   c2r_accum(L, g, a.T, tts, nullptr, 0, a.m_first, a.m_last, a.dev1, a.out, a.residue, a.guard, xrs);
 }
 
+bool rows_resumable(const LaunchCtx& L, const GridGeom& g) {
+  const int h = g.nl / 2;
+  if (L.generic_lines || g.d < 2 || !(h == 128 || h == 256 || h == 512)) return false;
+  for (int a = 0; a <= g.d - 2; ++a)
+    if (!(g.J[a] == 256 || g.J[a] == 512 || g.J[a] == 1024)) return false;
+  return true;
+}
+
 long long term_row_stride(const LaunchCtx& L, const GridGeom& g) {
   const int h = g.nl / 2;
   const bool lines2d = FW_TERM_PAD && g.d == 2 && !L.generic_lines && (g.J[0] == 256 || g.J[0] == 512 || g.J[0] == 1024) &&
@@ -594,7 +602,8 @@ void launch_forward_batch(const LaunchCtx& L, const GridGeom& g, int F, const Ba
 }
 
 void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_first, int m_last,
-                          const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2, const int* guard) {
+                          const BatchLine* tab0, const BatchLine* tab1, const BatchLine* tab2, const int* guard,
+                          bool resume) {
   const int nterms = m_last - m_first + 1;
   for (int a = 0; a <= g.d - 2; ++a) {
     const int n = g.J[a];
@@ -616,7 +625,8 @@ void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_fi
     count(L);
   }
   if (!L.generic_lines && launch_rows_c2r(L, g.nl, nullptr, (long long)term_elems(L, g), m_first, m_last, nullptr,
-                                         nullptr, (long long)g.rows, F, nullptr, guard, tab2, term_row_stride(L, g)))
+                                         nullptr, (long long)g.rows, F, nullptr, guard, tab2, term_row_stride(L, g),
+                                         resume ? 1 : 0))
     return;
   const int h = g.nl / 2;
   const int lpb = std::max(1, std::min(8, 4096 / g.nl));

@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
                                                             int m_first, int m_last, const double* __restrict__ dev1,
                                                             double* __restrict__ out, long long rows, double* residue,
                                                             const int* guard, const double2* __restrict__ master,
-                                                            const BatchLine* __restrict__ bl, long long xrs) {
+                                                            const BatchLine* __restrict__ bl, long long xrs, int resume) {
   using RP = C2RPlan<H>;
   using PL = Plan<H>;
   constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL, NL = 2 * H, NT = RP::NT;
@@ -463,6 +463,19 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
         tm_set(v, 2 * rr + 1, d.y);
       }
       tm_st16(tdev + 16 * c4, v);
+      if (resume && m_first > 1) {
+        // a later chunk of the operator's terms: the running power (s-s0)^{m_first-1} by the same
+        // recurrence the earlier chunks ran, (s-s0)^m = (s-s0)^{m-1} (s-s0) (flap.cpp:131)
+        unsigned pw[16];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double d1 = tm_get(v, e);
+          double d = d1;
+          for (int m = 2; m < m_first; ++m) d = d * d1;
+          tm_set(pw, e, d);
+        }
+        tm_st16(tpow + 16 * c4, pw);
+      }
     }
     tm_wait_st();
   }
@@ -479,6 +492,14 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
   double acc[2 * RL];
 #pragma unroll
   for (int e = 0; e < 2 * RL; ++e) acc[e] = 0.0;
+  if (resume && live) {  // partial sums of the operator's earlier terms (written by the previous chunk's launch)
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const double2 o = reinterpret_cast<const double2*>(out + row * NL)[i + r * TL];
+      acc[2 * r] = o.x;
+      acc[2 * r + 1] = o.y;
+    }
+  }
   double rmax = 0.0;
   for (int m = m_first; m <= m_last; ++m) {
     if (NXB > 1)
@@ -938,7 +959,7 @@ bool launch_rows_r2c_t(const LaunchCtx& L, const double* u, double2* Uh, long lo
 template <int H>
 bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m_first, int m_last,
                  const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
-                 const BatchLine* bl, long long xrs) {
+                 const BatchLine* bl, long long xrs, int resume) {
   using RP = C2RPlan<H>;
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [] {
@@ -946,7 +967,7 @@ bool launch_rows(const LaunchCtx& L, const double2* src, long long src_ts, int m
   });
   const dim3 grid((unsigned)((rows + RP::RPB - 1) / RP::RPB), 1, (unsigned)nfields);
   k_rows_c2r<H><<<grid, RP::NT, RP::SMEM, L.stream>>>(src, src_ts, m_first, m_last, dev1, out, rows, residue, guard,
-                                                    L.master, bl, xrs > 0 ? xrs : (long long)(H + 1));
+                                                    L.master, bl, xrs > 0 ? xrs : (long long)(H + 1), resume);
   if (L.launches) *L.launches += 1;
   return true;
 }
@@ -989,14 +1010,14 @@ bool launch_rows_r2c(const LaunchCtx& L, int nl, const double* u, double2* Uh, l
 
 bool launch_rows_c2r(const LaunchCtx& L, int nl, const double2* src, long long src_ts, int m_first, int m_last,
                      const double* dev1, double* out, long long rows, int nfields, double* residue, const int* guard,
-                     const BatchLine* bl, long long xrs) {
+                     const BatchLine* bl, long long xrs, int resume) {
   switch (nl / 2) {
     case 128:
-      return lines::launch_rows<128>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs);
+      return lines::launch_rows<128>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs, resume);
     case 256:
-      return lines::launch_rows<256>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs);
+      return lines::launch_rows<256>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs, resume);
     case 512:
-      return lines::launch_rows<512>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs);
+      return lines::launch_rows<512>(L, src, src_ts, m_first, m_last, dev1, out, rows, nfields, residue, guard, bl, xrs, resume);
     default:
       return false;
   }

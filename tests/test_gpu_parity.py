@@ -431,6 +431,42 @@ def test_batched_apply_equals_per_field(J, nf):
         assert np.array_equal(x, op.apply(u))
 
 
+def chunk_context(l2_mb, group):
+    import os
+
+    m = fw()
+    os.environ["FW_BATCH_L2_MB"] = str(l2_mb)
+    os.environ["FW_BATCH_GROUP"] = str(group)
+    try:
+        return m.Context(0)
+    finally:
+        del os.environ["FW_BATCH_L2_MB"]
+        del os.environ["FW_BATCH_GROUP"]
+
+
+@pytest.mark.parametrize("J,nf,M,l2_mb,group", [((512, 512), 5, 9, 5, 2), ((256, 256), 7, 6, 2, 3),
+                                                ((256, 256, 256), 2, 3, 300, 1)])
+def test_batched_apply_in_l2_chunks_equals_per_field(J, nf, M, l2_mb, group):
+    """The batched pipeline in L2-resident chunks (groups of fields x a few terms at a time; the
+    row C2R resumes the ascending-m recombination from the earlier chunks' partial sums and
+    regenerates the running power (s-s0)^{m-1}): identical bits to one apply per field.  The
+    budgets force chunks of 1-2 terms, ragged last chunks and a ragged last field group."""
+    m = fw()
+    lo, hi = tuple(-4.0 for _ in J), tuple(4.0 for _ in J)
+    rng = np.random.default_rng(23 + len(J))
+    ctx = chunk_context(l2_mb, group)
+    g = grid_of(J, lo, hi)
+    ops, ops_c, us = [], [], []
+    for f in range(nf):
+        s = 0.9 + 0.2 * rng.random(J)
+        ops.append(m.build_expansion(m.OrderField(g, s), M))
+        ops_c.append(m.build_expansion(m.OrderField(g, s), M, ctx=ctx))
+        us.append(rng.standard_normal(J))
+    got = m.apply_batch(ops_c, us)
+    for op, u, x in zip(ops, us, got):
+        assert np.array_equal(x, op.apply(u))
+
+
 def lines_context():
     import os
 
