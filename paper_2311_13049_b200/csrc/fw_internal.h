@@ -126,8 +126,13 @@ void launch_inverse(const LaunchCtx& L, const GridGeom& g, const InverseArgs& a)
 // the rows of T from J1/2 + 1 (odd) to a multiple of 8 elements, so that the strided 128-B runs
 // of the axis-0 pass and the rows the C2R fetches are 128-B aligned; everything else keeps the
 // Spectrum layout.
-long long term_row_stride(const LaunchCtx& L, const GridGeom& g);
-inline size_t term_elems(const LaunchCtx& L, const GridGeom& g) { return g.rows * (size_t)term_row_stride(L, g); }
+#ifndef FW_TERM_PAD
+#define FW_TERM_PAD 1  // 2D term scratch rows padded to 128 B (0: Spectrum layout; A/B)
+#endif
+// (nterms: terms of the launch; a single term takes the one-term line kernel, which keeps the
+// Spectrum layout.  term_elems = the allocation per term, an upper bound for every launch.)
+long long term_row_stride(const LaunchCtx& L, const GridGeom& g, int nterms);
+inline size_t term_elems(const LaunchCtx& L, const GridGeom& g) { return g.rows * (size_t)term_row_stride(L, g, 2); }
 // true when the register-resident kernels serve every pass of the grid's inverse, i.e. the row
 // C2R can resume a recombination from the partial sums of earlier term chunks
 bool rows_resumable(const LaunchCtx& L, const GridGeom& g);

@@ -430,9 +430,6 @@ void launch_forward(const LaunchCtx& L, const GridGeom& g, const double* u, doub
     c2c_axis(L, g, a, -1, Uh, Uh, nullptr, 0, 0, 0, 1, inv, scale && a == 0);
 }
 
-#ifndef FW_TERM_PAD
-#define FW_TERM_PAD 1  // 2D term scratch rows padded to 128 B (0: Spectrum layout; A/B)
-#endif
 static void c2r_accum(const LaunchCtx& L, const GridGeom& g, const double2* src, long long src_ts, const double* w,
                       long long w_ts, int m_first, int m_last, const double* dev1, double* out, double* residue,
                       const int* guard, long long xrs = 0) {
@@ -457,8 +454,8 @@ void launch_inverse(const LaunchCtx& L, const GridGeom& g, const InverseArgs& a)
     return;
   }
   // axis 0 for all terms: T[t] = IFFT_0(w_{m_first+t} .* Uh); T's rows may be padded (term_row_stride)
-  const long long xrs = term_row_stride(L, g);
-  const long long tts = (long long)term_elems(L, g);
+  const long long xrs = term_row_stride(L, g, nterms);
+  const long long tts = (long long)g.rows * xrs;
   c2c_axis(L, g, 0, +1, a.Uh, a.T, a.w + (long long)a.m_first * g.Nh, 0, tts, (long long)g.Nh, nterms, 1.0, false,
            xrs != g.hp1 ? xrs : 0);
   for (int ax = 1; ax <= g.d - 2; ++ax)
@@ -474,9 +471,9 @@ bool rows_resumable(const LaunchCtx& L, const GridGeom& g) {
   return true;
 }
 
-long long term_row_stride(const LaunchCtx& L, const GridGeom& g) {
+long long term_row_stride(const LaunchCtx& L, const GridGeom& g, int nterms) {
   const int h = g.nl / 2;
-  const bool lines2d = FW_TERM_PAD && g.d == 2 && !L.generic_lines && (g.J[0] == 256 || g.J[0] == 512 || g.J[0] == 1024) &&
+  const bool lines2d = FW_TERM_PAD && nterms > 1 && g.d == 2 && !L.generic_lines && (g.J[0] == 256 || g.J[0] == 512 || g.J[0] == 1024) &&
                        (h == 128 || h == 256 || h == 512);
   return lines2d ? (long long)((g.hp1 + 7) & ~7) : (long long)g.hp1;
 }
@@ -611,8 +608,8 @@ void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_fi
     for (int b = a + 1; b <= g.d - 2; ++b) S *= g.J[b];
     long long outer = 1;
     for (int b = 0; b < a; ++b) outer *= g.J[b];
-    const long long ts = (long long)term_elems(L, g);  // T's term stride (rows padded for 2D grids)
-    const long long xrs = term_row_stride(L, g);
+    const long long xrs = term_row_stride(L, g, nterms);
+    const long long ts = (long long)g.rows * xrs;  // T's term stride (rows padded for 2D grids)
     if (!L.generic_lines && launch_lines(L, n, +1, nullptr, nullptr, nullptr, S, outer, S, a == 0 ? 0 : ts, ts,
                                          a == 0 ? (long long)g.Nh : 0, nterms, F, 1.0, false, a == 0 ? tab0 : tab1,
                                          nullptr, (a == 0 && xrs != g.hp1) ? xrs : 0))
@@ -624,9 +621,9 @@ void launch_inverse_batch(const LaunchCtx& L, const GridGeom& g, int F, int m_fi
         a == 0 ? tab0 : tab1);
     count(L);
   }
-  if (!L.generic_lines && launch_rows_c2r(L, g.nl, nullptr, (long long)term_elems(L, g), m_first, m_last, nullptr,
-                                         nullptr, (long long)g.rows, F, nullptr, guard, tab2, term_row_stride(L, g),
-                                         resume ? 1 : 0))
+  if (!L.generic_lines && launch_rows_c2r(L, g.nl, nullptr, (long long)g.rows * term_row_stride(L, g, nterms), m_first,
+                                         m_last, nullptr, nullptr, (long long)g.rows, F, nullptr, guard, tab2,
+                                         term_row_stride(L, g, nterms), resume ? 1 : 0))
     return;
   const int h = g.nl / 2;
   const int lpb = std::max(1, std::min(8, 4096 / g.nl));

@@ -114,8 +114,11 @@ __device__ __forceinline__ void bfly(double2* a, int i, const double2* __restric
 
 // blocks per SM the register allocation of k_lines<N> is bounded for (shared memory allows 3
 // at N = 256, 6 at N = 512 / 1024)
+#ifndef FW_LINES_NTH256
+#define FW_LINES_NTH256 128  // threads per block of the 256-point line passes: 8 lines per block (256: 16 lines; A/B)
+#endif
 #ifndef FW_LINES_MINB256
-#define FW_LINES_MINB256 3
+#define FW_LINES_MINB256 3  // (of FW_LINES_NTH256 threads)
 #endif
 #ifndef FW_LINES_MINB512
 #define FW_LINES_MINB512 4
@@ -136,8 +139,7 @@ __global__ void __launch_bounds__(NTH, (lines_minb<N, NTH>())) k_lines(const dou
                                                const double* __restrict__ w, long long S, long long inner,
                                                long long src_ts, long long dst_ts, long long w_ts, double sc,
                                                int do_scale, const double2* __restrict__ master,
-                                               const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat,
-                                               long long Sd) {
+                                               const BatchLine* __restrict__ bl, const __grid_constant__ Scatter scat) {
   using PL = Plan<N, NTH>;
   constexpr int L = PL::L;
   extern __shared__ double2 sm[];  // L lines x LS
@@ -156,7 +158,6 @@ __global__ void __launch_bounds__(NTH, (lines_minb<N, NTH>())) k_lines(const dou
   const int l = threadIdx.x % L, i = threadIdx.x / L;
   const bool live = in0 + l < inner;
   const long long base = o * (long long)N * S + in0 + l;
-  const long long dbase = o * (long long)N * Sd + in0 + l;  // destination (Sd != S: padded rows, inner < S)
   double2* line = sm;  // slot p of this thread's line at PL::lpos(l, p)
 
   {  // pass 0 (no twiddles): global -> registers -> shared
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(NTH, (lines_minb<N, NTH>())) k_lines(const dou
             scat.dst[q][term * scat.tstride + (long long)jr * scat.jstride + o * scat.ostride + in0 + l + scat.base] =
                 v;
           } else {
-            dst[dbase + (long long)j * Sd] = v;
+            dst[base + (long long)j * S] = v;
           }
         }
       }
@@ -326,6 +327,15 @@ __device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, do
 #ifndef FW_C2R_MINB
 #define FW_C2R_MINB 2  // blocks per SM the register allocation is bounded for
 #endif
+#ifndef FW_C2R_RPB256
+#define FW_C2R_RPB256 8  // rows per block of the h = 256 row C2R (0: as many as fit two blocks per SM, 12)
+#endif
+#ifndef FW_C2R_MINB256
+#define FW_C2R_MINB256 FW_C2R_MINB
+#endif
+#ifndef FW_C2R_MINB128
+#define FW_C2R_MINB128 3  // the same for the h = 128 row C2R (8-row blocks of 128 threads)
+#endif
 #ifndef FW_C2R_WSYNC
 #define FW_C2R_WSYNC 1  // warp barriers between the passes when a row's threads share a warp (0: block barriers, A/B)
 #endif
@@ -362,8 +372,8 @@ struct C2RPlan {
                                   : (int)((CAP - TWN * sizeof(double2)) / ROWB);
   // h = 128: half-size blocks (8 rows, 4 warps), four per SM, X double-buffered (measured at C3:
   // 6.34 -> ~6.0 ms per step against 16-row blocks, two per SM)
-  static constexpr int RPB = H == 128 ? FW_C2R_RPB128 : RPB0;
-  static constexpr int MINB = H == 128 ? 4 : FW_C2R_MINB;
+  static constexpr int RPB = H == 128 ? FW_C2R_RPB128 : (H == 256 && FW_C2R_RPB256 > 0) ? FW_C2R_RPB256 : RPB0;
+  static constexpr int MINB = H == 128 ? FW_C2R_MINB128 : H == 256 ? FW_C2R_MINB256 : FW_C2R_MINB;
   static constexpr int NT = RPB * TM;
   // X rows double-buffered (next term and the one after in flight) when that keeps RPB
   static constexpr int NXB = (FW_C2R_XB2 || H == 128) && (size_t)TWN * sizeof(double2) + (size_t)RPB * (ROWB + XS * sizeof(double2)) <= CAP ? 2 : 1;
@@ -598,6 +608,9 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
 #ifndef FW_LT_MINB512
 #define FW_LT_MINB512 2  // blocks per SM of the 256-thread 512-point all-terms inverse
 #endif
+#ifndef FW_LT_MINB256
+#define FW_LT_MINB256 0  // blocks per SM of the 256-point all-terms inverse (0: 512 / threads)
+#endif
 #ifndef FW_LT_PREFETCH
 #define FW_LT_PREFETCH 1  // next term's weights loaded during the current term's passes
 #endif
@@ -614,7 +627,7 @@ struct TermPlan {
 };
 
 template <int N, bool SCAT, int NTH>
-__global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 : 512 / NTH) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
+__global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 : (N == 256 && FW_LT_MINB256 > 0) ? FW_LT_MINB256 : 512 / NTH) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
                                                         const double* __restrict__ w, long long S, long long inner,
                                                         long long dst_ts, long long w_ts, int nterms, int tchunk,
                                                         double sc, int do_scale, const double2* __restrict__ master,
@@ -866,6 +879,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
 #ifndef FW_LINES_TERMS
 #define FW_LINES_TERMS 1  // 0: one block per (lines, term), uhat re-read per term
 #endif
+static_assert(FW_LINES_TERMS || !FW_TERM_PAD, "padded term scratch rows need the all-terms inverse (FW_LINES_TERMS=0: build with -DFW_TERM_PAD=0)");
 template <int N, int NTH>
 bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, const double* w, long long S,
               long long outer, long long inner, long long src_ts, long long dst_ts, long long w_ts, int nterms,
@@ -906,21 +920,22 @@ bool launch_nt(const LaunchCtx& L, int dir, const double2* src, double2* dst, co
     if (L.launches) *L.launches += 1;
     return true;
   }
+  if (Sd != S) return false;  // only the all-terms inverse writes a differently strided destination
   const dim3 grid((unsigned)(outer * bpo), (unsigned)nterms, (unsigned)nfields);
   if (dir < 0) {
     if (scatter)
       k_lines<N, -1, true, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
-                                                           bl, sc_, Sd);
+                                                           bl, sc_);
     else
       k_lines<N, -1, false, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
-                                                            L.master, bl, sc_, Sd);
+                                                            L.master, bl, sc_);
   } else {
     if (scatter)
       k_lines<N, +1, true, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f, L.master,
-                                                           bl, sc_, Sd);
+                                                           bl, sc_);
     else
       k_lines<N, +1, false, NTH><<<grid, Plan<N, NTH>::NTHR, SMEM, L.stream>>>(src, dst, w, S, inner, src_ts, dst_ts, w_ts, sc, f,
-                                                            L.master, bl, sc_, Sd);
+                                                            L.master, bl, sc_);
   }
   if (L.launches) *L.launches += 1;
   return true;
@@ -936,7 +951,7 @@ bool launch_n(const LaunchCtx& L, int dir, const double2* src, double2* dst, con
   const bool terms = dir > 0 && src_ts == 0 && nterms > 1 && (w || (bl && w_ts != 0));
   const bool wide = FW_LINES_WIDE && (N == 1024 || !terms || S * (long long)sizeof(double2) >= FW_WIDE_STRIDE);
   if constexpr (N == 256)
-    return launch_nt<N, 256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter, Sd);
+    return launch_nt<N, FW_LINES_NTH256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter, Sd);
   else
     return wide ? launch_nt<N, 512>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter, Sd) : launch_nt<N, 256>(L, dir, src, dst, w, S, outer, inner, src_ts, dst_ts, w_ts, nterms, nfields, sc, scale, bl, scatter, Sd);
 }
