@@ -305,6 +305,28 @@ __device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, do
   return make_double2(E.x - O.y, E.y + O.x);
 }
 
+// bulk copies (TMA engine) with mbarrier completion: the X rows of the row C2R
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n FW_LMBW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra FW_LMBW_%=;\n}" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
 // Per row of the last axis (NL reals, h = NL/2 complex, rows contiguous): for every
 // term m = m_first..m_last in ascending order, C2R of the half-spectrum row src_m
 // (flap.cpp:21-36: pre-processing Z_q = f(X_q, X_{h-q}), h-point C2C, real parts
@@ -335,6 +357,9 @@ __device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, do
 #endif
 #ifndef FW_C2R_MINB128
 #define FW_C2R_MINB128 3  // the same for the h = 128 row C2R (8-row blocks of 128 threads)
+#endif
+#ifndef FW_C2R_BULK
+#define FW_C2R_BULK 1  // X rows by one bulk copy per row (TMA engine, mbarrier per warp) when a row's threads share a warp (0: 16-B cp.async per thread; A/B)
 #endif
 #ifndef FW_C2R_WSYNC
 #define FW_C2R_WSYNC 1  // warp barriers between the passes when a row's threads share a warp (0: block barriers, A/B)
@@ -418,9 +443,30 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
   double2* Wk = twpre + RP::TWN + rl * RP::LS;  // FFT work (in-place layout)
 
   const double* d1row = dev1 ? dev1 + (live ? row : 0) * NL : nullptr;
-  // X rows arrive by cp.async NXB terms ahead: a buffer is refilled as soon as pass 0 of its
-  // term has read it, and lands during the following terms' passes (one commit group per term)
+  // X rows arrive NXB terms ahead: a buffer is refilled as soon as pass 0 of its term has read it,
+  // and lands during the following terms' passes.  When a row's threads share a warp, lane 0 of the
+  // warp issues ONE bulk copy per row of the warp (the TMA engine writes the row into shared
+  // memory; 16-B cp.async per thread cost three times the shared-memory wavefronts of the row)
+  // and the warp waits on its own mbarrier; otherwise 16-B cp.async, one commit group per term.
+  // (h = 128: the 2-KB rows measured 2 % slower by bulk copy at C3, 1.7 % faster at h = 256, C5)
+  constexpr bool BULK = FW_C2R_BULK && FW_C2R_WSYNC && 32 % TM == 0 && H >= 256;
+  __shared__ __align__(8) unsigned long long xbar[BULK ? NT / 32 : 1][2];
   auto fetch = [&](int m) {
+    if constexpr (BULK) {
+      if ((tid & 31) == 0) {
+        constexpr int RPW = 32 / TM;  // rows per warp
+        const long long row0 = (long long)blockIdx.x * RPB + (tid / 32) * RPW;
+        const int b = (m - m_first) % NXB;
+        int nlive = 0;
+        for (int r = 0; r < RPW; ++r) nlive += (row0 + r < rows && m <= m_last) ? 1 : 0;
+        mbar_expect_tx(&xbar[tid / 32][b], (unsigned)(nlive * (H + 1) * sizeof(double2)));
+        for (int r = 0; r < nlive; ++r)
+          bulk_g2s(sm + ((tid / 32) * RPW + r) * RP::XS + b * RPB * RP::XS,
+                   src + (long long)(m - m_first) * src_ts + (row0 + r) * xrs, (unsigned)((H + 1) * sizeof(double2)),
+                   &xbar[tid / 32][b]);
+      }
+      return;
+    }
     if (live && m <= m_last) {
       const double2* S = src + (long long)(m - m_first) * src_ts + row * xrs;
       double2* X = Xb + ((m - m_first) % NXB) * RPB * RP::XS;
@@ -431,6 +477,15 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  if constexpr (BULK) {
+    if ((tid & 31) == 0) {
+      mbar_init(&xbar[tid / 32][0], 1);
+      mbar_init(&xbar[tid / 32][1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+  }
   fetch(m_first);
   if (NXB > 1) fetch(m_first + 1);
 
@@ -512,7 +567,9 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
   }
   double rmax = 0.0;
   for (int m = m_first; m <= m_last; ++m) {
-    if (NXB > 1)
+    if constexpr (BULK)
+      mbar_wait(&xbar[tid / 32][(m - m_first) % NXB], (unsigned)((m - m_first) / NXB) & 1u);
+    else if (NXB > 1)
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // term m landed (m + 1 may be in flight)
     else
       asm volatile("cp.async.wait_all;" ::: "memory");
@@ -608,6 +665,9 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
 #ifndef FW_LT_MINB512
 #define FW_LT_MINB512 2  // blocks per SM of the 256-thread 512-point all-terms inverse
 #endif
+#ifndef FW_LT_DBUF
+#define FW_LT_DBUF 0  // 1: double-buffered lines in the 512-point all-terms inverse (measured 1 % slower at C5; A/B)
+#endif
 #ifndef FW_LT_MINB256
 #define FW_LT_MINB256 0  // blocks per SM of the 256-point all-terms inverse (0: 512 / threads)
 #endif
@@ -620,7 +680,10 @@ struct TermPlan {
   static constexpr int TW1 = P::P > 2 ? P::R0 * (P::R1 - 1) : 0;  // pass-1 twiddles of a 3-pass plan
   static constexpr int TWL = pprod(N, P::P - 1) * (radix(N, P::P - 1) - 1);  // last pass
   static constexpr int TWN = TW1 + TWL;
-  static constexpr size_t SMEM = (size_t)(TWN + P::L * P::LLS) * sizeof(double2);
+  // line buffers: two at N = 512 (term t + 1's pass 0 fills the other one while slower warps
+  // still read term t's last pass: one block barrier per term fewer), one otherwise (shared memory)
+  static constexpr int NBUF = (FW_LT_DBUF && N == 512) ? 2 : 1;
+  static constexpr size_t SMEM = (size_t)(TWN + NBUF * P::L * P::LLS) * sizeof(double2);
   static constexpr int TMC = 4 * P::R0;  // columns per warp: R0 complex pass-0 inputs
   static constexpr int NSLOT = P::NTHR / 128;  // warps per TMEM lane quadrant
   static constexpr int TMALLOC = pow2ceil(NSLOT * TMC < 32 ? 32 : NSLOT * TMC);
@@ -658,7 +721,7 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
   const bool live = in0 + l < inner;
   const long long base = o * (long long)N * S + in0 + l;
   const long long dbase = o * (long long)N * Sd + in0 + l;  // destination (Sd != S: padded rows, inner < S)
-  double2* line = lines_sm;  // slot p of this thread's line at PL::lpos(l, p)
+  double2* line = lines_sm;  // slot p of this thread's line at PL::lpos(l, p)  (buffer term % NBUF)
 
   if constexpr (PL::P > 2) {
     for (int e = tid; e < TP::TW1; e += PL::NTHR) {
@@ -706,6 +769,7 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
     for (int r = 0; r < R0; ++r) wk[r] = live ? __ldg(&w[base + (long long)(i + r * T0) * S]) : 0.0;
   }
   for (int term = t0; term < t1; ++term) {
+    if constexpr (TP::NBUF > 1) line = lines_sm + ((term - t0) & 1) * (L * PL::LLS);
     if (p0) {  // pass 0: w_m .* uhat (no twiddles)
       if (!FW_LT_PREFETCH && term > t0) {
         const double* wn = w + (long long)(term - t0) * w_ts;
@@ -777,7 +841,9 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
         }
       }
     }
-    __syncthreads();  // the line buffer takes the next term's pass 0
+    // the line buffer takes the next term's pass 0 (with two buffers the barriers of the next
+    // term order its reuse the term after)
+    if constexpr (TP::NBUF == 1) __syncthreads();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -820,6 +886,13 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
   const long long row = (long long)blockIdx.x * RPB + rl;
   const bool live = row < rows;
   double2* Wk = sm + rl * XP::LS;  // FFT work, then the natural-order result
+  // a row's threads exchange data only among themselves: a warp barrier when they share a warp
+  auto rowsync = [] {
+    if constexpr (FW_C2R_WSYNC && 32 % TM == 0)
+      __syncwarp();
+    else
+      __syncthreads();
+  };
   const double2* z = reinterpret_cast<const double2*>(u) + row * H;
   {  // pass 0 straight from global
     constexpr int R = PL::R0, T = PL::T0;
@@ -832,7 +905,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
       for (int r = 0; r < R; ++r) Wk[XP::p0out(i * R + r)] = a[r];
     }
   }
-  __syncthreads();
+  rowsync();
   if constexpr (PL::P == 3) {
     constexpr int R = PL::R1, T = PL::T1;
     if (i < T) {
@@ -843,7 +916,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
 #pragma unroll
       for (int r = 0; r < R; ++r) Wk[XP::p1(i, r)] = a[r];
     }
-    __syncthreads();
+    rowsync();
   }
   {
     constexpr int LAST = PL::P - 1;
@@ -853,13 +926,13 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
       for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? XP::p1(i, r) : XP::p2in(i + r * TL)];
       bfly<H, LAST, -1>(a, i, master);
     }
-    __syncthreads();  // every read of the work layout is done: store the natural-order result
+    rowsync();  // every read of the work layout is done: store the natural-order result
     if (i < TL) {
 #pragma unroll
       for (int r = 0; r < RL; ++r) Wk[i + r * TL] = a[r];
     }
   }
-  __syncthreads();
+  rowsync();
   if (live) {
     double2* X = Uh + row * (H + 1);
     for (int k = i; k <= H; k += TM) {
