@@ -358,6 +358,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 #ifndef FW_C2R_MINB128
 #define FW_C2R_MINB128 3  // the same for the h = 128 row C2R (8-row blocks of 128 threads)
 #endif
+#ifndef FW_C2R_TM8
+#define FW_C2R_TM8 1  // h = 128 row C2R with 8 threads per row (0: 16; A/B)
+#endif
 #ifndef FW_C2R_BULK
 #define FW_C2R_BULK 1  // X rows by one bulk copy per row (TMA engine, mbarrier per warp) when a row's threads share a warp (0: 16-B cp.async per thread; A/B)
 #endif
@@ -367,9 +370,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 template <int H>
 struct C2RPlan {
   using P = Plan<H>;
-  static constexpr int TM = P::TMAX;                 // threads per row
   static constexpr int RL = radix(H, P::P - 1);      // last-pass radix
   static constexpr int TL = H / RL;
+  // threads per row.  h = 128 (radix 16 then 8: 8 butterflies in pass 0, 16 in the last pass):
+  // 8 threads per row, each with BOTH last-pass butterflies i and i + 8 -- with 16 threads the
+  // pre-processing and pass 0 (two thirds of the row's fp64 work) ran on half the lanes
+  static constexpr int TM = (H == 128 && FW_C2R_TM8) ? 8 : P::TMAX;
+  static constexpr int NB = TL / TM;                 // last-pass butterflies per thread
   // X row stride (natural order, odd; 128-B aligned rows measured 1-3 % slower)
   static constexpr int XS = (H + 1) | 1;
   // twiddles: pre-processing W_{2H}^k (k <= H), pass 1 [k < R0][R1 - 1], pass 2 [k < R0 R1][R2 - 1]
@@ -403,12 +410,13 @@ struct C2RPlan {
   // X rows double-buffered (next term and the one after in flight) when that keeps RPB
   static constexpr int NXB = (FW_C2R_XB2 || H == 128) && (size_t)TWN * sizeof(double2) + (size_t)RPB * (ROWB + XS * sizeof(double2)) <= CAP ? 2 : 1;
   static constexpr size_t SMEM = (size_t)TWN * sizeof(double2) + (size_t)RPB * (ROWB + (NXB - 1) * XS * sizeof(double2));
-  // tensor memory per warp: (s-s0) at [0, 4 RL), (s-s0)^{m-1} at [4 RL, 8 RL) (two columns per double)
-  static constexpr int TMC = 8 * RL;
+  // tensor memory per warp and last-pass butterfly: (s-s0) at [0, 4 RL), (s-s0)^{m-1} at [4 RL, 8 RL)
+  // (two columns per double)
+  static constexpr int TMC = 8 * RL * NB;
   static constexpr int NSLOT = (NT / 32 + 3) / 4;
   static constexpr int TMALLOC = pow2ceil(NSLOT * TMC < 32 ? 32 : NSLOT * TMC);
   static_assert(RPB >= 1 && NT % 32 == 0, "whole warps");
-  static_assert(TL == TM, "every thread owns RL outputs");
+  static_assert(TL == TM * NB && (NB == 1 || P::P == 2), "every thread owns NB RL outputs");
   static_assert(RL % 4 == 0, "16-column chunks");
   static_assert(TMALLOC <= 256, "two blocks per SM in tensor memory");
 };
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
                                                             const BatchLine* __restrict__ bl, long long xrs, int resume) {
   using RP = C2RPlan<H>;
   using PL = Plan<H>;
-  constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL, NL = 2 * H, NT = RP::NT;
+  constexpr int TM = RP::TM, RPB = RP::RPB, RL = RP::RL, TL = RP::TL, NL = 2 * H, NT = RP::NT, NB = RP::NB;
   if (guard && *guard != kNoBlowup) return;
   if (bl) {
     src = static_cast<const double2*>(bl[blockIdx.z].src);
@@ -514,32 +522,36 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int warp = tid >> 5;
+  // butterfly bb of the last pass (index i + bb TM): (s-s0) at tdev + bb 8 RL, the running power 4 RL further
   const unsigned tdev = tbase_sh + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * RP::TMC);
   const unsigned tpow = tdev + 4 * RL;
   if (d1row) {  // (s-s0) of this thread's outputs -> tensor memory, once
 #pragma unroll
-    for (int c4 = 0; c4 < RL / 4; ++c4) {
-      unsigned v[16];
+    for (int bb = 0; bb < NB; ++bb) {
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        const int q = i + (4 * c4 + rr) * TL;
-        const double2 d = live ? __ldg(reinterpret_cast<const double2*>(d1row) + q) : make_double2(0.0, 0.0);
-        tm_set(v, 2 * rr, d.x);
-        tm_set(v, 2 * rr + 1, d.y);
-      }
-      tm_st16(tdev + 16 * c4, v);
-      if (resume && m_first > 1) {
-        // a later chunk of the operator's terms: the running power (s-s0)^{m_first-1} by the same
-        // recurrence the earlier chunks ran, (s-s0)^m = (s-s0)^{m-1} (s-s0) (flap.cpp:131)
-        unsigned pw[16];
+      for (int c4 = 0; c4 < RL / 4; ++c4) {
+        unsigned v[16];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const double d1 = tm_get(v, e);
-          double d = d1;
-          for (int m = 2; m < m_first; ++m) d = d * d1;
-          tm_set(pw, e, d);
+        for (int rr = 0; rr < 4; ++rr) {
+          const int q = i + bb * TM + (4 * c4 + rr) * TL;
+          const double2 d = live ? __ldg(reinterpret_cast<const double2*>(d1row) + q) : make_double2(0.0, 0.0);
+          tm_set(v, 2 * rr, d.x);
+          tm_set(v, 2 * rr + 1, d.y);
         }
-        tm_st16(tpow + 16 * c4, pw);
+        tm_st16(tdev + bb * 8 * RL + 16 * c4, v);
+        if (resume && m_first > 1) {
+          // a later chunk of the operator's terms: the running power (s-s0)^{m_first-1} by the same
+          // recurrence the earlier chunks ran, (s-s0)^m = (s-s0)^{m-1} (s-s0) (flap.cpp:131)
+          unsigned pw[16];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const double d1 = tm_get(v, e);
+            double d = d1;
+            for (int m = 2; m < m_first; ++m) d = d * d1;
+            tm_set(pw, e, d);
+          }
+          tm_st16(tpow + bb * 8 * RL + 16 * c4, pw);
+        }
       }
     }
     tm_wait_st();
@@ -554,16 +566,20 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
     else
       __syncthreads();
   };
-  double acc[2 * RL];
+  double acc[NB][2 * RL];
 #pragma unroll
-  for (int e = 0; e < 2 * RL; ++e) acc[e] = 0.0;
+  for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+    for (int e = 0; e < 2 * RL; ++e) acc[bb][e] = 0.0;
   if (resume && live) {  // partial sums of the operator's earlier terms (written by the previous chunk's launch)
 #pragma unroll
-    for (int r = 0; r < RL; ++r) {
-      const double2 o = reinterpret_cast<const double2*>(out + row * NL)[i + r * TL];
-      acc[2 * r] = o.x;
-      acc[2 * r + 1] = o.y;
-    }
+    for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const double2 o = reinterpret_cast<const double2*>(out + row * NL)[i + bb * TM + r * TL];
+        acc[bb][2 * r] = o.x;
+        acc[bb][2 * r + 1] = o.y;
+      }
   }
   double rmax = 0.0;
   for (int m = m_first; m <= m_last; ++m) {
@@ -604,24 +620,26 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
       }
       rowsync();
     }
-    {  // last pass -> outputs z_q, q = i + r TL: reals x[2q], x[2q+1]
+#pragma unroll
+    for (int bb = 0; bb < NB; ++bb) {  // last pass -> outputs z_q, q = ib + r TL: reals x[2q], x[2q+1]
       constexpr int LAST = PL::P - 1;
+      const int ib = i + bb * TM;
       double2 a[RL];
 #pragma unroll
-      for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? RP::p1(i, r) : RP::p2in(i + r * TL)];
-      bfly_s<H, LAST, +1>(a, i, LAST == 1 ? tw1 : tw2);
+      for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? RP::p1(ib, r) : RP::p2in(ib + r * TL)];
+      bfly_s<H, LAST, +1>(a, ib, LAST == 1 ? tw1 : tw2);
       if (m == 0 || !d1row) {
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
-          acc[2 * r] += zero_plus(a[r].x);
-          acc[2 * r + 1] += zero_plus(a[r].y);
+          acc[bb][2 * r] += zero_plus(a[r].x);
+          acc[bb][2 * r + 1] += zero_plus(a[r].y);
         }
       } else {
 #pragma unroll
         for (int c4 = 0; c4 < RL / 4; ++c4) {
           unsigned dv[16], pv[16];
-          tm_ld16(tdev + 16 * c4, dv);
-          if (m > 1) tm_ld16(tpow + 16 * c4, pv);
+          tm_ld16(tdev + bb * 8 * RL + 16 * c4, dv);
+          if (m > 1) tm_ld16(tpow + bb * 8 * RL + 16 * c4, pv);
           tm_wait_ld();
 #pragma unroll
           for (int e = 0; e < 8; ++e) {  // element e of the chunk: output r = 4 c4 + e / 2, real part e % 2
@@ -630,9 +648,9 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
             double d = tm_get(dv, e);
             if (m > 1) d = tm_get(pv, e) * d;  // (s-s0)^m = (s-s0)^{m-1} (s-s0)
             tm_set(pv, e, d);
-            acc[2 * r + (e & 1)] += zero_plus(d * x);
+            acc[bb][2 * r + (e & 1)] += zero_plus(d * x);
           }
-          tm_st16(tpow + 16 * c4, pv);
+          tm_st16(tpow + bb * 8 * RL + 16 * c4, pv);
         }
         tm_wait_st();
       }
@@ -640,10 +658,12 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
   }
   if (live) {
 #pragma unroll
-    for (int r = 0; r < RL; ++r) {
-      const int q = i + r * TL;
-      reinterpret_cast<double2*>(out + row * NL)[q] = make_double2(acc[2 * r], acc[2 * r + 1]);
-    }
+    for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const int q = i + bb * TM + r * TL;
+        reinterpret_cast<double2*>(out + row * NL)[q] = make_double2(acc[bb][2 * r], acc[bb][2 * r + 1]);
+      }
   }
   if (residue && live && i == 0 && rmax > 0.0)
     atomicMax(reinterpret_cast<unsigned long long*>(residue), (unsigned long long)__double_as_longlong(rmax));
