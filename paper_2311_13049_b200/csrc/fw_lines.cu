@@ -688,6 +688,9 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
 #ifndef FW_LT_DBUF
 #define FW_LT_DBUF 0  // 1: double-buffered lines in the 512-point all-terms inverse (measured 1 % slower at C5; A/B)
 #endif
+#ifndef FW_LT_MINB512W
+#define FW_LT_MINB512W 1  // blocks per SM of the 512-thread 512-point all-terms inverse
+#endif
 #ifndef FW_LT_MINB256
 #define FW_LT_MINB256 0  // blocks per SM of the 256-point all-terms inverse (0: 512 / threads)
 #endif
@@ -710,7 +713,7 @@ struct TermPlan {
 };
 
 template <int N, bool SCAT, int NTH>
-__global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 : (N == 256 && FW_LT_MINB256 > 0) ? FW_LT_MINB256 : 512 / NTH) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
+__global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 : (N == 512 && NTH == 512) ? FW_LT_MINB512W : (N == 256 && FW_LT_MINB256 > 0) ? FW_LT_MINB256 : 512 / NTH) k_lines_terms(const double2* __restrict__ src, double2* __restrict__ dst,
                                                         const double* __restrict__ w, long long S, long long inner,
                                                         long long dst_ts, long long w_ts, int nterms, int tchunk,
                                                         double sc, int do_scale, const double2* __restrict__ master,
