@@ -17,9 +17,12 @@
 // (per row of the last axis; the C2R keeps (s-s0) and (s-s0)^{m-1} in tensor memory and
 // recombines the terms in registers).  Shared-memory layouts are bank-conflict-free for each
 // kernel's thread mapping (tools/layouts/).  Build switches (-D..., A/B only; defaults are the
-// measured best): FW_LINES_TERMS, FW_LT_PREFETCH, FW_LT_TARGET, FW_LINES_SWZ,
-// FW_LINES_WIDE, FW_WIDE_STRIDE, FW_LINES_MINB{256,512,1024}, FW_C2R_PAD, FW_C2R_XB2,
-// FW_C2R_RPB128, FW_C2R_MINB.
+// measured best): FW_LINES_TERMS, FW_LT_PREFETCH, FW_LT_TARGET, FW_LT_DBUF,
+// FW_LT_MINB{256,512,512W}, FW_LINES_SWZ, FW_LINES_WIDE, FW_WIDE_STRIDE, FW_LINES_NTH256,
+// FW_LINES_MINB{256,512,1024}, FW_C2R_PAD, FW_C2R_XB2, FW_C2R_RPB{128,256}, FW_C2R_MINB{,128,256},
+// FW_C2R_WSYNC, FW_C2R_BULK, FW_C2R_TM8, FW_ZERO_PLUS (and FW_TERM_PAD in fw_internal.h).
+// Block shapes are chosen spill-free: every kernel here compiles with a zero stack frame except
+// the 256-point all-terms inverse (24 B).
 #include <cuda_runtime.h>
 
 #include <algorithm>
