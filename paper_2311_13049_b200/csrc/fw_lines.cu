@@ -295,6 +295,20 @@ __device__ __forceinline__ void bfly_s(double2* a, int i, const double2* tw) {
   Dft<R, DIR>::run(a);
 }
 
+// R2C post-processing (r2c_post) with the master entry of W_{2h}^k given (conjugated here as twiddle<-1> does)
+__device__ __forceinline__ double2 r2c_post_w(const double2* Z, int k, int h, double2 wm) {
+  if (k == 0) return make_double2(Z[0].x + Z[0].y, 0.0);
+  if (k == h) return make_double2(Z[0].x - Z[0].y, 0.0);
+  const double2 A = Z[k];
+  const double2 Bz = Z[h - k];
+  const double2 B = make_double2(Bz.x, -Bz.y);
+  const double2 E = make_double2((A.x + B.x) * 0.5, (A.y + B.y) * 0.5);
+  const double2 D = make_double2((A.x - B.x) * 0.5, (A.y - B.y) * 0.5);
+  const double2 O = make_double2(D.y, -D.x);
+  const double2 t = cmulw(O, wm.x, -wm.y);
+  return make_double2(E.x + t.x, E.y + t.y);
+}
+
 // C2R pre-processing (c2r_pre) with W_{2h}^k given
 __device__ __forceinline__ double2 c2r_pre_w(double2 A, double2 Xhk, bool k0, double2 w) {
   double2 B = make_double2(Xhk.x, -Xhk.y);
@@ -911,7 +925,26 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
   const int rl = threadIdx.x / TM, i = threadIdx.x % TM;
   const long long row = (long long)blockIdx.x * RPB + rl;
   const bool live = row < rows;
-  double2* Wk = sm + rl * XP::LS;  // FFT work, then the natural-order result
+  // [twiddles: post-processing W_{2H}^k (k <= H), pass 1, pass 2 -- the row C2R's table][work: RPB x LS]
+  // (values = the master entries; one table per block instead of scattered master reads per thread)
+  double2* twpre = sm;
+  double2* tw1 = twpre + (H + 1);
+  double2* tw2 = tw1 + XP::TW1;
+  for (int e = threadIdx.x; e <= H; e += RP::NT) twpre[e] = master[e * (kTwMaster / (2 * H))];
+  for (int e = threadIdx.x; e < XP::TW1; e += RP::NT) {
+    constexpr int R = PL::R1, p = PL::R0;
+    const int k = e / (R - 1), r = e % (R - 1) + 1;
+    tw1[e] = master[(r * k) * (kTwMaster / (p * R))];
+  }
+  if constexpr (PL::P > 2) {
+    for (int e = threadIdx.x; e < XP::TW2; e += RP::NT) {
+      constexpr int R = PL::R2, p = PL::R0 * PL::R1;
+      const int k = e / (R - 1), r = e % (R - 1) + 1;
+      tw2[e] = master[(r * k) * (kTwMaster / (p * R))];
+    }
+  }
+  __syncthreads();
+  double2* Wk = sm + XP::TWN + rl * XP::LS;  // FFT work, then the natural-order result
   // a row's threads exchange data only among themselves: a warp barrier when they share a warp
   auto rowsync = [] {
     if constexpr (FW_C2R_WSYNC && 32 % TM == 0)
@@ -938,7 +971,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
       double2 a[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) a[r] = Wk[XP::p1(i, r)];
-      bfly<H, 1, -1>(a, i, master);
+      bfly_s<H, 1, -1>(a, i, tw1);
 #pragma unroll
       for (int r = 0; r < R; ++r) Wk[XP::p1(i, r)] = a[r];
     }
@@ -950,7 +983,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
     if (i < TL) {
 #pragma unroll
       for (int r = 0; r < RL; ++r) a[r] = Wk[LAST == 1 ? XP::p1(i, r) : XP::p2in(i + r * TL)];
-      bfly<H, LAST, -1>(a, i, master);
+      bfly_s<H, LAST, -1>(a, i, LAST == 1 ? tw1 : tw2);
     }
     rowsync();  // every read of the work layout is done: store the natural-order result
     if (i < TL) {
@@ -962,7 +995,7 @@ __global__ void __launch_bounds__(256) k_rows_r2c(const double* __restrict__ u, 
   if (live) {
     double2* X = Uh + row * (H + 1);
     for (int k = i; k <= H; k += TM) {
-      double2 v = r2c_post(Wk, k, H, master);
+      double2 v = r2c_post_w(Wk, k, H, twpre[k]);
       if (do_scale) {
         v.x *= sc;
         v.y *= sc;
@@ -1059,7 +1092,7 @@ template <int H>
 bool launch_rows_r2c_t(const LaunchCtx& L, const double* u, double2* Uh, long long rows, int nfields, double sc,
                        bool scale, const BatchLine* bl) {
   using RP = RowPlan<H>;
-  constexpr size_t SMEM = (size_t)RP::RPB * C2RPlan<H>::LS * sizeof(double2);
+  constexpr size_t SMEM = (size_t)(C2RPlan<H>::TWN + RP::RPB * C2RPlan<H>::LS) * sizeof(double2);
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [] {
     cudaFuncSetAttribute(k_rows_r2c<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
