@@ -479,7 +479,7 @@ def lines_context():
 
 
 @pytest.mark.parametrize("J", [(256, 16, 8), (512, 8, 8), (1024, 4, 8), (16, 256, 8), (8, 512, 4), (256, 64),
-                               (1024, 32), (512, 512)])
+                               (1024, 32), (512, 512), (4, 256), (4, 512), (12, 256), (4, 4, 512)])
 def test_register_line_ffts_equal_shared_memory_path(J):
     """fw_lines.cu (register-resident line FFTs for n in {256, 512, 1024}) against the
     shared-memory line kernels: identical bits, both directions (forward + inverse)."""
