@@ -705,6 +705,9 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
 #ifndef FW_LT_DBUF
 #define FW_LT_DBUF 0  // 1: double-buffered lines in the 512-point all-terms inverse (measured 1 % slower at C5; A/B)
 #endif
+#ifndef FW_LT_LD1
+#define FW_LT_LD1 1
+#endif
 #ifndef FW_LT_MINB512W
 #define FW_LT_MINB512W 1  // blocks per SM of the 512-thread 512-point all-terms inverse
 #endif
@@ -817,6 +820,15 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
         for (int r = 0; r < R0; ++r) wk[r] = live ? __ldg(&wn[base + (long long)(i + r * T0) * S]) : 0.0;
       }
       double2 a[R0];
+      if constexpr (FW_LT_LD1 && R0 == 8) {  // both tensor-memory loads in flight, one wait
+        unsigned v[32];
+        tm_ld16(tu, v);
+        tm_ld16(tu + 16, v + 16);
+        tm_wait_ld();
+#pragma unroll
+        for (int r = 0; r < R0; ++r)
+          a[r] = live ? make_double2(wk[r] * tm_get(v, 2 * r), wk[r] * tm_get(v, 2 * r + 1)) : make_double2(0.0, 0.0);
+      } else {
 #pragma unroll
       for (int c = 0; c < R0 / 4; ++c) {
         unsigned v[16];
@@ -827,6 +839,7 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
           const int r = 4 * c + rr;
           a[r] = live ? make_double2(wk[r] * tm_get(v, 2 * rr), wk[r] * tm_get(v, 2 * rr + 1)) : make_double2(0.0, 0.0);
         }
+      }
       }
       if (FW_LT_PREFETCH && term + 1 < t1) {
         const double* wn = w + (long long)(term + 1 - t0) * w_ts;
