@@ -705,6 +705,9 @@ __global__ void __launch_bounds__(C2RPlan<H>::NT, C2RPlan<H>::MINB) k_rows_c2r(c
 #ifndef FW_LT_DBUF
 #define FW_LT_DBUF 0  // 1: double-buffered lines in the 512-point all-terms inverse (measured 1 % slower at C5; A/B)
 #endif
+#ifndef FW_LT_LD2
+#define FW_LT_LD2 1
+#endif
 #ifndef FW_LT_LD1
 #define FW_LT_LD1 1
 #endif
@@ -828,6 +831,19 @@ __global__ void __launch_bounds__(NTH, (N == 512 && NTH == 256) ? FW_LT_MINB512 
 #pragma unroll
         for (int r = 0; r < R0; ++r)
           a[r] = live ? make_double2(wk[r] * tm_get(v, 2 * r), wk[r] * tm_get(v, 2 * r + 1)) : make_double2(0.0, 0.0);
+      } else if constexpr (FW_LT_LD2 && R0 == 16) {  // two loads in flight per wait
+#pragma unroll
+        for (int c = 0; c < R0 / 8; ++c) {
+          unsigned v[32];
+          tm_ld16(tu + 32 * c, v);
+          tm_ld16(tu + 32 * c + 16, v + 16);
+          tm_wait_ld();
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            const int r = 8 * c + rr;
+            a[r] = live ? make_double2(wk[r] * tm_get(v, 2 * rr), wk[r] * tm_get(v, 2 * rr + 1)) : make_double2(0.0, 0.0);
+          }
+        }
       } else {
 #pragma unroll
       for (int c = 0; c < R0 / 4; ++c) {
